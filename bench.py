@@ -1,0 +1,306 @@
+#!/usr/bin/env python3
+"""Benchmark: env-steps/s of Humanoid random-action rollouts, 4096 envs per GPU.
+
+Metric (BASELINE.json): "env-steps/sec (Humanoid, 4096 envs/GPU) at 1/2/4/8
+B200; % of HBM/FP32 roofline".  One *step* = one env_step of all 4096
+environments of this rank (actuation, contacts, 4 x Newton/PCR solve,
+integration, reward, termination, auto-reset, observation) = one launch of
+the fused sm_100a kernel.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: K steps, each bracketed by CUDA events on the launching stream with
+an L2 flush (a 256 MiB write, outside the events) between steps; a barrier +
+synchronize brackets the whole timed loop; the per-rank device time is the
+sum of the K event intervals; the job time is the MAX over ranks.  `value` is
+total env-steps of all ranks / that time.  `e2e` repeats the measurement
+through the host-buffer C-ABI call stp_step_host (pinned H2D actions, kernel,
+D2H obs/reward/done, synchronise) and is timed on the host clock.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ENVS = 4096
+TASK = "humanoid"
+SEED = 1234
+
+# Algorithmic work of the reference algorithm per Humanoid env-step (FP32
+# roofline numerator): 0.93 MFLOP measured with a
+# counting-scalar build of the unmodified reference on a 22-body / 21-hinge
+# humanoid under random actions; one 16-iteration PCR solve = 179,114 FLOP.
+# The PCR share is rescaled by the live Krylov iteration count the kernel
+# reports.
+F_ENV_STEP = 929_813.0
+F_PCR_SOLVE16 = 179_114.0
+F_PCR_ITER = F_PCR_SOLVE16 / 16.0
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rate(n_envs: int, steps: int, warmup: int, threads: int, budget_s: float = 20.0):
+    """Reference stampede::physics::step + restated env layer on host cores.
+
+    Runs oracle/_ref (the compiled reference, its Release flags) when it was
+    built, else the restated oracle port.  Bounded sample: the env count is
+    cut so the timed part stays within ~budget_s.
+    """
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    from oracle import OracleEnv, available
+    from paper_1810_05762_b200 import abi
+    kind = "reference_fast" if available("reference_fast") else "restatement"
+    model = abi.builtin_model("humanoid")
+    task = abi.default_task(abi.TASK_HUMANOID)
+    cfg = abi.default_step_config()
+    # calibrate on a small batch, then size the sample
+    probe_n = min(n_envs, 256)
+    env = OracleEnv(model, task, cfg, probe_n, seed=SEED, nthreads=threads, kind=kind)
+    for s in range(2):
+        env.step(env.random_actions(s))
+    t0 = time.perf_counter()
+    env.step(env.random_actions(2))
+    rate = probe_n / max(time.perf_counter() - t0, 1e-6)
+    env.close()
+    per_step_budget = budget_s / max(1, steps)
+    n_sample = int(max(16, min(n_envs, rate * per_step_budget)))
+    env = OracleEnv(model, task, cfg, n_sample, seed=SEED, nthreads=threads, kind=kind)
+    acts = [env.random_actions(s) for s in range(warmup + steps)]
+    for s in range(warmup):
+        env.step(acts[s])
+    t0 = time.perf_counter()
+    for s in range(steps):
+        env.step(acts[warmup + s])
+    dt = time.perf_counter() - t0
+    env.close()
+    value = n_sample * steps / dt
+    return {"value": value, "unit": "env-steps/s", "cores": threads,
+            "kind": "reference" if kind.startswith("reference") else "port",
+            "sample": f"{n_sample} of {n_envs} Humanoid envs x {steps} env_steps (random actions, auto-reset), "
+                      f"{'oracle/_ref/libstampede_ref_fast.so: unmodified stampede::physics::step, -O3 -march=native, util::ThreadPool' if kind.startswith('reference') else 'oracle/liboracle.so restatement'}"
+                      f" + restated env layer"}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    r = cpu_reference_rate(N_ENVS, max(1, args.steps), max(0, args.warmup), threads, budget_s=90.0)
+    line = {"metric": "env-steps/sec (Humanoid, 4096 envs/GPU)", "value": r["value"], "unit": "env-steps/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "humanoid_run_flat_4096envs_random_actions", "envs_per_gpu": N_ENVS,
+                       "task": TASK, "parallelism": "cpu-threads"},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_1810_05762_b200.sim import VecEnv
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    env = VecEnv(TASK, n_envs=N_ENVS, device=local, seed=SEED, env_offset=rank * N_ENVS)
+    K, Wm = args.steps, args.warmup
+    # synthetic inputs resident in HBM before timing: one action batch per step
+    acts = [env.random_actions(s) for s in range(Wm + K)]
+    obs = torch.empty((N_ENVS, env.obs_dim), device=dev)
+    rew = torch.empty((N_ENVS,), device=dev)
+    done = torch.empty((N_ENVS,), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    krylov = []
+    for s in range(Wm):
+        env.step(acts[s], obs, rew, done)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for s in range(K):
+        flush.fill_(float(s))
+        ev[s][0].record()
+        env.step(acts[Wm + s], obs, rew, done)
+        ev[s][1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    rep = env.report()
+    kry_mean = float(rep["krylov_iterations"].mean())
+    failed = int(rep["failed"].sum())
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    job_ms = float(t.item())
+    value = world * N_ENVS * K / (job_ms / 1e3)
+    ms_per_step = job_ms / K
+
+    # ---- e2e through the reference-facing C-ABI call with pinned host buffers
+    h_act = torch.empty((N_ENVS, env.action_dim), dtype=torch.float32, pin_memory=True)
+    h_obs = torch.empty((N_ENVS, env.obs_dim), dtype=torch.float32, pin_memory=True)
+    h_rew = torch.empty((N_ENVS,), dtype=torch.float32, pin_memory=True)
+    h_done = torch.empty((N_ENVS,), dtype=torch.uint8, pin_memory=True)
+    import numpy as np
+    host_acts = [acts[Wm + s].cpu() for s in range(min(K, 64))]
+    for s in range(min(Wm, 3)):
+        h_act.copy_(host_acts[s % len(host_acts)])
+        env.step_host(h_act.numpy(), h_obs.numpy(), h_rew.numpy(), h_done.numpy())
+    if world > 1:
+        torch.distributed.barrier()
+    e0 = time.perf_counter()
+    for s in range(K):
+        h_act.copy_(host_acts[s % len(host_acts)])
+        env.step_host(h_act.numpy(), h_obs.numpy(), h_rew.numpy(), h_done.numpy())
+    e2e_s = time.perf_counter() - e0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = world * N_ENVS * K / float(te.item())
+    h2d = N_ENVS * env.action_dim * 4
+    d2h = N_ENVS * (env.obs_dim * 4 + 4 + 1)
+
+    peaks, src = _peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
+    f_env = F_ENV_STEP - F_PCR_ITER * (64.0 - kry_mean)  # live Krylov count
+    achieved = N_ENVS * f_env / (ms_per_step / 1e3) / 1e12
+    roof = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp32_peak, "traffic": None,
+            "kernel": "k_env_step<float,32,2>",
+            "flop_per_env_step": f_env, "krylov_iters_per_env_step": kry_mean,
+            "peak_source": f"148 SM x 128 FP32 lanes x 2 x sm_max_mhz {sm_max:.0f} ({src})",
+            "hbm_gbs_achieved": N_ENVS * 2700 / (ms_per_step / 1e3) / 1e9,
+            "hbm_peak_gbs": float(peaks.get("hbm_gbs", 6650.0))}
+    if clocks.get("sm_mhz"):
+        roof["frac_at_measured_clock"] = achieved / (148 * 128 * 2 * clocks["sm_mhz"] * 1e6 / 1e12)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_rate(N_ENVS, 3, 1, os.cpu_count() or 1, budget_s=15.0)
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"unavailable: {ex!r}"}
+    if rank == 0:
+        line = {"metric": "env-steps/sec (Humanoid, 4096 envs/GPU)", "value": value, "unit": "env-steps/s",
+                "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "humanoid_run_flat_4096envs_random_actions", "envs_per_gpu": N_ENVS,
+                           "task": TASK, "parallelism": f"dp{world} (env shards, no collective)",
+                           "l2": "flushed between timed steps (256 MiB write)", "auto_reset": True},
+                "e2e": {"value": e2e_value, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "path": "stp_step_host (pinned host buffers)"},
+                "gpu_launches": K, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+                "wall_s_timed_region": wall, "failed_envs_last_step": failed}
+        print(json.dumps(line), flush=True)
+    env.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

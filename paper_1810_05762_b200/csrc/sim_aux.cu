@@ -1,0 +1,45 @@
+// Auxiliary device kernels of the C-ABI: bench random actions.
+#include <cuda_runtime.h>
+
+#include "stampede_sim.h"
+#include "stp_error.h"
+#include "stp_rng.h"
+
+struct stp_sim;
+
+namespace {
+
+// i.i.d. U[-1,1] actions keyed by derive_seed(seed, TAG_ACTION, env<<32|step)
+// (rng.hpp:35-37; SURVEY §8(d) synthetic inputs).
+__global__ void k_random_actions(float* out, int n, int J, uint64_t seed, long long env_offset, uint64_t step) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n * J) return;
+  const int e = int(i / J), j = int(i % J);
+  const uint64_t genv = uint64_t(env_offset + e);
+  const uint64_t s = stp_derive_seed(seed, STP_TAG_ACTION, (genv << 32) | uint32_t(step));
+  out[i] = 2.0f * stp_uniformf(s, uint32_t(j)) - 1.0f;
+}
+
+}  // namespace
+
+namespace stp {
+int sim_dims(const stp_sim* s, int* n, int* J, uint64_t* seed, long long* off, void** stream);
+}
+
+extern "C" int stp_random_actions(stp_sim* sim, float* actions, uint64_t step, void* stream) {
+  int n = 0, J = 0;
+  uint64_t seed = 0;
+  long long off = 0;
+  void* own = nullptr;
+  if (!sim || !actions || stp::sim_dims(sim, &n, &J, &seed, &off, &own) != STP_OK)
+    return stp::fail(STP_EINVAL, "stp_random_actions: bad arguments");
+  const long long total = (long long)n * J;
+  if (total == 0) return STP_OK;
+  const int threads = 256;
+  const int blocks = int((total + threads - 1) / threads);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream ? stream : own);
+  k_random_actions<<<blocks, threads, 0, st>>>(actions, n, J, seed, off, step);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_random_actions: ") + cudaGetErrorString(e));
+  return STP_OK;
+}

@@ -1,0 +1,153 @@
+// Device-side data structures and small-vector math of the B200 stepper.
+//
+// Layout decisions (DESIGN.md §"HBM layout"):
+//  * one environment = one segment of W lanes of a warp (W = 32 for the
+//    22-body Humanoid, 16 for the 9-body Ant, 8 for tiny test scenes);
+//    lane b of the segment owns body b;
+//  * body state is SoA per env: state[((e * 16) + field) * W + lane] so a
+//    segment reads each field with one coalesced transaction;
+//  * positions are stored relative to a per-env origin (double xy) that is
+//    re-centred on the root every step, so fp32 keeps ~1e-7 m resolution
+//    anywhere in a 200 m env grid (the reference is double everywhere).
+#pragma once
+
+#include <stdint.h>
+
+#include "stampede_sim.h"
+
+namespace stp {
+
+constexpr int kStateFields = 16;  // 13 used: x3 q4 v3 w3 (+3 pad)
+constexpr int kTaskCounters = 8;
+
+// Per-body / per-joint model constants, indexed by body lane.  The joint
+// fields describe the hinge whose child is that body (tree: at most one).
+template <class T>
+struct DevModel {
+  int nb, nj, root, feet_mask, n_feet;
+  int feet[STP_MAX_FEET];
+  int shape[32], is_static[32], parent[32], joint[32], child_mask[32], depth[32], quirk[32];
+  int max_depth;
+  int lane_of_joint[STP_MAX_JOINTS];
+  T radius[32], half_len[32], hext[3][32], lpos[3][32], lrot[4][32];
+  T mass[32], inv_mass[32], inertia[3][32], inv_inertia[3][32];
+  T anc_p[3][32], anc_c[3][32], ax_p[3][32], ax_c[3][32], rest[4][32];
+  T lim_lo[32], lim_hi[32], tmax[32];
+  T rest_state[13][32];
+  T fall_height, alive_bonus;
+};
+
+// Scalar physics parameters (StepConfig, types.hpp:92-107).
+template <class T>
+struct DevCfg {
+  T dt, tol, margin, beta, kj, kc, kl, epsf, lim_act;
+  T gx, gy, gz;
+  int newton, kmax, plane;
+};
+
+struct DevTask {
+  int kind, episode_cap, fall_grace, target_refresh;
+  double target_radius, target_tolerance, spacing;
+  int perturb_min, perturb_max;
+  double force_lo, force_hi, reset_noise;
+  int auto_reset, height_map;
+};
+
+// ---------------------------------------------------------------------------
+// small vector math (restating vec.hpp:21-190 for device use)
+// ---------------------------------------------------------------------------
+template <class T>
+struct v3 {
+  T x, y, z;
+};
+template <class T>
+struct qt {
+  T w, x, y, z;
+};
+
+template <class T> __device__ __forceinline__ v3<T> mk(T a, T b, T c) { return {a, b, c}; }
+template <class T> __device__ __forceinline__ v3<T> operator+(v3<T> a, v3<T> b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+template <class T> __device__ __forceinline__ v3<T> operator-(v3<T> a, v3<T> b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+template <class T> __device__ __forceinline__ v3<T> operator-(v3<T> a) { return {-a.x, -a.y, -a.z}; }
+template <class T> __device__ __forceinline__ v3<T> operator*(v3<T> a, T s) { return {a.x * s, a.y * s, a.z * s}; }
+template <class T> __device__ __forceinline__ T dot(v3<T> a, v3<T> b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+template <class T> __device__ __forceinline__ v3<T> cross(v3<T> a, v3<T> b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+template <class T> __device__ __forceinline__ T vnorm(v3<T> a) { return sqrt(dot(a, a)); }
+template <class T> __device__ __forceinline__ v3<T> vunit(v3<T> a) {  // vec.hpp:42-45
+  const T n = vnorm(a);
+  return n > T(0) ? v3<T>{a.x / n, a.y / n, a.z / n} : v3<T>{0, 0, 0};
+}
+template <class T> __device__ __forceinline__ bool vfinite(v3<T> a) {
+  return isfinite(a.x) && isfinite(a.y) && isfinite(a.z);
+}
+template <class T> __device__ __forceinline__ T comp(v3<T> a, int k) { return k == 0 ? a.x : (k == 1 ? a.y : a.z); }
+
+__device__ __forceinline__ void sincos_(float a, float* s, float* c) { sincosf(a, s, c); }
+__device__ __forceinline__ void sincos_(double a, double* s, double* c) { sincos(a, s, c); }
+
+template <class T> __device__ __forceinline__ qt<T> qmul(qt<T> a, qt<T> b) {
+  return {a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z, a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,
+          a.w * b.y - a.x * b.z + a.y * b.w + a.z * b.x, a.w * b.z + a.x * b.y - a.y * b.x + a.z * b.w};
+}
+template <class T> __device__ __forceinline__ qt<T> qconj(qt<T> q) { return {q.w, -q.x, -q.y, -q.z}; }
+template <class T> __device__ __forceinline__ qt<T> qunit(qt<T> q) {
+  const T n = sqrt(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
+  return {q.w / n, q.x / n, q.y / n, q.z / n};
+}
+// v' = v + 2 q_v x (q_v x v + w v), vec.hpp:163-168
+template <class T> __device__ __forceinline__ v3<T> qrot(qt<T> q, v3<T> v) {
+  const v3<T> u{q.x, q.y, q.z};
+  const v3<T> t = cross(u, v) * T(2);
+  return v + t * q.w + cross(u, t);
+}
+template <class T> __device__ __forceinline__ bool qfinite(qt<T> q) {
+  return isfinite(q.w) && isfinite(q.x) && isfinite(q.y) && isfinite(q.z);
+}
+// Quat::exp_map, vec.hpp:138-145
+template <class T> __device__ __forceinline__ qt<T> qexp(v3<T> rv) {
+  const T ang = vnorm(rv);
+  if (ang < T(1e-12)) return qunit(qt<T>{T(1), T(0.5) * rv.x, T(0.5) * rv.y, T(0.5) * rv.z});
+  const T h = T(0.5) * ang;
+  T s, c;
+  sincos_(h, &s, &c);
+  const v3<T> a = vunit(rv);
+  return {c, a.x * s, a.y * s, a.z * s};
+}
+
+
+// symmetric 3x3 stored as xx yy zz xy xz yz
+template <class T>
+struct sym3 {
+  T xx, yy, zz, xy, xz, yz;
+};
+template <class T> __device__ __forceinline__ v3<T> smul(const sym3<T>& m, v3<T> v) {
+  return {m.xx * v.x + m.xy * v.y + m.xz * v.z, m.xy * v.x + m.yy * v.y + m.yz * v.z,
+          m.xz * v.x + m.yz * v.y + m.zz * v.z};
+}
+// R diag(d) R^T with R = to_matrix(q) (vec.hpp:171-180; solver.cpp:250-252)
+template <class T> __device__ __forceinline__ void rot_mat(qt<T> q, T r[9]) {
+  const T xx = q.x * q.x, yy = q.y * q.y, zz = q.z * q.z;
+  const T xy = q.x * q.y, xz = q.x * q.z, yz = q.y * q.z;
+  const T wx = q.w * q.x, wy = q.w * q.y, wz = q.w * q.z;
+  r[0] = 1 - 2 * (yy + zz); r[1] = 2 * (xy - wz); r[2] = 2 * (xz + wy);
+  r[3] = 2 * (xy + wz); r[4] = 1 - 2 * (xx + zz); r[5] = 2 * (yz - wx);
+  r[6] = 2 * (xz - wy); r[7] = 2 * (yz + wx); r[8] = 1 - 2 * (xx + yy);
+}
+template <class T> __device__ __forceinline__ sym3<T> rdrt(const T r[9], T d0, T d1, T d2) {
+  sym3<T> s;
+  s.xx = r[0] * d0 * r[0] + r[1] * d1 * r[1] + r[2] * d2 * r[2];
+  s.yy = r[3] * d0 * r[3] + r[4] * d1 * r[4] + r[5] * d2 * r[5];
+  s.zz = r[6] * d0 * r[6] + r[7] * d1 * r[7] + r[8] * d2 * r[8];
+  s.xy = r[0] * d0 * r[3] + r[1] * d1 * r[4] + r[2] * d2 * r[5];
+  s.xz = r[0] * d0 * r[6] + r[1] * d1 * r[7] + r[2] * d2 * r[8];
+  s.yz = r[3] * d0 * r[6] + r[4] * d1 * r[7] + r[5] * d2 * r[8];
+  return s;
+}
+
+// 6x6 symmetric packed lower triangle: index(i, j) with i >= j
+__host__ __device__ constexpr int tri(int i, int j) { return i * (i + 1) / 2 + j; }
+__host__ __device__ constexpr int sidx(int i, int j) { return i >= j ? tri(i, j) : tri(j, i); }
+
+}  // namespace stp

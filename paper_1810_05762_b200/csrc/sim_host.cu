@@ -1,0 +1,683 @@
+// Host side of the C-ABI (include/stampede_sim.h): handle lifecycle,
+// device buffers, model upload, state import/export and kernel launches.
+//
+// This replaces the reference's in-process entry points
+//   stampede::physics::step            (solver.hpp:52-53)  -> stp_physics_step
+//   Scene state access / snapshot      (scene.hpp:31-63)   -> stp_set_state/get_state
+//   StepReport                         (types.hpp:115-120) -> stp_get_report/get_contacts
+// and the SPEC-only env API -> stp_reset / stp_step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sim_launch.h"
+#include "stampede_sim.h"
+#include "stp_error.h"
+
+struct stp_sim {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int precision = STP_PRECISION_F32;
+  int W = 32, cpb = 2, cap = 64;
+  stp_model model{};
+  stp_task task{};
+  stp_step_config cfg{};
+  int n = 0, B = 0, J = 0, obs_dim = 0;
+  uint64_t seed = 0;
+  int64_t env_offset = 0;
+  size_t tsize = 4;  // sizeof(T)
+  void* d_model = nullptr;
+  void* d_state = nullptr;
+  double* d_origin = nullptr;
+  void* d_loads = nullptr;
+  bool loads_pending = false;
+  int32_t* d_counters = nullptr;
+  void* d_target = nullptr;
+  void* d_last_tau = nullptr;
+  uint32_t* d_feet = nullptr;
+  int32_t* d_newton = nullptr;
+  int32_t* d_krylov = nullptr;
+  uint8_t* d_failed = nullptr;
+  uint8_t* d_overflow = nullptr;
+  int32_t* d_ccount = nullptr;
+  int32_t* d_cbody = nullptr;
+  double* d_cdata = nullptr;
+  bool record = false;  // record contacts on the next physics step(s)
+  double* d_boxes = nullptr;
+  int n_boxes = 0;
+  // staging for the host-buffer entry points
+  float* d_act = nullptr;
+  float* d_obs = nullptr;
+  float* d_rew = nullptr;
+  uint8_t* d_done = nullptr;
+  std::vector<void*> allocations;
+};
+
+namespace {
+
+using stp::fail;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(STP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                   \
+  do {                                             \
+    cudaError_t _e = (expr);                       \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+template <class P>
+int dalloc(stp_sim* s, P** p, size_t bytes) {
+  void* raw = nullptr;
+  cudaError_t e = cudaMalloc(&raw, std::max<size_t>(bytes, 16));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  CK(cudaMemsetAsync(raw, 0, std::max<size_t>(bytes, 16), s->stream));
+  s->allocations.push_back(raw);
+  *p = reinterpret_cast<P*>(raw);
+  return STP_OK;
+}
+
+// Island rule of the GPU path: an env's dynamic bodies must form ONE
+// joint-connected component (solver.cpp:458-502 then yields one island per
+// env) unless the env is a single free body.
+bool single_island(const stp_model& m) {
+  int par[STP_MAX_BODIES];
+  for (int b = 0; b < m.n_bodies; ++b) par[b] = b;
+  auto find = [&](int x) {
+    while (par[x] != x) x = par[x] = par[par[x]];
+    return x;
+  };
+  for (int j = 0; j < m.n_joints; ++j) {
+    const stp_joint& d = m.joints[j];
+    if (!m.bodies[d.parent].is_static && !m.bodies[d.child].is_static) par[find(d.parent)] = find(d.child);
+  }
+  int root = -1;
+  for (int b = 0; b < m.n_bodies; ++b) {
+    if (m.bodies[b].is_static) continue;
+    const int r = find(b);
+    if (root < 0) root = r;
+    else if (r != root) return false;
+  }
+  return true;
+}
+
+template <class T>
+void build_dev_model(const stp_model& m, const stp_step_config& cfg, stp::DevModel<T>& d) {
+  std::memset(&d, 0, sizeof(d));
+  d.nb = m.n_bodies;
+  d.nj = m.n_joints;
+  d.root = m.root;
+  d.n_feet = m.n_feet;
+  for (int f = 0; f < m.n_feet; ++f) {
+    d.feet[f] = m.feet[f];
+    d.feet_mask |= 1 << m.feet[f];
+  }
+  d.fall_height = T(m.fall_height);
+  d.alive_bonus = T(m.alive_bonus);
+  for (int b = 0; b < 32; ++b) {
+    d.parent[b] = -1;
+    d.joint[b] = -1;
+    d.lrot[0][b] = T(1);
+  }
+  for (int b = 0; b < m.n_bodies; ++b) {
+    const stp_body& s = m.bodies[b];
+    d.shape[b] = s.shape;
+    d.is_static[b] = s.is_static;
+    d.radius[b] = T(s.radius);
+    d.half_len[b] = T(s.half_length);
+    for (int k = 0; k < 3; ++k) {
+      d.hext[k][b] = T(s.half_extents[k]);
+      d.lpos[k][b] = T(s.local_pos[k]);
+      d.inertia[k][b] = T(s.inertia_diag[k]);
+      d.inv_inertia[k][b] = s.is_static ? T(0) : T(1.0 / s.inertia_diag[k]);
+    }
+    for (int k = 0; k < 4; ++k) d.lrot[k][b] = T(s.local_rot[k]);
+    d.mass[b] = T(s.mass);
+    d.inv_mass[b] = s.is_static ? T(0) : T(1.0 / s.mass);
+    for (int k = 0; k < 13; ++k) d.rest_state[k][b] = T(m.rest_state[b][k]);
+  }
+  int n_dyn = 0;
+  for (int b = 0; b < m.n_bodies; ++b) n_dyn += m.bodies[b].is_static ? 0 : 1;
+  int pair_index = 0;
+  for (int j = 0; j < m.n_joints; ++j) {
+    const stp_joint& s = m.joints[j];
+    const int c = s.child;
+    d.parent[c] = s.parent;
+    d.joint[c] = j;
+    d.lane_of_joint[j] = c;
+    d.child_mask[s.parent] |= 1 << c;
+    for (int k = 0; k < 3; ++k) {
+      d.anc_p[k][c] = T(s.anchor_parent[k]);
+      d.anc_c[k][c] = T(s.anchor_child[k]);
+      d.ax_p[k][c] = T(s.axis_parent[k]);
+      d.ax_c[k][c] = T(s.axis_child[k]);
+    }
+    for (int k = 0; k < 4; ++k) d.rest[k][c] = T(s.rest_relative[k]);
+    d.lim_lo[c] = T(s.limit_lo);
+    d.lim_hi[c] = T(s.limit_hi);
+    d.tmax[c] = T(s.max_torque);
+    // Reference aliasing quirk (solver.cpp:350-351, block_sparse.cpp:218):
+    // with n_dyn diagonal blocks created first and two blocks per coupled
+    // pair in row order, creating (child, parent) reallocates the block pool
+    // exactly when the count before it is a power of two.
+    if (!m.bodies[s.parent].is_static && !m.bodies[c].is_static) {
+      const int nblk = n_dyn + 2 * pair_index + 1;  // blocks once (parent, child) exists
+      if (cfg.reference_alias_quirk && (nblk & (nblk - 1)) == 0) d.quirk[c] = 1;
+      ++pair_index;
+    }
+  }
+  int maxd = 0;
+  for (int b = 0; b < m.n_bodies; ++b) {  // topological order: parent < child
+    d.depth[b] = d.parent[b] < 0 ? 0 : d.depth[d.parent[b]] + 1;
+    maxd = std::max(maxd, d.depth[b]);
+  }
+  d.max_depth = maxd;
+}
+
+template <class T>
+stp::DevCfg<T> dev_cfg(const stp_step_config& c) {
+  stp::DevCfg<T> d;
+  d.dt = T(c.dt);
+  d.tol = T(c.krylov_tol);
+  d.margin = T(c.contact_margin);
+  d.beta = T(c.baumgarte);
+  d.kj = T(c.joint_hardness);
+  d.kc = T(c.contact_hardness);
+  d.kl = T(c.limit_hardness);
+  d.epsf = T(c.friction_smoothing);
+  d.lim_act = T(c.limit_activation);
+  d.gx = T(c.gravity[0]);
+  d.gy = T(c.gravity[1]);
+  d.gz = T(c.gravity[2]);
+  d.newton = c.newton_iters;
+  d.kmax = c.krylov_max_iters;
+  d.plane = c.has_ground_plane;
+  return d;
+}
+
+stp::DevTask dev_task(const stp_task& t) {
+  stp::DevTask d;
+  d.kind = t.kind;
+  d.episode_cap = t.episode_cap;
+  d.fall_grace = t.fall_grace;
+  d.target_refresh = t.target_refresh;
+  d.target_radius = t.target_radius;
+  d.target_tolerance = t.target_tolerance;
+  d.spacing = t.spacing;
+  d.perturb_min = t.perturb_min;
+  d.perturb_max = t.perturb_max;
+  d.force_lo = t.perturb_force_lo;
+  d.force_hi = t.perturb_force_hi;
+  d.reset_noise = t.reset_noise;
+  d.auto_reset = t.auto_reset;
+  d.height_map = t.height_map;
+  return d;
+}
+
+template <class T>
+stp::KArgs<T> make_args(stp_sim* s, int mode) {
+  stp::KArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.model = reinterpret_cast<const stp::DevModel<T>*>(s->d_model);
+  a.cfg = dev_cfg<T>(s->cfg);
+  a.task = dev_task(s->task);
+  a.n = s->n;
+  a.mode = mode;
+  a.seed = s->seed;
+  a.env_offset = s->env_offset;
+  a.state = reinterpret_cast<T*>(s->d_state);
+  a.origin = s->d_origin;
+  a.loads = s->loads_pending ? reinterpret_cast<T*>(s->d_loads) : nullptr;
+  a.obs_dim = s->obs_dim;
+  a.counters = s->d_counters;
+  a.target = reinterpret_cast<T*>(s->d_target);
+  a.last_tau = reinterpret_cast<T*>(s->d_last_tau);
+  a.feet = s->d_feet;
+  a.newton_out = s->d_newton;
+  a.krylov_out = s->d_krylov;
+  a.failed_out = s->d_failed;
+  a.overflow_out = s->d_overflow;
+  a.record = s->record ? 1 : 0;
+  a.cap = s->cap;
+  a.c_count = s->d_ccount;
+  a.c_body = s->d_cbody;
+  a.c_data = s->d_cdata;
+  a.n_boxes = s->n_boxes;
+  a.boxes = s->d_boxes;
+  return a;
+}
+
+int launch(stp_sim* s, int mode, const float* torques, const float* actions, float* obs, float* reward,
+           uint8_t* done, const uint8_t* mask, cudaStream_t st) {
+  cudaError_t e;
+  if (s->precision == STP_PRECISION_F64) {
+    auto a = make_args<double>(s, mode);
+    a.torques = torques;
+    a.actions = actions;
+    a.obs = obs;
+    a.reward = reward;
+    a.done = done;
+    a.reset_mask = mask;
+    e = stp::launch_env_step<double>(a, s->W, s->cpb, st);
+  } else {
+    auto a = make_args<float>(s, mode);
+    a.torques = torques;
+    a.actions = actions;
+    a.obs = obs;
+    a.reward = reward;
+    a.done = done;
+    a.reset_mask = mask;
+    e = stp::launch_env_step<float>(a, s->W, s->cpb, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "k_env_step launch");
+  if (mode != 2) s->loads_pending = false;
+  return STP_OK;
+}
+
+cudaStream_t pick(stp_sim* s, void* stream) { return stream ? reinterpret_cast<cudaStream_t>(stream) : s->stream; }
+
+int validate_cfg(const stp_step_config& c) {
+  if (!(c.dt > 0)) return fail(STP_EINVAL, "step config: dt must be > 0");
+  if (c.newton_iters < 1) return fail(STP_EINVAL, "step config: newton_iters must be >= 1");
+  if (!(c.krylov_tol > 0) || c.krylov_max_iters < 1)
+    return fail(STP_EINVAL, "solve_krylov: tol must be > 0 and max_iters >= 1");
+  if (c.contact_margin < 0) return fail(STP_EINVAL, "detect_contacts: margin must be >= 0");
+  const double g = std::sqrt(c.gravity[0] * c.gravity[0] + c.gravity[1] * c.gravity[1] + c.gravity[2] * c.gravity[2]);
+  if (std::abs(g - 9.8) > 1e-9) return fail(STP_EINVAL, "scene: gravity magnitude must be 9.8");
+  return STP_OK;
+}
+
+}  // namespace
+
+namespace stp {
+int sim_dims(const stp_sim* s, int* n, int* J, uint64_t* seed, long long* off, void** stream) {
+  if (!s) return STP_EINVAL;
+  *n = s->n;
+  *J = s->J;
+  *seed = s->seed;
+  *off = s->env_offset;
+  *stream = reinterpret_cast<void*>(s->stream);
+  return STP_OK;
+}
+}  // namespace stp
+
+extern "C" {
+
+stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step_config* cfg, int32_t n_envs,
+                    int32_t device, uint64_t seed, int32_t precision, int64_t env_offset) {
+  if (!model || !task || !cfg) {
+    fail(STP_EINVAL, "stp_create: null argument");
+    return nullptr;
+  }
+  if (n_envs <= 0) {
+    fail(STP_EINVAL, "reset: N must be > 0");
+    return nullptr;
+  }
+  if (stp_validate_model(model) != STP_OK) return nullptr;
+  if (validate_cfg(*cfg) != STP_OK) return nullptr;
+  if (!single_island(*model)) {
+    fail(STP_EINVAL, "model: the GPU path needs every env's dynamic bodies joint-connected (one island per env)");
+    return nullptr;
+  }
+  if (precision != STP_PRECISION_F32 && precision != STP_PRECISION_F64) {
+    fail(STP_EINVAL, "stp_create: precision must be STP_PRECISION_F32 or STP_PRECISION_F64");
+    return nullptr;
+  }
+  auto* s = new stp_sim();
+  s->device = device;
+  s->precision = precision;
+  s->model = *model;
+  s->task = *task;
+  s->cfg = *cfg;
+  s->n = n_envs;
+  s->B = model->n_bodies;
+  s->J = model->n_joints;
+  s->seed = seed;
+  s->env_offset = env_offset;
+  s->W = s->B <= 8 ? 8 : (s->B <= 16 ? 16 : 32);
+  bool boxes_shape = false;
+  for (int b = 0; b < s->B; ++b) boxes_shape = boxes_shape || model->bodies[b].shape == STP_BOX;
+  s->cpb = boxes_shape || task->kind == STP_TASK_HFH_TERRAIN ? 8 : 2;
+  s->cap = s->B * s->cpb;
+  s->obs_dim = 11 + 3 * s->J + model->n_feet + (task->height_map ? 165 : 0);
+  s->tsize = precision == STP_PRECISION_F64 ? 8 : 4;
+  auto bail = [&](int) -> stp_sim* {
+    stp_destroy(s);
+    return nullptr;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaSetDevice");
+    delete s;
+    return nullptr;
+  }
+  e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaStreamCreate");
+    delete s;
+    return nullptr;
+  }
+  const size_t N = size_t(n_envs);
+  const size_t ts = s->tsize;
+  int rc = STP_OK;
+  if (precision == STP_PRECISION_F64) rc = dalloc(s, &s->d_model, sizeof(stp::DevModel<double>));
+  else rc = dalloc(s, &s->d_model, sizeof(stp::DevModel<float>));
+  if (rc || (rc = dalloc(s, &s->d_state, N * stp::kStateFields * s->W * ts)) ||
+      (rc = dalloc(s, &s->d_origin, N * 2 * sizeof(double))) || (rc = dalloc(s, &s->d_loads, N * 6 * s->W * ts)) ||
+      (rc = dalloc(s, &s->d_counters, N * 8 * sizeof(int32_t))) || (rc = dalloc(s, &s->d_target, N * 2 * ts)) ||
+      (rc = dalloc(s, &s->d_last_tau, N * std::max(1, s->J) * ts)) || (rc = dalloc(s, &s->d_feet, N * 4)) ||
+      (rc = dalloc(s, &s->d_newton, N * 4)) || (rc = dalloc(s, &s->d_krylov, N * 4)) ||
+      (rc = dalloc(s, &s->d_failed, N)) || (rc = dalloc(s, &s->d_overflow, N)) ||
+      (rc = dalloc(s, &s->d_ccount, N * 4)) || (rc = dalloc(s, &s->d_cbody, N * s->cap * 4)) ||
+      (rc = dalloc(s, &s->d_cdata, N * s->cap * stp::kCData * sizeof(double))) ||
+      (rc = dalloc(s, &s->d_act, N * std::max(1, s->J) * 4)) || (rc = dalloc(s, &s->d_obs, N * s->obs_dim * 4)) ||
+      (rc = dalloc(s, &s->d_rew, N * 4)) || (rc = dalloc(s, &s->d_done, N)))
+    return bail(rc);
+  if (precision == STP_PRECISION_F64) {
+    stp::DevModel<double> dm;
+    build_dev_model(*model, *cfg, dm);
+    e = cudaMemcpyAsync(s->d_model, &dm, sizeof(dm), cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  } else {
+    stp::DevModel<float> dm;
+    build_dev_model(*model, *cfg, dm);
+    e = cudaMemcpyAsync(s->d_model, &dm, sizeof(dm), cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  }
+  if (e != cudaSuccess) {
+    cuda_fail(e, "model upload");
+    return bail(STP_ECUDA);
+  }
+  // initial reset of every env
+  if (stp_reset(s, nullptr, nullptr, nullptr) != STP_OK) return bail(STP_ECUDA);
+  e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "initial reset");
+    return bail(STP_ECUDA);
+  }
+  return s;
+}
+
+void stp_destroy(stp_sim* s) {
+  if (!s) return;
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  for (void* p : s->allocations) cudaFree(p);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+int stp_set_terrain(stp_sim* s, const stp_static_box* boxes, int32_t n) {
+  if (!s || n < 0 || (n > 0 && !boxes)) return fail(STP_EINVAL, "stp_set_terrain: bad arguments");
+  std::vector<double> h(size_t(std::max(n, 1)) * 8);
+  for (int i = 0; i < n; ++i) {
+    const stp_static_box& b = boxes[i];
+    double* o = h.data() + 8 * i;
+    o[0] = b.center[0];
+    o[1] = b.center[1];
+    o[2] = b.center[2];
+    o[3] = b.half_extents[0];
+    o[4] = b.half_extents[1];
+    o[5] = b.half_extents[2];
+    o[6] = std::cos(b.yaw);  // obb_frame, collide.cpp:131
+    o[7] = std::sin(b.yaw);
+  }
+  CK(cudaStreamSynchronize(s->stream));
+  if (s->d_boxes) {
+    CK(cudaFree(s->d_boxes));
+    s->allocations.erase(std::remove(s->allocations.begin(), s->allocations.end(), (void*)s->d_boxes),
+                         s->allocations.end());
+    s->d_boxes = nullptr;
+  }
+  int rc = dalloc(s, &s->d_boxes, h.size() * sizeof(double));
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(s->d_boxes, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  s->n_boxes = n;
+  if (n > 0 && s->cpb < 8) {
+    // terrain contacts need more slots per body: grow the recorded list too
+    s->cpb = 8;
+    s->cap = s->B * s->cpb;
+    const size_t N = size_t(s->n);
+    for (void* p : {(void*)s->d_cbody, (void*)s->d_cdata}) {
+      CK(cudaFree(p));
+      s->allocations.erase(std::remove(s->allocations.begin(), s->allocations.end(), p), s->allocations.end());
+    }
+    if ((rc = dalloc(s, &s->d_cbody, N * s->cap * 4)) ||
+        (rc = dalloc(s, &s->d_cdata, N * s->cap * stp::kCData * sizeof(double))))
+      return rc;
+  }
+  return STP_OK;
+}
+
+int32_t stp_num_envs(const stp_sim* s) { return s ? s->n : 0; }
+int32_t stp_obs_dim(const stp_sim* s) { return s ? s->obs_dim : 0; }
+int32_t stp_action_dim(const stp_sim* s) { return s ? s->J : 0; }
+int32_t stp_contact_capacity(const stp_sim* s) { return s ? s->cap : 0; }
+void* stp_stream(const stp_sim* s) { return s ? reinterpret_cast<void*>(s->stream) : nullptr; }
+
+int stp_reset(stp_sim* s, const uint8_t* mask, float* obs, void* stream) {
+  if (!s) return fail(STP_EINVAL, "stp_reset: null handle");
+  return launch(s, 2, nullptr, nullptr, obs, nullptr, nullptr, mask, pick(s, stream));
+}
+
+int stp_step(stp_sim* s, const float* actions, float* obs, float* reward, uint8_t* done, void* stream) {
+  if (!s) return fail(STP_EINVAL, "stp_step: null handle");
+  if (s->J > 0 && !actions) return fail(STP_EINVAL, "env_step: actions required");
+  return launch(s, 1, nullptr, actions, obs, reward, done, nullptr, pick(s, stream));
+}
+
+int stp_step_host(stp_sim* s, const float* actions, float* obs, float* reward, uint8_t* done) {
+  if (!s || (s->J > 0 && !actions)) return fail(STP_EINVAL, "stp_step_host: bad arguments");
+  const size_t N = size_t(s->n);
+  CK(cudaMemcpyAsync(s->d_act, actions, N * s->J * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  int rc = launch(s, 1, nullptr, s->d_act, obs ? s->d_obs : nullptr, reward ? s->d_rew : nullptr,
+                  done ? s->d_done : nullptr, nullptr, s->stream);
+  if (rc) return rc;
+  if (obs) CK(cudaMemcpyAsync(obs, s->d_obs, N * s->obs_dim * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+  if (reward) CK(cudaMemcpyAsync(reward, s->d_rew, N * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+  if (done) CK(cudaMemcpyAsync(done, s->d_done, N, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return STP_OK;
+}
+
+int stp_physics_step(stp_sim* s, const float* torques, void* stream) {
+  if (!s) return fail(STP_EINVAL, "stp_physics_step: null handle");
+  if (s->J > 0 && !torques) return fail(STP_EINVAL, "clamp_torques: torque count must equal joint count");
+  return launch(s, 0, torques, nullptr, nullptr, nullptr, nullptr, nullptr, pick(s, stream));
+}
+
+int stp_physics_step_host(stp_sim* s, const double* torques) {
+  if (!s) return fail(STP_EINVAL, "stp_physics_step_host: null handle");
+  if (s->J > 0 && !torques) return fail(STP_EINVAL, "clamp_torques: torque count must equal joint count");
+  const size_t N = size_t(s->n);
+  std::vector<float> t(N * s->J);
+  for (size_t i = 0; i < t.size(); ++i) t[i] = float(torques[i]);
+  if (!t.empty()) CK(cudaMemcpyAsync(s->d_act, t.data(), t.size() * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  s->record = true;
+  int rc = launch(s, 0, s->d_act, nullptr, nullptr, nullptr, nullptr, nullptr, s->stream);
+  s->record = false;
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(s->stream));
+  return STP_OK;
+}
+
+
+int stp_set_state(stp_sim* s, const double* state) {
+  if (!s || !state) return fail(STP_EINVAL, "stp_set_state: bad arguments");
+  const size_t N = size_t(s->n);
+  const int W = s->W, B = s->B, R = s->model.root;
+  std::vector<double> origin(N * 2);
+  std::vector<unsigned char> buf(N * stp::kStateFields * W * s->tsize, 0);
+  for (size_t e = 0; e < N; ++e) {
+    const double* root = state + (e * B + R) * STP_STATE_STRIDE;
+    const double ox = std::rint(root[0]), oy = std::rint(root[1]);
+    origin[2 * e] = ox;
+    origin[2 * e + 1] = oy;
+    for (int b = 0; b < B; ++b) {
+      const double* st = state + (e * B + b) * STP_STATE_STRIDE;
+      for (int f = 0; f < STP_STATE_STRIDE; ++f) {
+        double v = st[f];
+        if (f == 0) v -= ox;
+        if (f == 1) v -= oy;
+        const size_t idx = (e * stp::kStateFields + f) * W + b;
+        if (s->precision == STP_PRECISION_F64) reinterpret_cast<double*>(buf.data())[idx] = v;
+        else reinterpret_cast<float*>(buf.data())[idx] = float(v);
+      }
+    }
+  }
+  // targets are stored relative to the origin: shift them with it
+  std::vector<double> tgt(N * 2);
+  std::vector<double> old(N * 2);
+  std::vector<unsigned char> traw(N * 2 * s->tsize);
+  CK(cudaMemcpyAsync(old.data(), s->d_origin, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(traw.data(), s->d_target, traw.size(), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  for (size_t i = 0; i < N * 2; ++i) {
+    const double t = s->precision == STP_PRECISION_F64 ? reinterpret_cast<double*>(traw.data())[i]
+                                                       : double(reinterpret_cast<float*>(traw.data())[i]);
+    const double tw = old[i] + t;
+    const double tl = tw - origin[i];
+    if (s->precision == STP_PRECISION_F64) reinterpret_cast<double*>(traw.data())[i] = tl;
+    else reinterpret_cast<float*>(traw.data())[i] = float(tl);
+  }
+  CK(cudaMemcpyAsync(s->d_state, buf.data(), buf.size(), cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(s->d_origin, origin.data(), origin.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(s->d_target, traw.data(), traw.size(), cudaMemcpyHostToDevice, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return STP_OK;
+}
+
+int stp_get_state(stp_sim* s, double* state) {
+  if (!s || !state) return fail(STP_EINVAL, "stp_get_state: bad arguments");
+  const size_t N = size_t(s->n);
+  const int W = s->W, B = s->B;
+  std::vector<unsigned char> buf(N * stp::kStateFields * W * s->tsize);
+  std::vector<double> origin(N * 2);
+  CK(cudaMemcpyAsync(buf.data(), s->d_state, buf.size(), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(origin.data(), s->d_origin, origin.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  for (size_t e = 0; e < N; ++e)
+    for (int b = 0; b < B; ++b)
+      for (int f = 0; f < STP_STATE_STRIDE; ++f) {
+        const size_t idx = (e * stp::kStateFields + f) * W + b;
+        double v = s->precision == STP_PRECISION_F64 ? reinterpret_cast<double*>(buf.data())[idx]
+                                                     : double(reinterpret_cast<float*>(buf.data())[idx]);
+        if (f == 0) v += origin[2 * e];
+        if (f == 1) v += origin[2 * e + 1];
+        state[(e * B + b) * STP_STATE_STRIDE + f] = v;
+      }
+  return STP_OK;
+}
+
+int stp_set_external_loads(stp_sim* s, const double* loads) {
+  if (!s || !loads) return fail(STP_EINVAL, "stp_set_external_loads: bad arguments");
+  const size_t N = size_t(s->n);
+  const int W = s->W, B = s->B;
+  std::vector<unsigned char> buf(N * 6 * W * s->tsize, 0);
+  for (size_t e = 0; e < N; ++e)
+    for (int b = 0; b < B; ++b)
+      for (int k = 0; k < 6; ++k) {
+        const double v = loads[(e * B + b) * 6 + k];
+        const size_t idx = (e * 6 + k) * W + b;
+        if (s->precision == STP_PRECISION_F64) reinterpret_cast<double*>(buf.data())[idx] = v;
+        else reinterpret_cast<float*>(buf.data())[idx] = float(v);
+      }
+  CK(cudaMemcpyAsync(s->d_loads, buf.data(), buf.size(), cudaMemcpyHostToDevice, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  s->loads_pending = true;
+  return STP_OK;
+}
+
+int stp_get_contacts(stp_sim* s, int32_t* count, int32_t* body_a, int32_t* body_b, double* point, double* normal,
+                     double* separation, double* normal_impulse, double* tangential_impulse) {
+  if (!s) return fail(STP_EINVAL, "stp_get_contacts: null handle");
+  const size_t N = size_t(s->n), C = size_t(s->cap);
+  std::vector<int32_t> cnt(N), body(N * C);
+  std::vector<double> data(N * C * stp::kCData);
+  CK(cudaMemcpyAsync(cnt.data(), s->d_ccount, N * 4, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(body.data(), s->d_cbody, N * C * 4, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(data.data(), s->d_cdata, data.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  for (size_t e = 0; e < N; ++e) {
+    if (count) count[e] = cnt[e];
+    const int m = std::min<int>(cnt[e], int(C));
+    for (int i = 0; i < m; ++i) {
+      const size_t k = e * C + i;
+      const double* d = data.data() + k * stp::kCData;
+      if (body_a) body_a[k] = body[k];
+      if (body_b) body_b[k] = -1;
+      for (int c = 0; c < 3; ++c) {
+        if (point) point[3 * k + c] = d[c];
+        if (normal) normal[3 * k + c] = d[3 + c];
+        if (tangential_impulse) tangential_impulse[3 * k + c] = d[8 + c];
+      }
+      if (separation) separation[k] = d[6];
+      if (normal_impulse) normal_impulse[k] = d[7];
+    }
+  }
+  return STP_OK;
+}
+
+int stp_get_report(stp_sim* s, int32_t* newton, int32_t* krylov, uint8_t* failed, uint8_t* overflow) {
+  if (!s) return fail(STP_EINVAL, "stp_get_report: null handle");
+  const size_t N = size_t(s->n);
+  if (newton) CK(cudaMemcpyAsync(newton, s->d_newton, N * 4, cudaMemcpyDeviceToHost, s->stream));
+  if (krylov) CK(cudaMemcpyAsync(krylov, s->d_krylov, N * 4, cudaMemcpyDeviceToHost, s->stream));
+  if (failed) CK(cudaMemcpyAsync(failed, s->d_failed, N, cudaMemcpyDeviceToHost, s->stream));
+  if (overflow) CK(cudaMemcpyAsync(overflow, s->d_overflow, N, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return STP_OK;
+}
+
+int stp_get_task_state(stp_sim* s, double* target, int32_t* counters, double* last_tau) {
+  if (!s) return fail(STP_EINVAL, "stp_get_task_state: null handle");
+  const size_t N = size_t(s->n), J = size_t(s->J);
+  std::vector<double> origin(N * 2);
+  std::vector<unsigned char> traw(N * 2 * s->tsize), lraw(N * std::max<size_t>(J, 1) * s->tsize);
+  CK(cudaMemcpyAsync(origin.data(), s->d_origin, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(traw.data(), s->d_target, traw.size(), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(lraw.data(), s->d_last_tau, lraw.size(), cudaMemcpyDeviceToHost, s->stream));
+  if (counters) CK(cudaMemcpyAsync(counters, s->d_counters, N * 8 * 4, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  auto rd = [&](const std::vector<unsigned char>& v, size_t i) {
+    return s->precision == STP_PRECISION_F64 ? reinterpret_cast<const double*>(v.data())[i]
+                                             : double(reinterpret_cast<const float*>(v.data())[i]);
+  };
+  if (target)
+    for (size_t i = 0; i < N * 2; ++i) target[i] = origin[i] + rd(traw, i);
+  if (last_tau)
+    for (size_t i = 0; i < N * J; ++i) last_tau[i] = rd(lraw, i);
+  return STP_OK;
+}
+
+int stp_set_task_state(stp_sim* s, const double* target, const int32_t* counters, const double* last_tau) {
+  if (!s) return fail(STP_EINVAL, "stp_set_task_state: null handle");
+  const size_t N = size_t(s->n), J = size_t(s->J);
+  std::vector<double> origin(N * 2);
+  CK(cudaMemcpyAsync(origin.data(), s->d_origin, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  auto put = [&](std::vector<unsigned char>& v, size_t i, double x) {
+    if (s->precision == STP_PRECISION_F64) reinterpret_cast<double*>(v.data())[i] = x;
+    else reinterpret_cast<float*>(v.data())[i] = float(x);
+  };
+  if (target) {
+    std::vector<unsigned char> traw(N * 2 * s->tsize);
+    for (size_t i = 0; i < N * 2; ++i) put(traw, i, target[i] - origin[i]);
+    CK(cudaMemcpyAsync(s->d_target, traw.data(), traw.size(), cudaMemcpyHostToDevice, s->stream));
+  }
+  if (last_tau && J > 0) {
+    std::vector<unsigned char> lraw(N * J * s->tsize);
+    for (size_t i = 0; i < N * J; ++i) put(lraw, i, last_tau[i]);
+    CK(cudaMemcpyAsync(s->d_last_tau, lraw.data(), lraw.size(), cudaMemcpyHostToDevice, s->stream));
+  }
+  if (counters) CK(cudaMemcpyAsync(s->d_counters, counters, N * 8 * 4, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return STP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,398 @@
+// The fused B200 environment-step kernel.
+//
+// One warp segment of W lanes = one environment; lane b = body b.  A single
+// launch performs, per env:
+//   K1  speculative contacts vs plane / terrain boxes     (collide.cpp:270-299)
+//   K2  actuation, body dynamics, constraint rows, 4 x (assembly + PCR),
+//       impulse report, integration, rollback             (solver.cpp:395-597,
+//                                                          krylov.cpp:106-174)
+//   K3  task epilogue: reward, termination, flagrun, perturbation schedule,
+//       auto-reset via hinge FK, observation
+// so the body state is read from HBM once and written once per step.
+//
+// The system matrix is never materialised in HBM: each lane keeps its 6x6
+// diagonal block (packed symmetric, 21 values) and its Cholesky factor in
+// registers and its off-diagonal block H(child, parent) in shared memory;
+// H(parent, child) = H(child, parent)^T is applied by the child lane and
+// gathered by the parent through shared memory (the articulation is a tree).
+// Dot products are segment reductions over warp shuffles.
+#pragma once
+
+#include <type_traits>
+
+#include "sim_device.cuh"
+#include "stp_rng.h"
+
+namespace stp {
+
+constexpr int kCData = 11;  // recorded contact: point3 normal3 sep pn pt3 (double)
+
+template <class T>
+struct KArgs {
+  const DevModel<T>* model;
+  DevCfg<T> cfg;
+  DevTask task;
+  int n;
+  int mode;  // 0 = physics::step, 1 = env_step, 2 = reset
+  uint64_t seed;
+  long long env_offset;
+  T* state;        // [n][16][W]
+  double* origin;  // [n][2]
+  T* loads;        // [n][6][W] or null
+  const float* torques;  // mode 0: [n][J] (N*m)
+  const float* actions;  // mode 1: [n][J] (normalised)
+  float* obs;
+  float* reward;
+  uint8_t* done;
+  int obs_dim;
+  int32_t* counters;  // [n][8]
+  T* target;          // [n][2], relative to origin
+  T* last_tau;        // [n][J]
+  uint32_t* feet;     // [n] feet-contact bits of the last env step
+  const uint8_t* reset_mask;
+  int32_t* newton_out;
+  int32_t* krylov_out;
+  uint8_t* failed_out;
+  uint8_t* overflow_out;
+  int record;
+  int cap;
+  int32_t* c_count;   // [n]
+  int32_t* c_body;    // [n][cap]
+  double* c_data;     // [n][cap][11]
+  int n_boxes;
+  const double* boxes;  // [nbox][8]: cx cy cz hx hy hz cos(yaw) sin(yaw)
+};
+
+enum { C_FRAME = 0, C_FLAG = 1, C_FALL = 2, C_NEXTP = 3, C_EPISODE = 4, C_FLAGDRAW = 5, C_PERTDRAW = 6 };
+constexpr int kGridCols = 64;
+
+template <int W, class T>
+__device__ __forceinline__ T seg_sum(T v, unsigned mask) {
+#pragma unroll
+  for (int off = W / 2; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off, W);
+  return v;
+}
+template <int W, class T>
+__device__ __forceinline__ T seg_max(T v, unsigned mask) {
+#pragma unroll
+  for (int off = W / 2; off > 0; off >>= 1) v = max(v, __shfl_xor_sync(mask, v, off, W));
+  return v;
+}
+template <int W, class T>
+__device__ __forceinline__ T from(T v, int src, unsigned mask) {
+  return __shfl_sync(mask, v, src, W);
+}
+template <int W, class T>
+__device__ __forceinline__ v3<T> from(v3<T> v, int src, unsigned mask) {
+  return {__shfl_sync(mask, v.x, src, W), __shfl_sync(mask, v.y, src, W), __shfl_sync(mask, v.z, src, W)};
+}
+template <int W, class T>
+__device__ __forceinline__ qt<T> from(qt<T> v, int src, unsigned mask) {
+  return {__shfl_sync(mask, v.w, src, W), __shfl_sync(mask, v.x, src, W), __shfl_sync(mask, v.y, src, W),
+          __shfl_sync(mask, v.z, src, W)};
+}
+
+template <class T>
+__device__ __forceinline__ T rcp_or_div(T num, T den) {
+  return num / den;
+}
+
+// packed symmetric 6x6 rank-1 update H += d j j^T (assemble, solver.cpp:337-338)
+template <class T>
+__device__ __forceinline__ void sym_add(T (&H)[21], const T (&j)[6], T d) {
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    const T dj = d * j[r];
+#pragma unroll
+    for (int c = 0; c <= r; ++c) H[tri(r, c)] += dj * j[c];
+  }
+}
+
+template <class T>
+__device__ __forceinline__ T dot6(const T (&a)[6], const T (&b)[6]) {
+  return a[0] * b[0] + a[1] * b[1] + a[2] * b[2] + a[3] * b[3] + a[4] * b[4] + a[5] * b[5];
+}
+
+// unilateral_bias, solver.cpp:84-87
+template <class T>
+__device__ __forceinline__ T uni_bias(T gap, T beta, T dt) {
+  return gap < T(0) ? -(beta / dt) * gap : -gap / dt;
+}
+
+// friction_weight, solver.cpp:267-270
+template <class T>
+__device__ __forceinline__ T fric_weight(T pn, T vt, T eps) {
+  const T s = vt / eps;
+  return pn / (eps * sqrt(T(1) + s * s));  // mu = 1 (collide.cpp:25)
+}
+
+// Body inertia quadratic form a^T Iinv a + inv_m |l|^2 for one side of a row.
+template <class T>
+__device__ __forceinline__ T quad(const sym3<T>& Iinv, v3<T> a) {
+  return dot(a, smul(Iinv, a));
+}
+
+// joint_angle, solver.cpp:405-411
+template <class T>
+__device__ __forceinline__ T hinge_angle(qt<T> qp, qt<T> qc, qt<T> rest, v3<T> axc) {
+  const qt<T> rel = qmul(qconj(qp), qc);
+  qt<T> d = qmul(qconj(rest), rel);
+  if (d.w < T(0)) d = qt<T>{-d.w, -d.x, -d.y, -d.z};
+  const T proj = d.x * axc.x + d.y * axc.y + d.z * axc.z;
+  return T(2) * atan2(proj, d.w);
+}
+
+template <class T>
+__device__ __forceinline__ v3<T> ldv(const T (&a)[3][32], int b) {
+  return {a[0][b], a[1][b], a[2][b]};
+}
+
+// ---------------------------------------------------------------------------
+// Block-tree matrix-vector product y = H v (BlockSparseSym::apply,
+// block_sparse.cpp:233-251) for the segment.
+// ---------------------------------------------------------------------------
+template <class T, int W>
+struct Tree {
+  unsigned mask;
+  int lane, base, b, par_src;
+  bool has_off;
+  uint32_t cmask;
+  T* hoff;  // smem [36][32]
+  T* scat;  // smem [28][32]
+  // rank-1 terms applied on top of the stored blocks
+  T lim_s;        // -sum of active limit weights (angular block -s a a^T)
+  v3<T> lim_a;
+  bool quirk;     // H(p,c) misses anchor row 0 (reference aliasing quirk)
+  T q_d0;
+  T q_ja[6], q_jb[6];
+
+  __device__ __forceinline__ void apply(const T (&H)[21], const T (&v)[6], T (&y)[6]) const {
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      T s = T(0);
+#pragma unroll
+      for (int c = 0; c < 6; ++c) s += H[sidx(r, c)] * v[c];
+      y[r] = s;
+    }
+    T vp[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) vp[k] = __shfl_sync(mask, v[k], par_src, W);
+    T t[6] = {0, 0, 0, 0, 0, 0};
+    if (has_off) {
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        T s = T(0);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const T h = hoff[(r * 6 + c) * 32 + lane];
+          s += h * vp[c];
+          t[c] += h * v[r];
+        }
+        y[r] += s;
+      }
+      if (lim_s != T(0)) {
+        const T ap = lim_a.x * vp[3] + lim_a.y * vp[4] + lim_a.z * vp[5];
+        const T ac = lim_a.x * v[3] + lim_a.y * v[4] + lim_a.z * v[5];
+        y[3] += lim_s * lim_a.x * ap;
+        y[4] += lim_s * lim_a.y * ap;
+        y[5] += lim_s * lim_a.z * ap;
+        t[3] += lim_s * lim_a.x * ac;
+        t[4] += lim_s * lim_a.y * ac;
+        t[5] += lim_s * lim_a.z * ac;
+      }
+      if (quirk) {
+        const T s0 = q_d0 * dot6(q_jb, v);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) t[k] -= s0 * q_ja[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) scat[k * 32 + lane] = t[k];
+    __syncwarp(mask);
+    uint32_t cm = cmask;
+    while (cm) {
+      const int c = __ffs(cm) - 1;
+      cm &= cm - 1;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) y[k] += scat[k * 32 + base + c];
+    }
+    __syncwarp(mask);
+  }
+
+  // Gather sum over children of K values into out (parent side scatter).
+  template <int K>
+  __device__ __forceinline__ void gather(const T (&v)[K], T (&out)[K]) const {
+#pragma unroll
+    for (int k = 0; k < K; ++k) scat[k * 32 + lane] = v[k];
+    __syncwarp(mask);
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = T(0);
+    uint32_t cm = cmask;
+    while (cm) {
+      const int c = __ffs(cm) - 1;
+      cm &= cm - 1;
+#pragma unroll
+      for (int k = 0; k < K; ++k) out[k] += scat[k * 32 + base + c];
+    }
+    __syncwarp(mask);
+  }
+};
+
+// 6x6 Cholesky of a packed SPD block (krylov.cpp:27-41); rinv = 1/diag.
+template <class T>
+__device__ __forceinline__ bool chol6(const T (&H)[21], T (&L)[21], T (&rinv)[6]) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      T s = H[tri(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s -= L[tri(i, k)] * L[tri(j, k)];
+      if (i == j) {
+        ok = ok && (s > T(0));
+        const T d = sqrt(s);
+        L[tri(i, i)] = d;
+        rinv[i] = T(1) / d;
+      } else {
+        if constexpr (std::is_same<T, double>::value) L[tri(i, j)] = s / L[tri(j, j)];
+        else L[tri(i, j)] = s * rinv[j];
+      }
+    }
+  }
+  return ok;
+}
+
+// block-Jacobi apply (cholesky_solve, krylov.cpp:43-56)
+template <class T>
+__device__ __forceinline__ void psolve(bool ok, const T (&L)[21], const T (&rinv)[6], const T (&r)[6],
+                                       T (&z)[6]) {
+  if (!ok) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) z[k] = r[k];
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    T s = r[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) s -= L[tri(i, k)] * z[k];
+    if constexpr (std::is_same<T, double>::value) z[i] = s / L[tri(i, i)];
+    else z[i] = s * rinv[i];
+  }
+#pragma unroll
+  for (int i = 5; i >= 0; --i) {
+    T s = z[i];
+#pragma unroll
+    for (int k = i + 1; k < 6; ++k) s -= L[tri(k, i)] * z[k];
+    if constexpr (std::is_same<T, double>::value) z[i] = s / L[tri(i, i)];
+    else z[i] = s * rinv[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Environment reset via hinge forward kinematics (the FK
+// convention reproduces joint_angle, solver.cpp:405-411, at the drawn angle).
+// All lanes of the segment call it; depth levels are resolved in order.
+// ---------------------------------------------------------------------------
+template <class T, int W>
+__device__ void reset_env(const KArgs<T>& a, const DevModel<T>& M, int e, int b, unsigned mask, bool act,
+                          v3<T>& x, qt<T>& q, v3<T>& v, v3<T>& w, int32_t (&cnt)[8], T& tx, T& ty, double& ox,
+                          double& oy) {
+  const uint64_t genv = uint64_t(a.env_offset + e);
+  const uint64_t s = stp_derive_seed(a.seed, STP_TAG_RESET, (genv << 32) | uint32_t(cnt[C_EPISODE]));
+  cnt[C_EPISODE] += 1;
+  const double amp = a.task.reset_noise;
+  const int J = M.nj;
+  auto noise = [&](uint32_t k) { return amp * (2.0 * stp_uniform(s, k) - 1.0); };
+  ox = double(genv % kGridCols) * a.task.spacing;
+  oy = double(genv / kGridCols) * a.task.spacing;
+  const int r = M.root;
+  if (b == r) {
+    x = {T(double(M.rest_state[0][b]) + noise(0)), T(double(M.rest_state[1][b]) + noise(1)),
+         T(double(M.rest_state[2][b]) + noise(2))};
+    const v3<T> rv{T(noise(3)), T(noise(4)), T(noise(5))};
+    const qt<T> rq{M.rest_state[3][b], M.rest_state[4][b], M.rest_state[5][b], M.rest_state[6][b]};
+    q = qunit(qmul(qexp(rv), rq));
+    v = {T(noise(6 + J)), T(noise(7 + J)), T(noise(8 + J))};
+    w = {T(noise(9 + J)), T(noise(10 + J)), T(noise(11 + J))};
+  } else if (act) {
+    // static bodies keep their rest pose; dynamic ones are set by FK below
+    x = {M.rest_state[0][b], M.rest_state[1][b], M.rest_state[2][b]};
+    q = {M.rest_state[3][b], M.rest_state[4][b], M.rest_state[5][b], M.rest_state[6][b]};
+    v = {0, 0, 0};
+    w = {0, 0, 0};
+  }
+  const int jn = act ? M.joint[b] : -1;
+  const int par = act && M.parent[b] >= 0 ? M.parent[b] : b;
+  const int my_depth = act ? M.depth[b] : -1;
+  for (int d = 1; d <= M.max_depth; ++d) {
+    const v3<T> xp = from<W>(x, par, mask);
+    const qt<T> qp = from<W>(q, par, mask);
+    const v3<T> vp = from<W>(v, par, mask);
+    const v3<T> wp = from<W>(w, par, mask);
+    if (my_depth == d && jn >= 0 && !M.is_static[b]) {
+      const T th = T(noise(6 + jn));
+      const T thd = T(noise(12 + J + jn));
+      const v3<T> axc = ldv(M.ax_c, b);
+      const qt<T> rest{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]};
+      // Quat::from_axis_angle, vec.hpp:130-135
+      T sh, ch;
+      sincos_(T(0.5) * th, &sh, &ch);
+      const v3<T> au = vunit(axc);
+      const qt<T> aa{ch, au.x * sh, au.y * sh, au.z * sh};
+      q = qmul(qmul(qp, rest), aa);
+      const v3<T> anchor = xp + qrot(qp, ldv(M.anc_p, b));
+      x = anchor - qrot(q, ldv(M.anc_c, b));
+      w = wp + qrot(q, axc) * thd;
+      v = vp + cross(wp, anchor - xp) - cross(w, anchor - x);
+    }
+  }
+  cnt[C_FRAME] = 0;
+  cnt[C_FLAG] = 0;
+  cnt[C_FALL] = 0;
+  const v3<T> xr = from<W>(x, r, mask);
+  if (a.task.target_refresh > 0) {
+    const uint64_t fs = stp_derive_seed(a.seed, STP_TAG_FLAG, (genv << 32) | uint32_t(cnt[C_FLAGDRAW]));
+    cnt[C_FLAGDRAW] += 1;
+    const double rad = a.task.target_radius * sqrt(stp_uniform(fs, 0));
+    const double phi = 2.0 * M_PI * stp_uniform(fs, 1);
+    tx = T(double(xr.x) + rad * cos(phi));
+    ty = T(double(xr.y) + rad * sin(phi));
+  } else {
+    tx = xr.x + T(1000);
+    ty = xr.y;
+  }
+  if (a.task.perturb_max > 0 && a.task.perturb_max >= a.task.perturb_min) {
+    const uint64_t ps = stp_derive_seed(a.seed, STP_TAG_PERTURB, (genv << 32) | uint32_t(cnt[C_PERTDRAW]));
+    const int span = a.task.perturb_max - a.task.perturb_min + 1;
+    int k = int(floor(stp_uniform(ps, 0) * span));
+    if (k >= span) k = span - 1;
+    cnt[C_NEXTP] = a.task.perturb_min + k;
+  } else {
+    cnt[C_NEXTP] = -1;
+  }
+}
+
+// terrain_height over the box list, relative to the env origin
+// (collide.cpp:348-359); boxes in double world coordinates.
+__device__ __forceinline__ double terrain_height_dev(const double* boxes, int n, double x, double y) {
+  double h = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double* bx = boxes + 8 * i;
+    const double dx = x - bx[0], dy = y - bx[1];
+    const double lx = bx[6] * dx + bx[7] * dy;
+    const double ly = -bx[7] * dx + bx[6] * dy;
+    if (fabs(lx) <= bx[3] && fabs(ly) <= bx[4]) h = fmax(h, bx[2] + bx[5]);
+  }
+  return h;
+}
+
+// geometric height-map offsets (ratio 1.3 from 0.2 m)
+__device__ __forceinline__ double geo_offset(int k) {
+  const int a = k < 0 ? -k : k;
+  const double d = 0.2 * (pow(1.3, double(a)) - 1.0) / 0.3;
+  return k < 0 ? -d : d;
+}
+
+}  // namespace stp

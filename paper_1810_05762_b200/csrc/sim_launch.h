@@ -1,0 +1,11 @@
+// Host-visible launch entry of the fused step kernel (sim_step.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "sim_kernels.cuh"
+
+namespace stp {
+// lanes = W (8/16/32 lanes per env), cpb = contact slots per body.
+template <class T>
+cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s);
+}  // namespace stp

@@ -1,0 +1,982 @@
+// Fused environment-step kernel (K1 contacts + K2 solve + K3 epilogue).
+// See sim_kernels.cuh for the execution model; every block below cites the
+// reference lines it re-implements.  Instantiated per precision in
+// sim_step_f32.cu / sim_step_f64.cu (parallel compilation).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "sim_kernels.cuh"
+#include "sim_launch.h"
+
+namespace stp {
+
+
+template <class T, int W, int CPB>
+__global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = tid / W;
+  if (e >= a.n) return;  // whole segments exit together
+  const int lane = threadIdx.x & 31;
+  const int b = lane % W;
+  const int base = lane - b;
+  const unsigned mask = W == 32 ? 0xffffffffu : (((1u << W) - 1u) << base);
+  const DevModel<T>& M = *a.model;
+  const DevCfg<T>& cf = a.cfg;
+  const bool act = b < M.nb;
+  const bool dyn = act && !M.is_static[b];
+  const int par = act ? M.parent[b] : -1;
+  const int jnt = act ? M.joint[b] : -1;
+  const int par_src = par >= 0 ? par : b;
+  const bool pdyn = par >= 0 && !M.is_static[par];
+  const int J = M.nj;
+
+  extern __shared__ unsigned char smem_raw[];
+  T* wsm = reinterpret_cast<T*>(smem_raw) + (threadIdx.x >> 5) * (64 * 32);
+  Tree<T, W> tree;
+  tree.mask = mask;
+  tree.lane = lane;
+  tree.base = base;
+  tree.b = b;
+  tree.par_src = par_src;
+  tree.has_off = dyn && pdyn && jnt >= 0;
+  tree.cmask = act ? uint32_t(M.child_mask[b]) : 0u;
+  tree.hoff = wsm;
+  tree.scat = wsm + 36 * 32;
+  tree.lim_s = T(0);
+  tree.lim_a = {0, 0, 0};
+  tree.quirk = false;
+
+  // ---- task state (every lane keeps a copy; lane 0 writes back) ----------
+  int32_t cnt[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) cnt[k] = a.counters ? a.counters[size_t(e) * 8 + k] : 0;
+  double ox = a.origin[2 * e], oy = a.origin[2 * e + 1];
+  T tx = a.target ? a.target[2 * e] : T(0), ty = a.target ? a.target[2 * e + 1] : T(0);
+
+  // ---- load body state (SoA, coalesced per field) ------------------------
+  const size_t sbase = size_t(e) * kStateFields * W + b;
+  v3<T> x{0, 0, 0}, v{0, 0, 0}, w{0, 0, 0};
+  qt<T> q{1, 0, 0, 0};
+  if (act) {
+    x = {a.state[sbase + 0 * W], a.state[sbase + 1 * W], a.state[sbase + 2 * W]};
+    q = {a.state[sbase + 3 * W], a.state[sbase + 4 * W], a.state[sbase + 5 * W], a.state[sbase + 6 * W]};
+    v = {a.state[sbase + 7 * W], a.state[sbase + 8 * W], a.state[sbase + 9 * W]};
+    w = {a.state[sbase + 10 * W], a.state[sbase + 11 * W], a.state[sbase + 12 * W]};
+  }
+
+  float act_u = 0.f;  // this lane's joint action (env mode)
+  bool step_failed = false;
+  bool overflow = false;
+  int nc = 0;
+  int newton_done = 0, krylov_total = 0;
+  T prev_rx = from<W>(x.x, M.root, mask), prev_ry = from<W>(x.y, M.root, mask);
+  bool perturbed = false;
+
+  T ltau = (jnt >= 0 && a.last_tau) ? a.last_tau[size_t(e) * J + jnt] : T(0);
+  unsigned feet_bits = a.feet ? a.feet[e] : 0u;
+  if (a.mode == 2) {
+    // ---------------- reset only ------------------------
+    const bool doit = a.reset_mask == nullptr || a.reset_mask[e];
+    if (doit) {
+      reset_env<T, W>(a, M, e, b, mask, act, x, q, v, w, cnt, tx, ty, ox, oy);
+      ltau = T(0);
+      feet_bits = 0u;
+    }
+  } else {
+    // ---------------- actuation (clamp_torques, solver.cpp:395-403) -------
+    T tau = T(0);
+    if (jnt >= 0) {
+      if (a.mode == 1) {
+        act_u = a.actions[size_t(e) * J + jnt];
+        tau = T(act_u) * M.tmax[b];  // actions scaled by tau_max
+      } else {
+        tau = T(a.torques[size_t(e) * J + jnt]);
+      }
+      tau = min(max(tau, -M.tmax[b]), M.tmax[b]);
+    }
+    // external loads (Scene::external_force/torque, scene.hpp:45-46)
+    v3<T> fext{0, 0, 0}, text{0, 0, 0};
+    if (a.loads && act) {
+      const size_t lb = size_t(e) * 6 * W + b;
+      fext = {a.loads[lb + 0 * W], a.loads[lb + 1 * W], a.loads[lb + 2 * W]};
+      text = {a.loads[lb + 3 * W], a.loads[lb + 4 * W], a.loads[lb + 5 * W]};
+      for (int k = 0; k < 6; ++k) a.loads[lb + k * W] = T(0);  // clear_external_loads
+    }
+    // perturbation schedule (apply_perturbations)
+    if (a.mode == 1 && a.task.perturb_max > 0 && cnt[C_FRAME] == cnt[C_NEXTP]) {
+      perturbed = true;
+      if (b == M.root) {
+        const uint64_t genv = uint64_t(a.env_offset + e);
+        const uint64_t ps = stp_derive_seed(a.seed, STP_TAG_PERTURB, (genv << 32) | uint32_t(cnt[C_PERTDRAW]));
+        const double f = a.task.force_lo + (a.task.force_hi - a.task.force_lo) * stp_uniform(ps, 1);
+        const double phi = 2.0 * M_PI * stp_uniform(ps, 2);
+        fext.x += T(f * cos(phi));
+        fext.y += T(f * sin(phi));
+      }
+    }
+
+    // ---------------- K1: contacts (detect_contacts, collide.cpp:270-299) -
+    v3<T> c_n[CPB], c_r[CPB];  // normal, lever arm (point - x)
+    T c_sep[CPB];
+#pragma unroll
+    for (int k = 0; k < CPB; ++k) {
+      c_n[k] = {0, 0, 1};
+      c_r[k] = {0, 0, 0};
+      c_sep[k] = T(0);
+    }
+    auto add_contact = [&](v3<T> p, v3<T> n, T sep) {
+      if (nc < CPB) {
+#pragma unroll
+        for (int k = 0; k < CPB; ++k)
+          if (k == nc) {
+            c_n[k] = n;
+            c_r[k] = p - x;
+            c_sep[k] = sep;
+          }
+        ++nc;
+      } else {
+        overflow = true;
+      }
+    };
+    if (dyn) {
+      const T margin = cf.margin;
+      const int shp = M.shape[b];
+      const T rad = M.radius[b];
+      // world_shape, collide.cpp:38-78
+      const qt<T> lr{M.lrot[0][b], M.lrot[1][b], M.lrot[2][b], M.lrot[3][b]};
+      const qt<T> rot = qmul(q, lr);
+      const v3<T> pos = x + qrot(q, ldv(M.lpos, b));
+      v3<T> p0 = pos, p1 = pos;
+      T lo_z;
+      T Rb[9];
+      if (shp == STP_CAPSULE) {
+        const v3<T> ax = qrot(rot, v3<T>{T(0), T(0), M.half_len[b]});
+        p0 = pos - ax;
+        p1 = pos + ax;
+        lo_z = min(p0.z, p1.z) - rad;
+      } else if (shp == STP_SPHERE) {
+        lo_z = pos.z - rad;
+      } else {
+        rot_mat(rot, Rb);
+        const T ez = fabs(Rb[6]) * M.hext[0][b] + fabs(Rb[7]) * M.hext[1][b] + fabs(Rb[8]) * M.hext[2][b];
+        lo_z = pos.z - ez;
+      }
+      // collide_plane, collide.cpp:93-119 (gated by aabb_min.z < margin, :286)
+      if (cf.plane && lo_z < margin) {
+        const v3<T> up{0, 0, 1};
+        if (shp == STP_SPHERE) {
+          const T sep = p0.z - rad;
+          if (sep < margin) add_contact(p0 - up * rad, up, sep);
+        } else if (shp == STP_CAPSULE) {
+          const T s0 = p0.z - rad;
+          if (s0 < margin) add_contact(p0 - up * rad, up, s0);
+          const T s1 = p1.z - rad;
+          if (s1 < margin) add_contact(p1 - up * rad, up, s1);
+        } else {
+          for (int cx = -1; cx <= 1; cx += 2)
+            for (int cy = -1; cy <= 1; cy += 2)
+              for (int cz = -1; cz <= 1; cz += 2) {
+                const v3<T> l{T(cx) * M.hext[0][b], T(cy) * M.hext[1][b], T(cz) * M.hext[2][b]};
+                const v3<T> corner{pos.x + Rb[0] * l.x + Rb[1] * l.y + Rb[2] * l.z,
+                                   pos.y + Rb[3] * l.x + Rb[4] * l.y + Rb[5] * l.z,
+                                   pos.z + Rb[6] * l.x + Rb[7] * l.y + Rb[8] * l.z};
+                if (corner.z < margin) add_contact(corner, up, corner.z);
+              }
+        }
+      }
+      // static terrain boxes (collide.cpp:287-298), in box-index order
+      if (a.n_boxes > 0 && shp != STP_BOX) {
+        v3<T> lo, hi;
+        lo = {min(p0.x, p1.x) - rad, min(p0.y, p1.y) - rad, min(p0.z, p1.z) - rad};
+        hi = {max(p0.x, p1.x) + rad, max(p0.y, p1.y) + rad, max(p0.z, p1.z) + rad};
+        for (int i = 0; i < a.n_boxes; ++i) {
+          const double* bx = a.boxes + 8 * i;
+          // box centre relative to the env origin, exact in double first
+          const v3<T> c{T(bx[0] - ox), T(bx[1] - oy), T(bx[2])};
+          const v3<T> h{T(bx[3]), T(bx[4]), T(bx[5])};
+          const T ex = h.x + h.y;
+          if (hi.x + margin < c.x - ex || lo.x - margin > c.x + ex || hi.y + margin < c.y - ex ||
+              lo.y - margin > c.y + ex || hi.z + margin < c.z - h.z || lo.z - margin > c.z + h.z)
+            continue;
+          const T cs = T(bx[6]), sn = T(bx[7]);
+          // point_obb, collide.cpp:140-173
+          auto point_box = [&](v3<T> p, v3<T>& nrm, v3<T>& surf) -> T {
+            const v3<T> d0 = p - c;
+            const v3<T> loc{cs * d0.x + sn * d0.y, -sn * d0.x + cs * d0.y, d0.z};
+            const v3<T> cl{min(max(loc.x, -h.x), h.x), min(max(loc.y, -h.y), h.y), min(max(loc.z, -h.z), h.z)};
+            const v3<T> dl = loc - cl;
+            const T out = vnorm(dl);
+            if (out > T(1e-12)) {
+              surf = {c.x + cs * cl.x - sn * cl.y, c.y + sn * cl.x + cs * cl.y, c.z + cl.z};
+              nrm = {(cs * dl.x - sn * dl.y) / out, (sn * dl.x + cs * dl.y) / out, dl.z / out};
+              return out;
+            }
+            T best = h.x - fabs(loc.x);
+            int axis = 0;
+            T sgn = loc.x >= T(0) ? T(1) : T(-1);
+            if (h.y - fabs(loc.y) < best) {
+              best = h.y - fabs(loc.y);
+              axis = 1;
+              sgn = loc.y >= T(0) ? T(1) : T(-1);
+            }
+            if (h.z - fabs(loc.z) < best) {
+              best = h.z - fabs(loc.z);
+              axis = 2;
+              sgn = loc.z >= T(0) ? T(1) : T(-1);
+            }
+            v3<T> ln{0, 0, 0}, ls = loc;
+            if (axis == 0) { ln.x = sgn; ls.x = sgn * h.x; }
+            else if (axis == 1) { ln.y = sgn; ls.y = sgn * h.y; }
+            else { ln.z = sgn; ls.z = sgn * h.z; }
+            surf = {c.x + cs * ls.x - sn * ls.y, c.y + sn * ls.x + cs * ls.y, c.z + ls.z};
+            nrm = {cs * ln.x - sn * ln.y, sn * ln.x + cs * ln.y, ln.z};
+            return -best;
+          };
+          v3<T> nrm, surf;
+          if (shp == STP_SPHERE) {
+            const T d = point_box(p0, nrm, surf);
+            if (d - rad < margin) add_contact(surf, nrm, d - rad);
+          } else {
+            // collide_capsule_obb, collide.cpp:183-214
+            const v3<T> seg = p1 - p0;
+            T lo_t = 0, hi_t = 1;
+            for (int it = 0; it < 32; ++it) {
+              const T m1 = lo_t + (hi_t - lo_t) / T(3), m2 = hi_t - (hi_t - lo_t) / T(3);
+              v3<T> n1, s1;
+              const T d1 = point_box(p0 + seg * m1, n1, s1);
+              const T d2 = point_box(p0 + seg * m2, n1, s1);
+              if (d1 <= d2) hi_t = m2;
+              else lo_t = m1;
+            }
+            const T tmid = T(0.5) * (lo_t + hi_t);
+            bool mid_added = false;
+            {
+              const T d = point_box(p0 + seg * tmid, nrm, surf);
+              if (d - rad < margin) {
+                add_contact(surf, nrm, d - rad);
+                mid_added = true;
+              }
+            }
+            for (int te = 0; te < 2; ++te) {
+              const T tt = T(te);
+              if (mid_added && fabs(tt - tmid) < T(0.05)) continue;
+              const T d = point_box(p0 + seg * tt, nrm, surf);
+              if (d - rad < margin) add_contact(surf, nrm, d - rad);
+            }
+          }
+        }
+      }
+    }
+    const bool any_contact = __any_sync(mask, nc > 0);
+
+    // ---------------- body dynamics (body_dynamics, solver.cpp:230-262) ---
+    const qt<T> qp = from<W>(q, par_src, mask);
+    v3<T> torque = text;
+    v3<T> jt{0, 0, 0};  // torque this joint applies to the child (+) / parent (-)
+    if (jnt >= 0) {
+      jt = qrot(qp, ldv(M.ax_p, b)) * tau;  // parent's axis (solver.cpp:240)
+      torque = torque + jt;
+    }
+    {
+      T mine[3] = {jt.x, jt.y, jt.z}, kids[3];
+      tree.gather<3>(mine, kids);
+      torque = torque - v3<T>{kids[0], kids[1], kids[2]};
+    }
+    T Rm[9];
+    rot_mat(q, Rm);
+    const T inv_m = dyn ? M.inv_mass[b] : T(0);
+    const T mass = dyn ? M.mass[b] : T(0);
+    sym3<T> Iw = rdrt(Rm, M.inertia[0][b], M.inertia[1][b], M.inertia[2][b]);
+    sym3<T> Iinv = rdrt(Rm, M.inv_inertia[0][b], M.inv_inertia[1][b], M.inv_inertia[2][b]);
+    if (!dyn) {
+      Iw = {0, 0, 0, 0, 0, 0};
+      Iinv = {0, 0, 0, 0, 0, 0};
+    }
+    v3<T> vfree{0, 0, 0}, wfree{0, 0, 0};
+    if (dyn) {
+      const v3<T> force = v3<T>{cf.gx, cf.gy, cf.gz} * mass + fext;
+      vfree = v + force * (cf.dt * inv_m);
+      // implicit_gyro, solver.cpp:216-226
+      v3<T> wg = w;
+      const v3<T> mom = smul(Iw, w) + torque * cf.dt;
+      for (int it = 0; it < 2; ++it) {
+        const v3<T> iw = smul(Iw, wg);
+        const v3<T> f = iw + cross(wg, iw) * cf.dt - mom;
+        // jac = I + (skew(w) I - skew(Iw)) dt
+        const T I00 = Iw.xx, I01 = Iw.xy, I02 = Iw.xz, I11 = Iw.yy, I12 = Iw.yz, I22 = Iw.zz;
+        T jm[9];
+        // skew(w) * I
+        jm[0] = -wg.z * I01 + wg.y * I02;
+        jm[1] = -wg.z * I11 + wg.y * I12;
+        jm[2] = -wg.z * I12 + wg.y * I22;
+        jm[3] = wg.z * I00 - wg.x * I02;
+        jm[4] = wg.z * I01 - wg.x * I12;
+        jm[5] = wg.z * I02 - wg.x * I22;
+        jm[6] = -wg.y * I00 + wg.x * I01;
+        jm[7] = -wg.y * I01 + wg.x * I11;
+        jm[8] = -wg.y * I02 + wg.x * I12;
+        // - skew(iw)
+        jm[1] += iw.z;
+        jm[2] -= iw.y;
+        jm[3] -= iw.z;
+        jm[5] += iw.x;
+        jm[6] += iw.y;
+        jm[7] -= iw.x;
+        const T A[9] = {I00 + jm[0] * cf.dt, I01 + jm[1] * cf.dt, I02 + jm[2] * cf.dt,
+                        I01 + jm[3] * cf.dt, I11 + jm[4] * cf.dt, I12 + jm[5] * cf.dt,
+                        I02 + jm[6] * cf.dt, I12 + jm[7] * cf.dt, I22 + jm[8] * cf.dt};
+        // adjugate inverse (vec.hpp:107-120) applied to f
+        const T cA = A[4] * A[8] - A[5] * A[7], cB = A[2] * A[7] - A[1] * A[8], cC = A[1] * A[5] - A[2] * A[4];
+        const T cD = A[5] * A[6] - A[3] * A[8], cE = A[0] * A[8] - A[2] * A[6], cF = A[2] * A[3] - A[0] * A[5];
+        const T cG = A[3] * A[7] - A[4] * A[6], cH = A[1] * A[6] - A[0] * A[7], cI = A[0] * A[4] - A[1] * A[3];
+        const T det = A[0] * cA + A[1] * cD + A[2] * cG;
+        const v3<T> step{(cA / det) * f.x + (cB / det) * f.y + (cC / det) * f.z,
+                         (cD / det) * f.x + (cE / det) * f.y + (cF / det) * f.z,
+                         (cG / det) * f.x + (cH / det) * f.y + (cI / det) * f.z};
+        wg = wg - step;
+      }
+      wfree = vfinite(wg) ? wg : w;
+    }
+
+    // ---------------- joint rows (build_rows, solver.cpp:105-174) --------
+    const T bdt = cf.beta / cf.dt;
+    const v3<T> xp = from<W>(x, par_src, mask);
+    const v3<T> wp = from<W>(w, par_src, mask);
+    const T p_invm = from<W>(inv_m, par_src, mask);
+    sym3<T> pIinv;
+    pIinv.xx = from<W>(Iinv.xx, par_src, mask);
+    pIinv.yy = from<W>(Iinv.yy, par_src, mask);
+    pIinv.zz = from<W>(Iinv.zz, par_src, mask);
+    pIinv.xy = from<W>(Iinv.xy, par_src, mask);
+    pIinv.xz = from<W>(Iinv.xz, par_src, mask);
+    pIinv.yz = from<W>(Iinv.yz, par_src, mask);
+    const bool has_joint = dyn && jnt >= 0;
+    // equality rows: 3 anchor + 2 angular; ja/jb per row
+    T eq_d[5] = {0, 0, 0, 0, 0}, eq_bias[5] = {0, 0, 0, 0, 0};
+    v3<T> ra{0, 0, 0}, rb{0, 0, 0}, t1{0, 0, 0}, t2{0, 0, 0};
+    v3<T> axw{0, 0, 0};
+    T d_lo = 0, d_hi = 0, b_lo = 0, b_hi = 0;
+    bool has_lo = false, has_hi = false;
+    if (has_joint) {
+      ra = qrot(qp, ldv(M.anc_p, b));
+      rb = qrot(q, ldv(M.anc_c, b));
+      const v3<T> cpos = (x + rb) - (xp + ra);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const v3<T> ek{T(k == 0), T(k == 1), T(k == 2)};
+        T wsum = T(0);
+        if (pdyn) {
+          wsum += p_invm * T(1);
+          wsum += quad(pIinv, -cross(ra, ek));
+        }
+        wsum += inv_m * T(1);
+        wsum += quad(Iinv, cross(rb, ek));
+        eq_d[k] = cf.kj * (wsum > T(1e-12) ? T(1) / wsum : T(0));  // effective_mass :69-80
+        eq_bias[k] = -bdt * comp(cpos, k);
+      }
+      const v3<T> aw = qrot(qp, ldv(M.ax_p, b));
+      const v3<T> bw = qrot(q, ldv(M.ax_c, b));
+      const v3<T> ref = fabs(aw.z) < T(0.9) ? v3<T>{0, 0, 1} : v3<T>{1, 0, 0};
+      t1 = vunit(cross(aw, ref));
+      t2 = cross(aw, t1);
+      const v3<T> err = cross(aw, bw);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const v3<T> t = k == 0 ? t1 : t2;
+        T wsum = T(0);
+        if (pdyn) wsum += quad(pIinv, -t);
+        wsum += quad(Iinv, t);
+        eq_d[3 + k] = cf.kj * (wsum > T(1e-12) ? T(1) / wsum : T(0));
+        eq_bias[3 + k] = -bdt * dot(t, err);
+      }
+      // speculative limits (solver.cpp:144-173)
+      const qt<T> rest{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]};
+      const v3<T> axc = ldv(M.ax_c, b);
+      const T angle = hinge_angle(qp, q, rest, axc);
+      axw = qrot(q, axc);
+      const T rate = dot(axw, w - wp);
+      const T lo_gap = angle - M.lim_lo[b];
+      const T hi_gap = M.lim_hi[b] - angle;
+      const T travel = T(1.5) * fabs(rate) * cf.dt;
+      const T thr = max(cf.lim_act, travel);
+      T wl = T(0);
+      if (pdyn) wl += quad(pIinv, axw);
+      wl += quad(Iinv, axw);
+      const T meff = wl > T(1e-12) ? T(1) / wl : T(0);
+      if (lo_gap < thr) {
+        has_lo = true;
+        d_lo = cf.kl * meff;
+        b_lo = uni_bias(lo_gap, cf.beta, cf.dt);
+      }
+      if (hi_gap < thr) {
+        has_hi = true;
+        d_hi = cf.kl * meff;
+        b_hi = uni_bias(hi_gap, cf.beta, cf.dt);
+      }
+      if (M.quirk[b]) {
+        tree.quirk = true;
+        tree.q_d0 = eq_d[0];
+        const v3<T> ca = -cross(ra, v3<T>{1, 0, 0});
+        const v3<T> cb = cross(rb, v3<T>{1, 0, 0});
+        tree.q_ja[0] = T(-1); tree.q_ja[1] = 0; tree.q_ja[2] = 0;
+        tree.q_ja[3] = ca.x; tree.q_ja[4] = ca.y; tree.q_ja[5] = ca.z;
+        tree.q_jb[0] = T(1); tree.q_jb[1] = 0; tree.q_jb[2] = 0;
+        tree.q_jb[3] = cb.x; tree.q_jb[4] = cb.y; tree.q_jb[5] = cb.z;
+      }
+    }
+    // contact rows (solver.cpp:176-210): per contact normal + 2 tangents
+    T c_d[CPB], c_b[CPB];
+    v3<T> c_t1[CPB];
+#pragma unroll
+    for (int k = 0; k < CPB; ++k) {
+      c_d[k] = T(0);
+      c_b[k] = T(0);
+      c_t1[k] = {1, 0, 0};
+      if (k < nc) {
+        const v3<T> n = c_n[k];
+        const v3<T> rn = cross(c_r[k], n);
+        T wsum = inv_m * dot(n, n);
+        wsum += quad(Iinv, rn);
+        c_d[k] = cf.kc * (wsum > T(1e-12) ? T(1) / wsum : T(0));
+        c_b[k] = uni_bias(c_sep[k], cf.beta, cf.dt);
+        const v3<T> ref = fabs(n.z) < T(0.9) ? v3<T>{0, 0, 1} : v3<T>{1, 0, 0};
+        c_t1[k] = vunit(cross(n, ref));
+      }
+    }
+
+    // ---------------- constant part of the system (assemble, :288-359) ---
+    // own diagonal block: mass + equality rows as child; off block H(c,p)
+    T Heq[21];
+#pragma unroll
+    for (int k = 0; k < 21; ++k) Heq[k] = T(0);
+    T rhs_eq[6] = {0, 0, 0, 0, 0, 0};
+    if (dyn) {
+      Heq[tri(0, 0)] = mass;
+      Heq[tri(1, 1)] = mass;
+      Heq[tri(2, 2)] = mass;
+      Heq[tri(3, 3)] = Iw.xx;
+      Heq[tri(4, 3)] = Iw.xy;
+      Heq[tri(4, 4)] = Iw.yy;
+      Heq[tri(5, 3)] = Iw.xz;
+      Heq[tri(5, 4)] = Iw.yz;
+      Heq[tri(5, 5)] = Iw.zz;
+      const v3<T> iwf = smul(Iw, wfree);
+      rhs_eq[0] = mass * vfree.x;
+      rhs_eq[1] = mass * vfree.y;
+      rhs_eq[2] = mass * vfree.z;
+      rhs_eq[3] = iwf.x;
+      rhs_eq[4] = iwf.y;
+      rhs_eq[5] = iwf.z;
+    }
+    {
+      // parent-side contributions of this lane's joint rows, gathered by parent
+      T up[27];
+#pragma unroll
+      for (int k = 0; k < 27; ++k) up[k] = T(0);
+      T* hoff = tree.hoff;
+      T Hoff[36];
+#pragma unroll
+      for (int k = 0; k < 36; ++k) Hoff[k] = T(0);
+      if (has_joint) {
+#pragma unroll
+        for (int rr = 0; rr < 5; ++rr) {
+          T ja[6], jb[6];
+          if (rr < 3) {
+            const v3<T> ek{T(rr == 0), T(rr == 1), T(rr == 2)};
+            const v3<T> ca = -cross(ra, ek), cb = cross(rb, ek);
+            ja[0] = -ek.x; ja[1] = -ek.y; ja[2] = -ek.z; ja[3] = ca.x; ja[4] = ca.y; ja[5] = ca.z;
+            jb[0] = ek.x; jb[1] = ek.y; jb[2] = ek.z; jb[3] = cb.x; jb[4] = cb.y; jb[5] = cb.z;
+          } else {
+            const v3<T> t = rr == 3 ? t1 : t2;
+            ja[0] = 0; ja[1] = 0; ja[2] = 0; ja[3] = -t.x; ja[4] = -t.y; ja[5] = -t.z;
+            jb[0] = 0; jb[1] = 0; jb[2] = 0; jb[3] = t.x; jb[4] = t.y; jb[5] = t.z;
+          }
+          const T d = eq_d[rr];
+          if (!(d > T(0))) continue;  // assemble skips reg <= 0 (solver.cpp:331)
+          sym_add(Heq, jb, d);
+          const T db = d * eq_bias[rr];
+#pragma unroll
+          for (int r = 0; r < 6; ++r) rhs_eq[r] += jb[r] * db;
+          if (pdyn) {
+            T Hp[21];
+#pragma unroll
+            for (int k = 0; k < 21; ++k) Hp[k] = T(0);
+            sym_add(Hp, ja, d);
+#pragma unroll
+            for (int k = 0; k < 21; ++k) up[k] += Hp[k];
+#pragma unroll
+            for (int r = 0; r < 6; ++r) up[21 + r] += ja[r] * db;
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+              const T djb = d * jb[r];
+#pragma unroll
+              for (int c = 0; c < 6; ++c) Hoff[r * 6 + c] += djb * ja[c];
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 36; ++k) hoff[k * 32 + lane] = Hoff[k];
+      T got[27];
+      tree.gather<27>(up, got);
+#pragma unroll
+      for (int k = 0; k < 21; ++k) Heq[k] += got[k];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) rhs_eq[r] += got[21 + r];
+    }
+
+    // ---------------- Newton loop (solver.cpp:540-548) ---------------------
+    T u[6] = {v.x, v.y, v.z, w.x, w.y, w.z};  // warm start from current velocities
+    const bool need_solve = J > 0 || any_contact;
+    if (!need_solve) {
+      // free-body fast path, solver.cpp:517-523
+      u[0] = vfree.x; u[1] = vfree.y; u[2] = vfree.z;
+      u[3] = wfree.x; u[4] = wfree.y; u[5] = wfree.z;
+    } else {
+      for (int it = 0; it < cf.newton; ++it) {
+        // unilateral activity + friction weights at the iterate (:304-328)
+        const T up_[6] = {from<W>(u[0], par_src, mask), from<W>(u[1], par_src, mask),
+                          from<W>(u[2], par_src, mask), from<W>(u[3], par_src, mask),
+                          from<W>(u[4], par_src, mask), from<W>(u[5], par_src, mask)};
+        T H[21], rhs[6];
+#pragma unroll
+        for (int k = 0; k < 21; ++k) H[k] = Heq[k];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) rhs[k] = rhs_eq[k];
+        // joint limit rows: angular only, child side here, parent side gathered
+        T lim_s = T(0);
+        T pl[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (has_joint && (has_lo || has_hi)) {
+          const T wc_a = axw.x * u[3] + axw.y * u[4] + axw.z * u[5];
+          const T wp_a = pdyn ? axw.x * up_[3] + axw.y * up_[4] + axw.z * up_[5] : T(0);
+          for (int side = 0; side < 2; ++side) {
+            const bool has = side == 0 ? has_lo : has_hi;
+            if (!has) continue;
+            const T d = side == 0 ? d_lo : d_hi;
+            const T bias = side == 0 ? b_lo : b_hi;
+            const T sg = side == 0 ? T(1) : T(-1);  // lo: jb = +axw; hi: jb = -axw
+            const T rate = sg * (wc_a - wp_a);
+            const T pred = d * (bias - rate);
+            if (pred > T(0) && d > T(0)) {
+              lim_s -= d;
+              T jb[6] = {0, 0, 0, sg * axw.x, sg * axw.y, sg * axw.z};
+              sym_add(H, jb, d);
+              const T db = d * bias;
+              rhs[3] += jb[3] * db;
+              rhs[4] += jb[4] * db;
+              rhs[5] += jb[5] * db;
+              if (pdyn) {
+                pl[0] += d * axw.x * axw.x;
+                pl[1] += d * axw.y * axw.x;
+                pl[2] += d * axw.y * axw.y;
+                pl[3] += d * axw.z * axw.x;
+                pl[4] += d * axw.z * axw.y;
+                pl[5] += d * axw.z * axw.z;
+                pl[6] += -sg * axw.x * db;
+                pl[7] += -sg * axw.y * db;
+                pl[8] += -sg * axw.z * db;
+              }
+            }
+          }
+        }
+        {
+          T got[9];
+          tree.gather<9>(pl, got);
+          H[tri(3, 3)] += got[0];
+          H[tri(4, 3)] += got[1];
+          H[tri(4, 4)] += got[2];
+          H[tri(5, 3)] += got[3];
+          H[tri(5, 4)] += got[4];
+          H[tri(5, 5)] += got[5];
+          rhs[3] += got[6];
+          rhs[4] += got[7];
+          rhs[5] += got[8];
+        }
+        tree.lim_s = lim_s;
+        tree.lim_a = axw;
+        // contacts: normal + smoothed Coulomb friction (:311-327)
+#pragma unroll
+        for (int k = 0; k < CPB; ++k) {
+          if (k < nc) {
+            const v3<T> n = c_n[k];
+            const v3<T> rn = cross(c_r[k], n);
+            const T jn[6] = {n.x, n.y, n.z, rn.x, rn.y, rn.z};
+            const T rate = dot6(jn, u);
+            const T pred = c_d[k] * (c_b[k] - rate);
+            if (pred > T(0)) {
+              const v3<T> ta = c_t1[k], tb = cross(n, ta);
+              const v3<T> rta = cross(c_r[k], ta), rtb = cross(c_r[k], tb);
+              const T j1[6] = {ta.x, ta.y, ta.z, rta.x, rta.y, rta.z};
+              const T j2[6] = {tb.x, tb.y, tb.z, rtb.x, rtb.y, rtb.z};
+              const T vt1 = dot6(j1, u), vt2 = dot6(j2, u);
+              const T vt = sqrt(vt1 * vt1 + vt2 * vt2);
+              const T fw = fric_weight(pred, vt, cf.epsf);
+              if (c_d[k] > T(0)) {
+                sym_add(H, jn, c_d[k]);
+                const T db = c_d[k] * c_b[k];
+#pragma unroll
+                for (int r = 0; r < 6; ++r) rhs[r] += jn[r] * db;
+              }
+              if (fw > T(0)) {
+                sym_add(H, j1, fw);
+                sym_add(H, j2, fw);
+              }
+            }
+          }
+        }
+
+        // ---------------- PCR (solve_krylov_inplace, krylov.cpp:106-174) --
+        bool fin = true;
+#pragma unroll
+        for (int k = 0; k < 21; ++k) fin = fin && isfinite(H[k]);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) fin = fin && isfinite(rhs[k]);
+        if (tree.has_off) {
+          for (int k = 0; k < 36; ++k) fin = fin && isfinite(tree.hoff[k * 32 + lane]);
+        }
+        if (!__all_sync(mask, fin)) {  // reference throws (krylov.cpp:113-114)
+          step_failed = true;
+          ++newton_done;
+          break;
+        }
+        const T bn = sqrt(seg_sum<W>(dot6(rhs, rhs), mask));
+        ++newton_done;
+        if (bn == T(0)) {
+#pragma unroll
+          for (int k = 0; k < 6; ++k) u[k] = T(0);
+          continue;
+        }
+        T L[21], rinv[6];
+        const bool ok = dyn && chol6(H, L, rinv);
+        T r[6], z[6], p[6], ap[6], tmp[6];
+        tree.apply(H, u, tmp);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) r[k] = dyn ? rhs[k] - tmp[k] : T(0);
+        psolve(ok, L, rinv, r, z);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) p[k] = z[k];
+        tree.apply(H, z, ap);
+        T zaz = seg_sum<W>(dot6(z, ap), mask);
+        const T tol_abs = cf.tol * bn;
+        T rn = sqrt(seg_sum<W>(dot6(r, r), mask));
+        int kk = 0;
+        while (kk < cf.kmax && rn > tol_abs) {
+          T map[6];
+          psolve(ok, L, rinv, ap, map);
+          const T denom = seg_sum<W>(dot6(ap, map), mask);
+          if (!(denom > T(0)) || !(zaz > T(0))) break;  // breakdown (:144)
+          const T alpha = zaz / denom;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            u[k] += alpha * p[k];
+            r[k] -= alpha * ap[k];
+          }
+          ++kk;
+          psolve(ok, L, rinv, r, z);
+          rn = sqrt(seg_sum<W>(dot6(r, r), mask));
+          if (rn <= tol_abs) break;
+          T az[6];
+          tree.apply(H, z, az);
+          const T zn = seg_sum<W>(dot6(z, az), mask);
+          const T beta = zn / zaz;
+          zaz = zn;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            p[k] = z[k] + beta * p[k];
+            ap[k] = az[k] + beta * ap[k];
+          }
+        }
+        krylov_total += kk;
+        bool ufin = true;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) ufin = ufin && isfinite(u[k]);
+        if (!__all_sync(mask, ufin)) {  // never hand back a poisoned iterate (:168-172)
+#pragma unroll
+          for (int k = 0; k < 6; ++k) u[k] = T(0);
+        }
+      }
+    }
+
+    // ---------------- impulse report (report_impulses, :365-391) ----------
+    if (a.record) {
+      int off = nc;
+#pragma unroll
+      for (int s2 = 1; s2 < W; s2 <<= 1) {
+        const int o = __shfl_up_sync(mask, off, s2, W);
+        if (b >= s2) off += o;
+      }
+      off -= nc;  // exclusive prefix: contact list order = body order
+      const int total = __shfl_sync(mask, off + nc, W - 1, W);
+      if (b == 0) a.c_count[e] = total;
+#pragma unroll
+      for (int k = 0; k < CPB; ++k) {
+        if (k < nc && off + k < a.cap) {
+          const v3<T> n = c_n[k];
+          const v3<T> rn = cross(c_r[k], n);
+          const T jn[6] = {n.x, n.y, n.z, rn.x, rn.y, rn.z};
+          const T pn = max(T(0), c_d[k] * (c_b[k] - dot6(jn, u)));
+          v3<T> pt{0, 0, 0};
+          if (pn > T(0)) {
+            const v3<T> ta = c_t1[k], tb = cross(n, ta);
+            const v3<T> rta = cross(c_r[k], ta), rtb = cross(c_r[k], tb);
+            const T j1[6] = {ta.x, ta.y, ta.z, rta.x, rta.y, rta.z};
+            const T j2[6] = {tb.x, tb.y, tb.z, rtb.x, rtb.y, rtb.z};
+            const T vt1 = dot6(j1, u), vt2 = dot6(j2, u);
+            const T vt = sqrt(vt1 * vt1 + vt2 * vt2);
+            const T fw = fric_weight(pn, vt, cf.epsf);
+            pt = ta * (-fw * vt1) + tb * (-fw * vt2);
+          }
+          const size_t slot = size_t(e) * a.cap + off + k;
+          a.c_body[slot] = b;
+          double* cd = a.c_data + slot * kCData;
+          const v3<T> pw = x + c_r[k];
+          cd[0] = ox + double(pw.x);
+          cd[1] = oy + double(pw.y);
+          cd[2] = double(pw.z);
+          cd[3] = double(n.x);
+          cd[4] = double(n.y);
+          cd[5] = double(n.z);
+          cd[6] = double(c_sep[k]);
+          cd[7] = double(pn);
+          cd[8] = double(pt.x);
+          cd[9] = double(pt.y);
+          cd[10] = double(pt.z);
+        }
+      }
+    }
+
+    // ---------------- integrate + rollback (:562-569, :580-593) -----------
+    v3<T> xn = x, vn = v, wn = w;
+    qt<T> qn = q;
+    if (dyn) {
+      vn = {u[0], u[1], u[2]};
+      wn = {u[3], u[4], u[5]};
+      xn = x + vn * cf.dt;
+      qn = qunit(qmul(qexp(wn * cf.dt), q));
+    }
+    const bool fin_state = vfinite(xn) && qfinite(qn) && vfinite(vn) && vfinite(wn);
+    step_failed = step_failed || !__all_sync(mask, fin_state);
+    if (!step_failed) {
+      x = xn;
+      q = qn;
+      v = vn;
+      w = wn;
+    }
+  }
+
+  // ---------------- K3: task epilogue (env_step) ---------
+  if (a.mode == 1) {
+    const int R = M.root;
+    const v3<T> xr = from<W>(x, R, mask);
+    const qt<T> qr = from<W>(q, R, mask);
+    // feet-ground flags: foot has >= 1 static contact this step
+    const unsigned fb = __ballot_sync(mask, act && nc > 0 && ((M.feet_mask >> b) & 1)) >> base;
+    T rew = T(0);
+    if (!step_failed) {
+      // compute_reward
+      const T ox_ = tx - prev_rx, oy_ = ty - prev_ry;
+      const T od0 = sqrt(ox_ * ox_ + oy_ * oy_);
+      T S = T(0);
+      if (od0 > T(0)) S = ((xr.x - prev_rx) * ox_ + (xr.y - prev_ry) * oy_) / od0 / cf.dt;
+      const T yaw = atan2(T(2) * (qr.w * qr.z + qr.x * qr.y), T(1) - T(2) * (qr.y * qr.y + qr.z * qr.z));
+      const T cth = cos(atan2(ty - xr.y, tx - xr.x) - yaw);
+      const T rhead = cth > T(0.8) ? T(1) : cth / T(0.8);
+      const T cvert = T(1) - T(2) * (qr.x * qr.x + qr.y * qr.y);
+      const T rstand = cvert > T(0.93) ? T(1) : T(0);
+      T tc = T(0), uc = T(0), nl = T(0);
+      const qt<T> qpn = from<W>(q, par_src, mask);
+      if (jnt >= 0) {
+        const T uu = T(act_u);
+        tc = fabs(min(max(uu, T(-1)), T(1)));
+        uc = uu * uu;
+        const T ang = hinge_angle(qpn, q, qt<T>{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]},
+                                  ldv(M.ax_c, b));
+        nl = (ang - M.lim_lo[b] < cf.lim_act || M.lim_hi[b] - ang < cf.lim_act) ? T(1) : T(0);
+      }
+      tc = seg_sum<W>(tc, mask);
+      uc = seg_sum<W>(uc, mask);
+      nl = seg_sum<W>(nl, mask);
+      const T nfeet = T(__popc(fb));
+      rew = M.alive_bonus + S + T(0.5) * rhead + T(0.05) * rstand - T(4) * tc - T(0.5) * uc - T(0.2) * nl - nfeet;
+    }
+    // termination
+    const int frame_before = cnt[C_FRAME];
+    cnt[C_FRAME] += 1;
+    const bool low = xr.z < M.fall_height;
+    cnt[C_FALL] = low ? cnt[C_FALL] + 1 : 0;
+    const bool fell = a.task.fall_grace > 0 ? cnt[C_FALL] >= a.task.fall_grace : low;
+    const bool dn = step_failed || fell || cnt[C_FRAME] >= a.task.episode_cap;
+    const uint64_t genv = uint64_t(a.env_offset + e);
+    if (perturbed) {
+      cnt[C_PERTDRAW] += 1;
+      const uint64_t ps = stp_derive_seed(a.seed, STP_TAG_PERTURB, (genv << 32) | uint32_t(cnt[C_PERTDRAW]));
+      const int span = a.task.perturb_max - a.task.perturb_min + 1;
+      int k = int(floor(stp_uniform(ps, 0) * span));
+      if (k >= span) k = span - 1;
+      cnt[C_NEXTP] = frame_before + a.task.perturb_min + k;
+    }
+    // flagrun targets (update_flagrun_targets)
+    if (a.task.target_refresh > 0) {
+      cnt[C_FLAG] += 1;
+      const T dx = tx - xr.x, dy = ty - xr.y;
+      if (cnt[C_FLAG] >= a.task.target_refresh || sqrt(dx * dx + dy * dy) < T(a.task.target_tolerance)) {
+        const uint64_t fs = stp_derive_seed(a.seed, STP_TAG_FLAG, (genv << 32) | uint32_t(cnt[C_FLAGDRAW]));
+        cnt[C_FLAGDRAW] += 1;
+        const double rad = a.task.target_radius * sqrt(stp_uniform(fs, 0));
+        const double phi = 2.0 * M_PI * stp_uniform(fs, 1);
+        tx = T(double(xr.x) + rad * cos(phi));
+        ty = T(double(xr.y) + rad * sin(phi));
+        cnt[C_FLAG] = 0;
+      }
+    }
+    ltau = jnt >= 0 ? min(max(T(act_u), T(-1)), T(1)) : T(0);
+    feet_bits = fb;
+    if (dn && a.task.auto_reset) {
+      reset_env<T, W>(a, M, e, b, mask, act, x, q, v, w, cnt, tx, ty, ox, oy);
+      ltau = T(0);
+      feet_bits = 0;
+    }
+    if (b == 0) {
+      if (a.reward) a.reward[e] = float(rew);
+      if (a.done) a.done[e] = dn ? 1 : 0;
+    }
+  }
+  if (a.mode >= 1) {
+    if (jnt >= 0 && a.last_tau) a.last_tau[size_t(e) * J + jnt] = ltau;
+    if (b == 0 && a.feet) a.feet[e] = feet_bits;
+    // observation (Table 2)
+    if (a.obs) {
+      const int R = M.root;
+      float* o = a.obs + size_t(e) * a.obs_dim;
+      const v3<T> xr2 = from<W>(x, R, mask);
+      const qt<T> qr2 = from<W>(q, R, mask);
+      const v3<T> vr2 = from<W>(v, R, mask);
+      const v3<T> wr2 = from<W>(w, R, mask);
+      const T yaw = atan2(T(2) * (qr2.w * qr2.z + qr2.x * qr2.y), T(1) - T(2) * (qr2.y * qr2.y + qr2.z * qr2.z));
+      T sy, cy;
+      sincos_(yaw, &sy, &cy);
+      if (b == 0) {
+        o[0] = float(xr2.z);
+        o[1] = float(atan2(T(2) * (qr2.w * qr2.x + qr2.y * qr2.z), T(1) - T(2) * (qr2.x * qr2.x + qr2.y * qr2.y)));
+        T sp = T(2) * (qr2.w * qr2.y - qr2.z * qr2.x);
+        sp = min(max(sp, T(-1)), T(1));
+        o[2] = float(asin(sp));
+        o[3] = float(cy * vr2.x + sy * vr2.y);
+        o[4] = float(-sy * vr2.x + cy * vr2.y);
+        o[5] = float(vr2.z);
+        o[6] = float(cy * wr2.x + sy * wr2.y);
+        o[7] = float(-sy * wr2.x + cy * wr2.y);
+        o[8] = float(wr2.z);
+        T sh, ch;
+        sincos_(atan2(ty - xr2.y, tx - xr2.x) - yaw, &sh, &ch);
+        o[9] = float(sh);
+        o[10] = float(ch);
+        for (int f = 0; f < M.n_feet; ++f) o[11 + 3 * J + f] = ((feet_bits >> M.feet[f]) & 1) ? 1.f : 0.f;
+      }
+      const qt<T> qpo = from<W>(q, par_src, mask);
+      const v3<T> wpo = from<W>(w, par_src, mask);
+      if (jnt >= 0) {
+        const v3<T> axc = ldv(M.ax_c, b);
+        const T ang = hinge_angle(qpo, q, qt<T>{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]}, axc);
+        const T rate = dot(qrot(q, axc), w - wpo);  // joint_velocity, solver.cpp:413-417
+        o[11 + jnt] = float(ang);
+        o[11 + J + jnt] = float(rate);
+        o[11 + 2 * J + jnt] = float(ltau);
+      }
+      if (a.task.height_map) {
+        const double rx = ox + double(xr2.x), ry = oy + double(xr2.y);
+        for (int k = b; k < 165; k += W) {
+          const int i = k / 11, jj = k % 11;
+          const double fx = geo_offset(i - 7), fy = geo_offset(jj - 5);
+          const double px = rx + double(cy) * fx - double(sy) * fy;
+          const double py = ry + double(sy) * fx + double(cy) * fy;
+          o[11 + 3 * J + M.n_feet + k] = float(terrain_height_dev(a.boxes, a.n_boxes, px, py) - double(xr2.z));
+        }
+      }
+    }
+  }
+
+  // ---------------- re-centre the env origin on the root (fp32 range) -----
+  {
+    const T rx = from<W>(x.x, M.root, mask), ry = from<W>(x.y, M.root, mask);
+    const T sx = fabs(rx) >= T(1) ? T(rint(rx)) : T(0);
+    const T sy = fabs(ry) >= T(1) ? T(rint(ry)) : T(0);
+    if (sx != T(0) || sy != T(0)) {
+      x.x -= sx;
+      x.y -= sy;
+      tx -= sx;
+      ty -= sy;
+      ox += double(sx);
+      oy += double(sy);
+    }
+  }
+
+  // ---------------- store ---------------------------------------------------
+  if (act) {
+    a.state[sbase + 0 * W] = x.x;
+    a.state[sbase + 1 * W] = x.y;
+    a.state[sbase + 2 * W] = x.z;
+    a.state[sbase + 3 * W] = q.w;
+    a.state[sbase + 4 * W] = q.x;
+    a.state[sbase + 5 * W] = q.y;
+    a.state[sbase + 6 * W] = q.z;
+    a.state[sbase + 7 * W] = v.x;
+    a.state[sbase + 8 * W] = v.y;
+    a.state[sbase + 9 * W] = v.z;
+    a.state[sbase + 10 * W] = w.x;
+    a.state[sbase + 11 * W] = w.y;
+    a.state[sbase + 12 * W] = w.z;
+  }
+  if (b == 0) {
+    a.origin[2 * e] = ox;
+    a.origin[2 * e + 1] = oy;
+    if (a.target) {
+      a.target[2 * e] = tx;
+      a.target[2 * e + 1] = ty;
+    }
+    if (a.counters)
+      for (int k = 0; k < 8; ++k) a.counters[size_t(e) * 8 + k] = cnt[k];
+    if (a.mode != 2) {
+      if (a.newton_out) a.newton_out[e] = newton_done;
+      if (a.krylov_out) a.krylov_out[e] = krylov_total;
+      if (a.failed_out) a.failed_out[e] = step_failed ? 1 : 0;
+    }
+  }
+  if (a.mode != 2 && a.overflow_out) {
+    const bool ov = __any_sync(mask, overflow);
+    if (b == 0) a.overflow_out[e] = ov ? 1 : 0;
+  }
+}
+
+template <class T, int W, int CPB>
+static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
+  constexpr int threads = 128;
+  const size_t smem = size_t(threads / 32) * 64 * 32 * sizeof(T);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t err = cudaFuncSetAttribute(k_env_step<T, W, CPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(smem));
+    if (err != cudaSuccess) return err;
+    configured = true;
+  }
+  const long long total = (long long)a.n * W;
+  const int blocks = int((total + threads - 1) / threads);
+  k_env_step<T, W, CPB><<<blocks, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s) {
+  if (lanes == 32) {
+    if (cpb <= 2) return launch_one<T, 32, 2>(a, s);
+    return launch_one<T, 32, 8>(a, s);
+  }
+  if (lanes == 16) {
+    if (cpb <= 2) return launch_one<T, 16, 2>(a, s);
+    return launch_one<T, 16, 8>(a, s);
+  }
+  if (cpb <= 2) return launch_one<T, 8, 2>(a, s);
+  return launch_one<T, 8, 8>(a, s);
+}
+
+}  // namespace stp

@@ -1,0 +1,5 @@
+#include "sim_step.cuh"
+
+namespace stp {
+template cudaError_t launch_env_step<double>(const KArgs<double>&, int, int, cudaStream_t);
+}  // namespace stp
