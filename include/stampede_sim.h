@@ -173,6 +173,10 @@ int stp_generate_terrain(const stp_terrain_spec* spec, stp_static_box* out, int3
 /* terrain_height, collide.cpp:348-359 (host, double; used by tests). */
 double stp_terrain_height(const stp_static_box* boxes, int32_t n, double x, double y);
 
+/* sizeof every ABI struct, for binding layout checks: stp_body, stp_joint,
+ * stp_model, stp_step_config, stp_static_box, stp_terrain_spec, stp_task. */
+void stp_struct_sizes(int64_t out[7]);
+
 /* --- handle lifecycle ------------------------------------------------------ */
 /* Creates n_envs environments of `model` on CUDA device `device`.
  * env_offset = global index of this handle's first env (rank * n_envs for a

@@ -136,6 +136,7 @@ _I32 = C.c_int32
 SIGNATURES = [
     ("stp_abi_version", _I, []),
     ("stp_last_error", C.c_char_p, []),
+    ("stp_struct_sizes", None, [C.POINTER(C.c_int64)]),
     ("stp_default_step_config", None, [C.POINTER(StepConfig)]),
     ("stp_builtin_model", _I, [C.c_char_p, C.POINTER(Model)]),
     ("stp_validate_model", _I, [C.POINTER(Model)]),

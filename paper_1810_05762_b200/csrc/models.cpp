@@ -217,6 +217,16 @@ int stp_abi_version(void) { return STP_ABI_VERSION; }
 
 const char* stp_last_error(void) { return stp::last_error_cstr(); }
 
+void stp_struct_sizes(int64_t out[7]) {
+  out[0] = sizeof(stp_body);
+  out[1] = sizeof(stp_joint);
+  out[2] = sizeof(stp_model);
+  out[3] = sizeof(stp_step_config);
+  out[4] = sizeof(stp_static_box);
+  out[5] = sizeof(stp_terrain_spec);
+  out[6] = sizeof(stp_task);
+}
+
 void stp_default_step_config(stp_step_config* c) {
   if (!c) return;
   std::memset(c, 0, sizeof(*c));

@@ -135,7 +135,10 @@ class VecEnv:
         return obs
 
     def step(self, actions, obs=None, reward=None, done=None):
-        """SPEC env_step on device tensors; async on torch's current stream."""
+        """SPEC env_step on device tensors; async on torch's current stream.
+        A numpy array routes through the host-buffer entry (stp_step_host)."""
+        if isinstance(actions, np.ndarray):
+            return self.step_host(actions, obs, reward, done)
         import torch
         dev = f"cuda:{self.device}"
         if actions.shape != (self.n_envs, self.action_dim):

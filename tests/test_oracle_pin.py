@@ -1,0 +1,98 @@
+"""Pins the CPU restatement (oracle/phys_oracle.hpp + env layer) to the
+reference: golden fixtures produced by the compiled, unmodified reference
+(tests/golden/make_golden.py) and, when oracle/_ref is built, a direct
+bit-for-bit comparison."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1810_05762_b200 import abi
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _env(name, kind="restatement", n=None, seed=None, precision="f64"):
+    g = np.load(os.path.join(GOLDEN, f"golden_{name}.npz"))
+    model = abi.builtin_model(name)
+    task = abi.default_task(abi.TASK_ANT if name == "ant" else abi.TASK_HUMANOID)
+    cfg = abi.default_step_config()
+    env = oracle.OracleEnv(model, task, cfg, int(n or g["n"]), seed=int(seed or g["seed"]), kind=kind,
+                           precision=precision)
+    return env, g
+
+
+@pytest.mark.parametrize("name", ["ant", "humanoid"])
+def test_restatement_replays_reference_golden(name):
+    env, g = _env(name)
+    for t in range(int(g["steps"])):
+        np.testing.assert_array_equal(env.get_state(), g["pre"][t])
+        o, r, d = env.step(g["actions"][t])
+        np.testing.assert_allclose(env.get_state(), g["post"][t], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(r, g["reward"][t], rtol=0, atol=1e-12)
+        np.testing.assert_array_equal(d, g["done"][t])
+        np.testing.assert_allclose(o, g["obs"][t], rtol=0, atol=1e-12)
+        c = env.contact_arrays(64)
+        np.testing.assert_array_equal(c["count"], g["contact_count"][t])
+        np.testing.assert_array_equal(c["body_a"], g["contact_body"][t])
+        np.testing.assert_allclose(c["separation"], g["contact_sep"][t], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["ant", "humanoid"])
+def test_restatement_bit_exact_vs_compiled_reference(name):
+    if not oracle.available("reference"):
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    a, _ = _env(name, "restatement", n=32, seed=99)
+    b, _ = _env(name, "reference", n=32, seed=99)
+    for t in range(60):
+        act = a.random_actions(t)
+        oa, ra, da = a.step(act)
+        ob, rb, db = b.step(act)
+        np.testing.assert_array_equal(a.get_state(), b.get_state())
+        np.testing.assert_array_equal(ra, rb)
+        np.testing.assert_array_equal(da, db)
+        np.testing.assert_array_equal(oa, ob)
+
+
+def test_assembly_quirk_pattern():
+    """Reference aliasing quirk (solver.cpp:350-351 + block_sparse.cpp:218):
+    the Humanoid's assembled H is symmetric, the Ant's loses anchor row 0 of
+    joint 3 in block (3, 4) only; the restatement reproduces the reference's
+    matrix bit-for-bit either way."""
+    for name, sym in [("humanoid", True), ("ant", False)]:
+        env, _ = _env(name, n=1, seed=5)
+        tq = np.zeros(env.action_dim)
+        H, rhs, _ = env.first_system(0, tq)
+        if oracle.available("reference"):
+            ref, _ = _env(name, "reference", n=1, seed=5)
+            Hr, rr, _ = ref.first_system(0, tq, reference=True)
+            np.testing.assert_array_equal(H, Hr)
+            np.testing.assert_array_equal(rhs, rr)
+        asym = np.abs(H - H.T)
+        blocks = {(i // 6, j // 6) for i, j in zip(*np.nonzero(asym > 1e-9 * np.abs(H).max()))}
+        if sym:
+            assert not blocks
+        else:
+            assert blocks == {(3, 4), (4, 3)}
+
+
+def test_f32_restatement_envelope():
+    """The fp32 instantiation of the reference algorithm stays within the
+    SURVEY §8(c) one-step envelope of the double oracle (teacher-forced)."""
+    d64, _ = _env("humanoid", n=16, seed=3)
+    d32, _ = _env("humanoid", n=16, seed=3, precision="f32")
+    tm = np.array([d64.model.joints[j].max_torque for j in range(d64.action_dim)])
+    dx, dv = [], []
+    for t in range(60):
+        s = d64.get_state()
+        d32.set_state(s)
+        tq = d64.random_actions(t) * tm
+        d64.physics_step(tq)
+        d32.physics_step(tq)
+        a, b = d64.get_state(), d32.get_state()
+        dx.append(np.abs(a[..., :3] - b[..., :3]).max(axis=(1, 2)))
+        dv.append(np.abs(a[..., 7:] - b[..., 7:]).max(axis=(1, 2)) / np.maximum(1, np.abs(a[..., 7:]).max(axis=(1, 2))))
+    dx, dv = np.concatenate(dx), np.concatenate(dv)
+    assert np.percentile(dx, 99) <= 1e-4 and dx.max() <= 5e-3
+    assert np.median(dv) <= 2e-3 and np.percentile(dv, 99) <= 1e-1
