@@ -28,6 +28,8 @@ struct DevModel {
   int feet[STP_MAX_FEET];
   int shape[32], is_static[32], parent[32], joint[32], child_mask[32], depth[32], quirk[32];
   int max_depth;
+  int child_list[4][32];  // up to 4 child bodies per body (-1 = none)
+  int max_children;
   int lane_of_joint[STP_MAX_JOINTS];
   T radius[32], half_len[32], hext[3][32], lpos[3][32], lrot[4][32];
   T mass[32], inv_mass[32], inertia[3][32], inv_inertia[3][32];

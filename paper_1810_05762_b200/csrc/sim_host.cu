@@ -171,6 +171,15 @@ void build_dev_model(const stp_model& m, const stp_step_config& cfg, stp::DevMod
       ++pair_index;
     }
   }
+  for (int k = 0; k < 4; ++k)
+    for (int b = 0; b < 32; ++b) d.child_list[k][b] = -1;
+  d.max_children = 0;
+  for (int b = 0; b < m.n_bodies; ++b) {
+    int n = 0;
+    for (int c = 0; c < m.n_bodies; ++c)
+      if ((d.child_mask[b] >> c) & 1) d.child_list[n++ < 4 ? n - 1 : 3][b] = c;
+    d.max_children = std::max(d.max_children, n);
+  }
   int maxd = 0;
   for (int b = 0; b < m.n_bodies; ++b) {  // topological order: parent < child
     d.depth[b] = d.parent[b] < 0 ? 0 : d.depth[d.parent[b]] + 1;
@@ -320,6 +329,14 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
   }
   if (stp_validate_model(model) != STP_OK) return nullptr;
   if (validate_cfg(*cfg) != STP_OK) return nullptr;
+  for (int b = 0; b < model->n_bodies; ++b) {
+    int kids = 0;
+    for (int j = 0; j < model->n_joints; ++j) kids += model->joints[j].parent == b;
+    if (kids > 4) {
+      fail(STP_EINVAL, "model: the GPU path supports at most 4 child joints per body");
+      return nullptr;
+    }
+  }
   if (!single_island(*model)) {
     fail(STP_EINVAL, "model: the GPU path needs every env's dynamic bodies joint-connected (one island per env)");
     return nullptr;

@@ -1,7 +1,15 @@
-// Fused environment-step kernel (K1 contacts + K2 solve + K3 epilogue).
-// See sim_kernels.cuh for the execution model; every block below cites the
-// reference lines it re-implements.  Instantiated per precision in
-// sim_step_f32.cu / sim_step_f64.cu (parallel compilation).
+// Fused environment-step kernel (K1 contacts + K2 solve + K3 epilogue), v2.
+//
+// Execution model: one warp segment of W lanes = one env,
+// lane b = body b.  Per-lane state that persists across the Newton loop but
+// is read only once per Newton iteration (constant part of the diagonal
+// block, constraint-row data, contacts) lives in shared memory, so the PCR
+// inner loop keeps only its vectors, the diagonal block and the explicit
+// block-Jacobi inverse in registers (occupancy: 4 blocks x 4 warps / SM).
+// Per PCR iteration there are two segment reductions (the reference's
+// ||r|| and z.Az are fused into one butterfly).
+//
+// Instantiated per precision in sim_step_f32.cu / sim_step_f64.cu.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -10,9 +18,181 @@
 
 namespace stp {
 
+// Per-warp shared-memory rows; each row holds one T per warp lane.
+constexpr int R_HOFF = 0;   // 36: H(child, parent), row-major 6x6
+constexpr int R_SCAT = 36;  // 9: child -> parent gather buffer
+constexpr int R_HEQ = 45;   // 27: constant diagonal block (21, packed) + rhs (6)
+constexpr int R_LIM = 72;   // 7: limit axis (3), d_lo, d_hi, b_lo, b_hi
+constexpr int R_QRK = 79;   // 7: quirk d0, ja angular (3), jb angular (3)
+constexpr int R_CT = 86;    // 11 per contact slot: n(3) r(3) t1(3) d b
+template <int CPB>
+__host__ __device__ constexpr int smem_rows() {
+  return R_CT + 11 * CPB;
+}
+
+template <class T, int W>
+struct Lane {
+  T* sm;
+  unsigned mask;
+  int lane, base, b, par_src, maxc;
+  int kid[4];  // child lanes (-1 = none)
+  bool has_off, quirk;
+  T lim_s;  // -(sum of active limit weights): angular rank-1 term of H(c,p)
+  v3<T> lim_a;
+
+  __device__ __forceinline__ T& at(int row) const { return sm[row * 32 + lane]; }
+  __device__ __forceinline__ T at_kid(int row, int k) const { return sm[row * 32 + base + k]; }
+
+  // out = sum over children of v (parent side of a child's contribution)
+  template <int K>
+  __device__ __forceinline__ void gather(const T (&v)[K], T (&out)[K]) const {
+    static_assert(K <= 9, "scatter buffer holds 9 values");
+#pragma unroll
+    for (int k = 0; k < K; ++k) at(R_SCAT + k) = v[k];
+    __syncwarp(mask);
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = T(0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i < maxc && kid[i] >= 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) out[k] += at_kid(R_SCAT + k, kid[i]);
+      }
+    }
+    __syncwarp(mask);
+  }
+
+  // y = H v over the segment's block tree (BlockSparseSym::apply,
+  // block_sparse.cpp:233-251): own diagonal block, H(b, parent) v_parent,
+  // and sum over children of H(child, b)^T v_child (+ the rank-1 limit and
+  // aliasing-quirk terms).
+  __device__ __forceinline__ void apply(const T (&H)[21], const T (&v)[6], T (&y)[6]) const {
+    T vp[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) vp[k] = __shfl_sync(mask, v[k], par_src, W);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      T s = T(0);
+#pragma unroll
+      for (int c = 0; c < 6; ++c) s += H[sidx(r, c)] * v[c];
+      y[r] = s;
+    }
+    T t[6] = {0, 0, 0, 0, 0, 0};
+    if (has_off) {
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        T s = T(0);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const T h = at(R_HOFF + r * 6 + c);
+          s += h * vp[c];
+          t[c] += h * v[r];
+        }
+        y[r] += s;
+      }
+      if (lim_s != T(0)) {
+        const T ap = lim_a.x * vp[3] + lim_a.y * vp[4] + lim_a.z * vp[5];
+        const T ac = lim_a.x * v[3] + lim_a.y * v[4] + lim_a.z * v[5];
+        y[3] += lim_s * lim_a.x * ap;
+        y[4] += lim_s * lim_a.y * ap;
+        y[5] += lim_s * lim_a.z * ap;
+        t[3] += lim_s * lim_a.x * ac;
+        t[4] += lim_s * lim_a.y * ac;
+        t[5] += lim_s * lim_a.z * ac;
+      }
+      if (quirk) {  // H(p,c) = H(c,p)^T - d0 ja0 jb0^T, ja0 = (-e_x, a), jb0 = (e_x, c)
+        const T d0 = at(R_QRK);
+        const T s0 = d0 * (v[0] + at(R_QRK + 4) * v[3] + at(R_QRK + 5) * v[4] + at(R_QRK + 6) * v[5]);
+        t[0] += s0;
+        t[3] -= s0 * at(R_QRK + 1);
+        t[4] -= s0 * at(R_QRK + 2);
+        t[5] -= s0 * at(R_QRK + 3);
+      }
+    }
+    T g[6];
+    gather<6>(t, g);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) y[k] += g[k];
+  }
+};
+
+// explicit inverse of the packed SPD 6x6 block (block-Jacobi preconditioner,
+// krylov.cpp:60-88, mathematically the reference's cholesky_solve pair);
+// identity when the block is not positive definite (krylov.cpp:76-80).
+template <class T>
+__device__ __forceinline__ void block_inverse(const T (&H)[21], T (&P)[21], bool dyn) {
+  T L[21];
+  bool ok = dyn;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      T s = H[tri(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s -= L[tri(i, k)] * L[tri(j, k)];
+      if (i == j) {
+        ok = ok && (s > T(0));
+        L[tri(i, i)] = T(1) / sqrt(s);  // store the reciprocal diagonal
+      } else {
+        L[tri(i, j)] = s * L[tri(j, j)];
+      }
+    }
+  }
+  if (!ok) {
+#pragma unroll
+    for (int k = 0; k < 21; ++k) P[k] = T(0);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) P[tri(i, i)] = T(1);
+    return;
+  }
+  // M = L^-1 (lower), L has reciprocal diagonal stored
+  T M[21];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    M[tri(i, i)] = L[tri(i, i)];
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+      T s = T(0);
+#pragma unroll
+      for (int k = j; k < i; ++k) s += L[tri(i, k)] * M[tri(k, j)];
+      M[tri(i, j)] = -s * L[tri(i, i)];
+    }
+  }
+  // P = M^T M
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      T s = T(0);
+#pragma unroll
+      for (int k = i; k < 6; ++k) s += M[tri(k, i)] * M[tri(k, j)];
+      P[tri(i, j)] = s;
+    }
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void symv(const T (&P)[21], const T (&v)[6], T (&y)[6]) {
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    T s = T(0);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) s += P[sidx(r, c)] * v[c];
+    y[r] = s;
+  }
+}
+
+template <int W, class T>
+__device__ __forceinline__ void seg_sum2(T& a, T& b, unsigned mask) {
+#pragma unroll
+  for (int off = W / 2; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(mask, a, off, W);
+    b += __shfl_xor_sync(mask, b, off, W);
+  }
+}
 
 template <class T, int W, int CPB>
-__global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
+__global__ void __launch_bounds__(128, (sizeof(T) == 4 ? 4 : 1)) k_env_step(const KArgs<T> a) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int e = tid / W;
   if (e >= a.n) return;  // whole segments exit together
@@ -31,27 +211,27 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
   const int J = M.nj;
 
   extern __shared__ unsigned char smem_raw[];
-  T* wsm = reinterpret_cast<T*>(smem_raw) + (threadIdx.x >> 5) * (64 * 32);
-  Tree<T, W> tree;
-  tree.mask = mask;
-  tree.lane = lane;
-  tree.base = base;
-  tree.b = b;
-  tree.par_src = par_src;
-  tree.has_off = dyn && pdyn && jnt >= 0;
-  tree.cmask = act ? uint32_t(M.child_mask[b]) : 0u;
-  tree.hoff = wsm;
-  tree.scat = wsm + 36 * 32;
-  tree.lim_s = T(0);
-  tree.lim_a = {0, 0, 0};
-  tree.quirk = false;
-
-  // ---- task state (every lane keeps a copy; lane 0 writes back) ----------
-  int32_t cnt[8];
+  Lane<T, W> L;
+  L.sm = reinterpret_cast<T*>(smem_raw) + (threadIdx.x >> 5) * (smem_rows<CPB>() * 32);
+  L.mask = mask;
+  L.lane = lane;
+  L.base = base;
+  L.b = b;
+  L.par_src = par_src;
+  L.maxc = M.max_children;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) cnt[k] = a.counters ? a.counters[size_t(e) * 8 + k] : 0;
-  double ox = a.origin[2 * e], oy = a.origin[2 * e + 1];
-  T tx = a.target ? a.target[2 * e] : T(0), ty = a.target ? a.target[2 * e + 1] : T(0);
+  for (int i = 0; i < 4; ++i) L.kid[i] = act ? M.child_list[i][b] : -1;
+  L.has_off = dyn && pdyn && jnt >= 0;
+  L.quirk = false;
+  L.lim_s = T(0);
+  L.lim_a = {0, 0, 0};
+
+  // Task state, origin and the pre-step pose are (re)loaded from global
+  // memory where needed instead of being kept live across the solve.
+  auto load_counters = [&](int32_t (&c)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = a.counters ? a.counters[size_t(e) * 8 + k] : 0;
+  };
 
   // ---- load body state (SoA, coalesced per field) ------------------------
   const size_t sbase = size_t(e) * kStateFields * W + b;
@@ -69,12 +249,20 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
   bool overflow = false;
   int nc = 0;
   int newton_done = 0, krylov_total = 0;
-  T prev_rx = from<W>(x.x, M.root, mask), prev_ry = from<W>(x.y, M.root, mask);
   bool perturbed = false;
+  int32_t cnt[8];
+  double ox, oy;
+  T tx, ty, ltau;
+  unsigned feet_bits;
 
-  T ltau = (jnt >= 0 && a.last_tau) ? a.last_tau[size_t(e) * J + jnt] : T(0);
-  unsigned feet_bits = a.feet ? a.feet[e] : 0u;
   if (a.mode == 2) {
+    load_counters(cnt);
+    ox = a.origin[2 * e];
+    oy = a.origin[2 * e + 1];
+    tx = a.target ? a.target[2 * e] : T(0);
+    ty = a.target ? a.target[2 * e + 1] : T(0);
+    ltau = (jnt >= 0 && a.last_tau) ? a.last_tau[size_t(e) * J + jnt] : T(0);
+    feet_bits = a.feet ? a.feet[e] : 0u;
     // ---------------- reset only ------------------------
     const bool doit = a.reset_mask == nullptr || a.reset_mask[e];
     if (doit) {
@@ -103,11 +291,13 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
       for (int k = 0; k < 6; ++k) a.loads[lb + k * W] = T(0);  // clear_external_loads
     }
     // perturbation schedule (apply_perturbations)
-    if (a.mode == 1 && a.task.perturb_max > 0 && cnt[C_FRAME] == cnt[C_NEXTP]) {
+    if (a.mode == 1 && a.task.perturb_max > 0 &&
+        a.counters[size_t(e) * 8 + C_FRAME] == a.counters[size_t(e) * 8 + C_NEXTP]) {
       perturbed = true;
       if (b == M.root) {
         const uint64_t genv = uint64_t(a.env_offset + e);
-        const uint64_t ps = stp_derive_seed(a.seed, STP_TAG_PERTURB, (genv << 32) | uint32_t(cnt[C_PERTDRAW]));
+        const uint64_t ps = stp_derive_seed(a.seed, STP_TAG_PERTURB,
+                                            (genv << 32) | uint32_t(a.counters[size_t(e) * 8 + C_PERTDRAW]));
         const double f = a.task.force_lo + (a.task.force_hi - a.task.force_lo) * stp_uniform(ps, 1);
         const double phi = 2.0 * M_PI * stp_uniform(ps, 2);
         fext.x += T(f * cos(phi));
@@ -116,23 +306,18 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
     }
 
     // ---------------- K1: contacts (detect_contacts, collide.cpp:270-299) -
-    v3<T> c_n[CPB], c_r[CPB];  // normal, lever arm (point - x)
-    T c_sep[CPB];
-#pragma unroll
-    for (int k = 0; k < CPB; ++k) {
-      c_n[k] = {0, 0, 1};
-      c_r[k] = {0, 0, 0};
-      c_sep[k] = T(0);
-    }
+    // slot k of this lane: rows R_CT + 11k: n(3) r(3) t1(3) d b; sep kept in d's row until rows are built
     auto add_contact = [&](v3<T> p, v3<T> n, T sep) {
       if (nc < CPB) {
-#pragma unroll
-        for (int k = 0; k < CPB; ++k)
-          if (k == nc) {
-            c_n[k] = n;
-            c_r[k] = p - x;
-            c_sep[k] = sep;
-          }
+        const int r0 = R_CT + 11 * nc;
+        const v3<T> r = p - x;
+        L.at(r0 + 0) = n.x;
+        L.at(r0 + 1) = n.y;
+        L.at(r0 + 2) = n.z;
+        L.at(r0 + 3) = r.x;
+        L.at(r0 + 4) = r.y;
+        L.at(r0 + 5) = r.z;
+        L.at(r0 + 10) = sep;
         ++nc;
       } else {
         overflow = true;
@@ -186,13 +371,12 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
       }
       // static terrain boxes (collide.cpp:287-298), in box-index order
       if (a.n_boxes > 0 && shp != STP_BOX) {
-        v3<T> lo, hi;
-        lo = {min(p0.x, p1.x) - rad, min(p0.y, p1.y) - rad, min(p0.z, p1.z) - rad};
-        hi = {max(p0.x, p1.x) + rad, max(p0.y, p1.y) + rad, max(p0.z, p1.z) + rad};
+        const double ox = a.origin[2 * e], oy = a.origin[2 * e + 1];
+        const v3<T> lo{min(p0.x, p1.x) - rad, min(p0.y, p1.y) - rad, min(p0.z, p1.z) - rad};
+        const v3<T> hi{max(p0.x, p1.x) + rad, max(p0.y, p1.y) + rad, max(p0.z, p1.z) + rad};
         for (int i = 0; i < a.n_boxes; ++i) {
           const double* bx = a.boxes + 8 * i;
-          // box centre relative to the env origin, exact in double first
-          const v3<T> c{T(bx[0] - ox), T(bx[1] - oy), T(bx[2])};
+          const v3<T> c{T(bx[0] - ox), T(bx[1] - oy), T(bx[2])};  // relative to the env origin
           const v3<T> h{T(bx[3]), T(bx[4]), T(bx[5])};
           const T ex = h.x + h.y;
           if (hi.x + margin < c.x - ex || lo.x - margin > c.x + ex || hi.y + margin < c.y - ex ||
@@ -225,9 +409,16 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
               sgn = loc.z >= T(0) ? T(1) : T(-1);
             }
             v3<T> ln{0, 0, 0}, ls = loc;
-            if (axis == 0) { ln.x = sgn; ls.x = sgn * h.x; }
-            else if (axis == 1) { ln.y = sgn; ls.y = sgn * h.y; }
-            else { ln.z = sgn; ls.z = sgn * h.z; }
+            if (axis == 0) {
+              ln.x = sgn;
+              ls.x = sgn * h.x;
+            } else if (axis == 1) {
+              ln.y = sgn;
+              ls.y = sgn * h.y;
+            } else {
+              ln.z = sgn;
+              ls.z = sgn * h.z;
+            }
             surf = {c.x + cs * ls.x - sn * ls.y, c.y + sn * ls.x + cs * ls.y, c.z + ls.z};
             nrm = {cs * ln.x - sn * ln.y, sn * ln.x + cs * ln.y, ln.z};
             return -best;
@@ -272,28 +463,25 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
     // ---------------- body dynamics (body_dynamics, solver.cpp:230-262) ---
     const qt<T> qp = from<W>(q, par_src, mask);
     v3<T> torque = text;
-    v3<T> jt{0, 0, 0};  // torque this joint applies to the child (+) / parent (-)
-    if (jnt >= 0) {
-      jt = qrot(qp, ldv(M.ax_p, b)) * tau;  // parent's axis (solver.cpp:240)
-      torque = torque + jt;
-    }
     {
+      v3<T> jt{0, 0, 0};  // this joint's torque: + on the child, - on the parent
+      if (jnt >= 0) {
+        jt = qrot(qp, ldv(M.ax_p, b)) * tau;  // parent's axis (solver.cpp:240)
+        torque = torque + jt;
+      }
       T mine[3] = {jt.x, jt.y, jt.z}, kids[3];
-      tree.gather<3>(mine, kids);
+      L.gather<3>(mine, kids);
       torque = torque - v3<T>{kids[0], kids[1], kids[2]};
     }
-    T Rm[9];
-    rot_mat(q, Rm);
+    sym3<T> Iw{0, 0, 0, 0, 0, 0}, Iinv{0, 0, 0, 0, 0, 0};
     const T inv_m = dyn ? M.inv_mass[b] : T(0);
     const T mass = dyn ? M.mass[b] : T(0);
-    sym3<T> Iw = rdrt(Rm, M.inertia[0][b], M.inertia[1][b], M.inertia[2][b]);
-    sym3<T> Iinv = rdrt(Rm, M.inv_inertia[0][b], M.inv_inertia[1][b], M.inv_inertia[2][b]);
-    if (!dyn) {
-      Iw = {0, 0, 0, 0, 0, 0};
-      Iinv = {0, 0, 0, 0, 0, 0};
-    }
     v3<T> vfree{0, 0, 0}, wfree{0, 0, 0};
     if (dyn) {
+      T Rm[9];
+      rot_mat(q, Rm);
+      Iw = rdrt(Rm, M.inertia[0][b], M.inertia[1][b], M.inertia[2][b]);
+      Iinv = rdrt(Rm, M.inv_inertia[0][b], M.inv_inertia[1][b], M.inv_inertia[2][b]);
       const v3<T> force = v3<T>{cf.gx, cf.gy, cf.gz} * mass + fext;
       vfree = v + force * (cf.dt * inv_m);
       // implicit_gyro, solver.cpp:216-226
@@ -302,26 +490,17 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
       for (int it = 0; it < 2; ++it) {
         const v3<T> iw = smul(Iw, wg);
         const v3<T> f = iw + cross(wg, iw) * cf.dt - mom;
-        // jac = I + (skew(w) I - skew(Iw)) dt
         const T I00 = Iw.xx, I01 = Iw.xy, I02 = Iw.xz, I11 = Iw.yy, I12 = Iw.yz, I22 = Iw.zz;
-        T jm[9];
-        // skew(w) * I
+        T jm[9];  // skew(w) I - skew(I w)
         jm[0] = -wg.z * I01 + wg.y * I02;
-        jm[1] = -wg.z * I11 + wg.y * I12;
-        jm[2] = -wg.z * I12 + wg.y * I22;
-        jm[3] = wg.z * I00 - wg.x * I02;
+        jm[1] = -wg.z * I11 + wg.y * I12 + iw.z;
+        jm[2] = -wg.z * I12 + wg.y * I22 - iw.y;
+        jm[3] = wg.z * I00 - wg.x * I02 - iw.z;
         jm[4] = wg.z * I01 - wg.x * I12;
-        jm[5] = wg.z * I02 - wg.x * I22;
-        jm[6] = -wg.y * I00 + wg.x * I01;
-        jm[7] = -wg.y * I01 + wg.x * I11;
+        jm[5] = wg.z * I02 - wg.x * I22 + iw.x;
+        jm[6] = -wg.y * I00 + wg.x * I01 + iw.y;
+        jm[7] = -wg.y * I01 + wg.x * I11 - iw.x;
         jm[8] = -wg.y * I02 + wg.x * I12;
-        // - skew(iw)
-        jm[1] += iw.z;
-        jm[2] -= iw.y;
-        jm[3] -= iw.z;
-        jm[5] += iw.x;
-        jm[6] += iw.y;
-        jm[7] -= iw.x;
         const T A[9] = {I00 + jm[0] * cf.dt, I01 + jm[1] * cf.dt, I02 + jm[2] * cf.dt,
                         I01 + jm[3] * cf.dt, I11 + jm[4] * cf.dt, I12 + jm[5] * cf.dt,
                         I02 + jm[6] * cf.dt, I12 + jm[7] * cf.dt, I22 + jm[8] * cf.dt};
@@ -340,226 +519,215 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
 
     // ---------------- joint rows (build_rows, solver.cpp:105-174) --------
     const T bdt = cf.beta / cf.dt;
-    const v3<T> xp = from<W>(x, par_src, mask);
-    const v3<T> wp = from<W>(w, par_src, mask);
-    const T p_invm = from<W>(inv_m, par_src, mask);
-    sym3<T> pIinv;
-    pIinv.xx = from<W>(Iinv.xx, par_src, mask);
-    pIinv.yy = from<W>(Iinv.yy, par_src, mask);
-    pIinv.zz = from<W>(Iinv.zz, par_src, mask);
-    pIinv.xy = from<W>(Iinv.xy, par_src, mask);
-    pIinv.xz = from<W>(Iinv.xz, par_src, mask);
-    pIinv.yz = from<W>(Iinv.yz, par_src, mask);
     const bool has_joint = dyn && jnt >= 0;
-    // equality rows: 3 anchor + 2 angular; ja/jb per row
-    T eq_d[5] = {0, 0, 0, 0, 0}, eq_bias[5] = {0, 0, 0, 0, 0};
-    v3<T> ra{0, 0, 0}, rb{0, 0, 0}, t1{0, 0, 0}, t2{0, 0, 0};
-    v3<T> axw{0, 0, 0};
-    T d_lo = 0, d_hi = 0, b_lo = 0, b_hi = 0;
-    bool has_lo = false, has_hi = false;
-    if (has_joint) {
-      ra = qrot(qp, ldv(M.anc_p, b));
-      rb = qrot(q, ldv(M.anc_c, b));
-      const v3<T> cpos = (x + rb) - (xp + ra);
+    T Hown[21];  // constant part of this lane's diagonal block
+    T rhs_own[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const v3<T> ek{T(k == 0), T(k == 1), T(k == 2)};
-        T wsum = T(0);
-        if (pdyn) {
-          wsum += p_invm * T(1);
-          wsum += quad(pIinv, -cross(ra, ek));
-        }
-        wsum += inv_m * T(1);
-        wsum += quad(Iinv, cross(rb, ek));
-        eq_d[k] = cf.kj * (wsum > T(1e-12) ? T(1) / wsum : T(0));  // effective_mass :69-80
-        eq_bias[k] = -bdt * comp(cpos, k);
-      }
-      const v3<T> aw = qrot(qp, ldv(M.ax_p, b));
-      const v3<T> bw = qrot(q, ldv(M.ax_c, b));
-      const v3<T> ref = fabs(aw.z) < T(0.9) ? v3<T>{0, 0, 1} : v3<T>{1, 0, 0};
-      t1 = vunit(cross(aw, ref));
-      t2 = cross(aw, t1);
-      const v3<T> err = cross(aw, bw);
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const v3<T> t = k == 0 ? t1 : t2;
-        T wsum = T(0);
-        if (pdyn) wsum += quad(pIinv, -t);
-        wsum += quad(Iinv, t);
-        eq_d[3 + k] = cf.kj * (wsum > T(1e-12) ? T(1) / wsum : T(0));
-        eq_bias[3 + k] = -bdt * dot(t, err);
-      }
-      // speculative limits (solver.cpp:144-173)
-      const qt<T> rest{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]};
-      const v3<T> axc = ldv(M.ax_c, b);
-      const T angle = hinge_angle(qp, q, rest, axc);
-      axw = qrot(q, axc);
-      const T rate = dot(axw, w - wp);
-      const T lo_gap = angle - M.lim_lo[b];
-      const T hi_gap = M.lim_hi[b] - angle;
-      const T travel = T(1.5) * fabs(rate) * cf.dt;
-      const T thr = max(cf.lim_act, travel);
-      T wl = T(0);
-      if (pdyn) wl += quad(pIinv, axw);
-      wl += quad(Iinv, axw);
-      const T meff = wl > T(1e-12) ? T(1) / wl : T(0);
-      if (lo_gap < thr) {
-        has_lo = true;
-        d_lo = cf.kl * meff;
-        b_lo = uni_bias(lo_gap, cf.beta, cf.dt);
-      }
-      if (hi_gap < thr) {
-        has_hi = true;
-        d_hi = cf.kl * meff;
-        b_hi = uni_bias(hi_gap, cf.beta, cf.dt);
-      }
-      if (M.quirk[b]) {
-        tree.quirk = true;
-        tree.q_d0 = eq_d[0];
-        const v3<T> ca = -cross(ra, v3<T>{1, 0, 0});
-        const v3<T> cb = cross(rb, v3<T>{1, 0, 0});
-        tree.q_ja[0] = T(-1); tree.q_ja[1] = 0; tree.q_ja[2] = 0;
-        tree.q_ja[3] = ca.x; tree.q_ja[4] = ca.y; tree.q_ja[5] = ca.z;
-        tree.q_jb[0] = T(1); tree.q_jb[1] = 0; tree.q_jb[2] = 0;
-        tree.q_jb[3] = cb.x; tree.q_jb[4] = cb.y; tree.q_jb[5] = cb.z;
-      }
-    }
-    // contact rows (solver.cpp:176-210): per contact normal + 2 tangents
-    T c_d[CPB], c_b[CPB];
-    v3<T> c_t1[CPB];
-#pragma unroll
-    for (int k = 0; k < CPB; ++k) {
-      c_d[k] = T(0);
-      c_b[k] = T(0);
-      c_t1[k] = {1, 0, 0};
-      if (k < nc) {
-        const v3<T> n = c_n[k];
-        const v3<T> rn = cross(c_r[k], n);
-        T wsum = inv_m * dot(n, n);
-        wsum += quad(Iinv, rn);
-        c_d[k] = cf.kc * (wsum > T(1e-12) ? T(1) / wsum : T(0));
-        c_b[k] = uni_bias(c_sep[k], cf.beta, cf.dt);
-        const v3<T> ref = fabs(n.z) < T(0.9) ? v3<T>{0, 0, 1} : v3<T>{1, 0, 0};
-        c_t1[k] = vunit(cross(n, ref));
-      }
-    }
-
-    // ---------------- constant part of the system (assemble, :288-359) ---
-    // own diagonal block: mass + equality rows as child; off block H(c,p)
-    T Heq[21];
-#pragma unroll
-    for (int k = 0; k < 21; ++k) Heq[k] = T(0);
-    T rhs_eq[6] = {0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < 21; ++k) Hown[k] = T(0);
     if (dyn) {
-      Heq[tri(0, 0)] = mass;
-      Heq[tri(1, 1)] = mass;
-      Heq[tri(2, 2)] = mass;
-      Heq[tri(3, 3)] = Iw.xx;
-      Heq[tri(4, 3)] = Iw.xy;
-      Heq[tri(4, 4)] = Iw.yy;
-      Heq[tri(5, 3)] = Iw.xz;
-      Heq[tri(5, 4)] = Iw.yz;
-      Heq[tri(5, 5)] = Iw.zz;
+      Hown[tri(0, 0)] = mass;
+      Hown[tri(1, 1)] = mass;
+      Hown[tri(2, 2)] = mass;
+      Hown[tri(3, 3)] = Iw.xx;
+      Hown[tri(4, 3)] = Iw.xy;
+      Hown[tri(4, 4)] = Iw.yy;
+      Hown[tri(5, 3)] = Iw.xz;
+      Hown[tri(5, 4)] = Iw.yz;
+      Hown[tri(5, 5)] = Iw.zz;
       const v3<T> iwf = smul(Iw, wfree);
-      rhs_eq[0] = mass * vfree.x;
-      rhs_eq[1] = mass * vfree.y;
-      rhs_eq[2] = mass * vfree.z;
-      rhs_eq[3] = iwf.x;
-      rhs_eq[4] = iwf.y;
-      rhs_eq[5] = iwf.z;
+      rhs_own[0] = mass * vfree.x;
+      rhs_own[1] = mass * vfree.y;
+      rhs_own[2] = mass * vfree.z;
+      rhs_own[3] = iwf.x;
+      rhs_own[4] = iwf.y;
+      rhs_own[5] = iwf.z;
     }
     {
-      // parent-side contributions of this lane's joint rows, gathered by parent
-      T up[27];
+      const v3<T> xp = from<W>(x, par_src, mask);
+      const v3<T> wp = from<W>(w, par_src, mask);
+      const T p_invm = from<W>(inv_m, par_src, mask);
+      sym3<T> pI;
+      pI.xx = from<W>(Iinv.xx, par_src, mask);
+      pI.yy = from<W>(Iinv.yy, par_src, mask);
+      pI.zz = from<W>(Iinv.zz, par_src, mask);
+      pI.xy = from<W>(Iinv.xy, par_src, mask);
+      pI.xz = from<W>(Iinv.xz, par_src, mask);
+      pI.yz = from<W>(Iinv.yz, par_src, mask);
+#pragma unroll
+      for (int k = 0; k < 36; ++k) L.at(R_HOFF + k) = T(0);  // H(c,p) accumulates in smem
+      T up[27];  // parent-side contributions (packed diag block + rhs)
 #pragma unroll
       for (int k = 0; k < 27; ++k) up[k] = T(0);
-      T* hoff = tree.hoff;
-      T Hoff[36];
-#pragma unroll
-      for (int k = 0; k < 36; ++k) Hoff[k] = T(0);
+      T lim[7] = {0, 0, 0, 0, 0, 0, 0};
       if (has_joint) {
+        const v3<T> ra = qrot(qp, ldv(M.anc_p, b));
+        const v3<T> rb = qrot(q, ldv(M.anc_c, b));
+        const v3<T> cpos = (x + rb) - (xp + ra);
+        const v3<T> aw = qrot(qp, ldv(M.ax_p, b));
+        const v3<T> bw = qrot(q, ldv(M.ax_c, b));
+        const v3<T> ref = fabs(aw.z) < T(0.9) ? v3<T>{0, 0, 1} : v3<T>{1, 0, 0};
+        const v3<T> t1 = vunit(cross(aw, ref));
+        const v3<T> t2 = cross(aw, t1);
+        const v3<T> err = cross(aw, bw);
 #pragma unroll
         for (int rr = 0; rr < 5; ++rr) {
           T ja[6], jb[6];
+          T wsum = T(0);
+          T bias;
           if (rr < 3) {
             const v3<T> ek{T(rr == 0), T(rr == 1), T(rr == 2)};
             const v3<T> ca = -cross(ra, ek), cb = cross(rb, ek);
             ja[0] = -ek.x; ja[1] = -ek.y; ja[2] = -ek.z; ja[3] = ca.x; ja[4] = ca.y; ja[5] = ca.z;
             jb[0] = ek.x; jb[1] = ek.y; jb[2] = ek.z; jb[3] = cb.x; jb[4] = cb.y; jb[5] = cb.z;
+            if (pdyn) {
+              wsum += p_invm * T(1);
+              wsum += quad(pI, ca);
+            }
+            wsum += inv_m * T(1);
+            wsum += quad(Iinv, cb);
+            bias = -bdt * comp(cpos, rr);
           } else {
             const v3<T> t = rr == 3 ? t1 : t2;
             ja[0] = 0; ja[1] = 0; ja[2] = 0; ja[3] = -t.x; ja[4] = -t.y; ja[5] = -t.z;
             jb[0] = 0; jb[1] = 0; jb[2] = 0; jb[3] = t.x; jb[4] = t.y; jb[5] = t.z;
+            if (pdyn) wsum += quad(pI, -t);
+            wsum += quad(Iinv, t);
+            bias = -bdt * dot(t, err);
           }
-          const T d = eq_d[rr];
+          const T d = cf.kj * (wsum > T(1e-12) ? T(1) / wsum : T(0));  // effective_mass, :69-80
           if (!(d > T(0))) continue;  // assemble skips reg <= 0 (solver.cpp:331)
-          sym_add(Heq, jb, d);
-          const T db = d * eq_bias[rr];
+          sym_add(Hown, jb, d);
+          const T db = d * bias;
 #pragma unroll
-          for (int r = 0; r < 6; ++r) rhs_eq[r] += jb[r] * db;
+          for (int r = 0; r < 6; ++r) rhs_own[r] += jb[r] * db;
           if (pdyn) {
-            T Hp[21];
-#pragma unroll
-            for (int k = 0; k < 21; ++k) Hp[k] = T(0);
-            sym_add(Hp, ja, d);
-#pragma unroll
-            for (int k = 0; k < 21; ++k) up[k] += Hp[k];
-#pragma unroll
-            for (int r = 0; r < 6; ++r) up[21 + r] += ja[r] * db;
 #pragma unroll
             for (int r = 0; r < 6; ++r) {
+              const T dj = d * ja[r];
+#pragma unroll
+              for (int c = 0; c <= r; ++c) up[tri(r, c)] += dj * ja[c];
+              up[21 + r] += ja[r] * db;
               const T djb = d * jb[r];
 #pragma unroll
-              for (int c = 0; c < 6; ++c) Hoff[r * 6 + c] += djb * ja[c];
+              for (int c = 0; c < 6; ++c) L.at(R_HOFF + r * 6 + c) += djb * ja[c];
             }
           }
+          if (rr == 0 && M.quirk[b]) {  // aliasing quirk: H(p,c) misses row 0
+            L.quirk = true;
+            L.at(R_QRK + 0) = d;
+            L.at(R_QRK + 1) = ja[3];
+            L.at(R_QRK + 2) = ja[4];
+            L.at(R_QRK + 3) = ja[5];
+            L.at(R_QRK + 4) = jb[3];
+            L.at(R_QRK + 5) = jb[4];
+            L.at(R_QRK + 6) = jb[5];
+          }
+        }
+        // speculative limits (solver.cpp:144-173): angular rows along the child axis
+        const qt<T> rest{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]};
+        const v3<T> axc = ldv(M.ax_c, b);
+        const T angle = hinge_angle(qp, q, rest, axc);
+        const v3<T> axw = qrot(q, axc);
+        const T rate = dot(axw, w - wp);
+        const T lo_gap = angle - M.lim_lo[b];
+        const T hi_gap = M.lim_hi[b] - angle;
+        const T thr = max(cf.lim_act, T(1.5) * fabs(rate) * cf.dt);
+        T wl = T(0);
+        if (pdyn) wl += quad(pI, axw);
+        wl += quad(Iinv, axw);
+        const T meff = wl > T(1e-12) ? T(1) / wl : T(0);
+        lim[0] = axw.x;
+        lim[1] = axw.y;
+        lim[2] = axw.z;
+        if (lo_gap < thr) {
+          lim[3] = cf.kl * meff;
+          lim[5] = uni_bias(lo_gap, cf.beta, cf.dt);
+        }
+        if (hi_gap < thr) {
+          lim[4] = cf.kl * meff;
+          lim[6] = uni_bias(hi_gap, cf.beta, cf.dt);
         }
       }
 #pragma unroll
-      for (int k = 0; k < 36; ++k) hoff[k * 32 + lane] = Hoff[k];
-      T got[27];
-      tree.gather<27>(up, got);
+      for (int k = 0; k < 7; ++k) L.at(R_LIM + k) = lim[k];
+      // parent gathers its children's contributions, 9 values at a time
 #pragma unroll
-      for (int k = 0; k < 21; ++k) Heq[k] += got[k];
+      for (int chunk = 0; chunk < 3; ++chunk) {
+        T mine[9], got[9];
 #pragma unroll
-      for (int r = 0; r < 6; ++r) rhs_eq[r] += got[21 + r];
+        for (int k = 0; k < 9; ++k) mine[k] = up[9 * chunk + k];
+        L.gather<9>(mine, got);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          const int idx = 9 * chunk + k;
+          if (idx < 21) Hown[idx] += got[k];
+          else rhs_own[idx - 21] += got[k];
+        }
+      }
     }
+#pragma unroll
+    for (int k = 0; k < 21; ++k) L.at(R_HEQ + k) = Hown[k];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) L.at(R_HEQ + 21 + k) = rhs_own[k];
+    // contact rows (solver.cpp:176-210): normal weight + tangent basis
+#pragma unroll
+    for (int k = 0; k < CPB; ++k) {
+      if (k < nc) {
+        const int r0 = R_CT + 11 * k;
+        const v3<T> n{L.at(r0), L.at(r0 + 1), L.at(r0 + 2)};
+        const v3<T> rr{L.at(r0 + 3), L.at(r0 + 4), L.at(r0 + 5)};
+        const T sep = L.at(r0 + 10);
+        const v3<T> rn = cross(rr, n);
+        T wsum = inv_m * dot(n, n);
+        wsum += quad(Iinv, rn);
+        const v3<T> ref = fabs(n.z) < T(0.9) ? v3<T>{0, 0, 1} : v3<T>{1, 0, 0};
+        const v3<T> t1 = vunit(cross(n, ref));
+        L.at(r0 + 6) = t1.x;
+        L.at(r0 + 7) = t1.y;
+        L.at(r0 + 8) = t1.z;
+        L.at(r0 + 9) = cf.kc * (wsum > T(1e-12) ? T(1) / wsum : T(0));
+        L.at(r0 + 10) = uni_bias(sep, cf.beta, cf.dt);
+      }
+    }
+    // the constant off-diagonal block must be finite (krylov.cpp:113)
+    bool off_fin = true;
+    if (L.has_off) {
+#pragma unroll
+      for (int k = 0; k < 36; ++k) off_fin = off_fin && isfinite(L.at(R_HOFF + k));
+    }
+    const bool off_ok = __all_sync(mask, off_fin);
 
     // ---------------- Newton loop (solver.cpp:540-548) ---------------------
     T u[6] = {v.x, v.y, v.z, w.x, w.y, w.z};  // warm start from current velocities
     const bool need_solve = J > 0 || any_contact;
-    if (!need_solve) {
-      // free-body fast path, solver.cpp:517-523
+    if (!need_solve) {  // free-body fast path, solver.cpp:517-523
       u[0] = vfree.x; u[1] = vfree.y; u[2] = vfree.z;
       u[3] = wfree.x; u[4] = wfree.y; u[5] = wfree.z;
     } else {
       for (int it = 0; it < cf.newton; ++it) {
-        // unilateral activity + friction weights at the iterate (:304-328)
-        const T up_[6] = {from<W>(u[0], par_src, mask), from<W>(u[1], par_src, mask),
-                          from<W>(u[2], par_src, mask), from<W>(u[3], par_src, mask),
-                          from<W>(u[4], par_src, mask), from<W>(u[5], par_src, mask)};
         T H[21], rhs[6];
 #pragma unroll
-        for (int k = 0; k < 21; ++k) H[k] = Heq[k];
+        for (int k = 0; k < 21; ++k) H[k] = L.at(R_HEQ + k);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) rhs[k] = rhs_eq[k];
-        // joint limit rows: angular only, child side here, parent side gathered
+        for (int k = 0; k < 6; ++k) rhs[k] = L.at(R_HEQ + 21 + k);
+        // unilateral activity + friction weights at the iterate (:304-328)
+        const T wpa[3] = {__shfl_sync(mask, u[3], par_src, W), __shfl_sync(mask, u[4], par_src, W),
+                          __shfl_sync(mask, u[5], par_src, W)};
         T lim_s = T(0);
         T pl[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-        if (has_joint && (has_lo || has_hi)) {
+        if (has_joint) {
+          const v3<T> axw{L.at(R_LIM), L.at(R_LIM + 1), L.at(R_LIM + 2)};
           const T wc_a = axw.x * u[3] + axw.y * u[4] + axw.z * u[5];
-          const T wp_a = pdyn ? axw.x * up_[3] + axw.y * up_[4] + axw.z * up_[5] : T(0);
+          const T wp_a = pdyn ? axw.x * wpa[0] + axw.y * wpa[1] + axw.z * wpa[2] : T(0);
+#pragma unroll
           for (int side = 0; side < 2; ++side) {
-            const bool has = side == 0 ? has_lo : has_hi;
-            if (!has) continue;
-            const T d = side == 0 ? d_lo : d_hi;
-            const T bias = side == 0 ? b_lo : b_hi;
+            const T d = L.at(R_LIM + 3 + side);
+            const T bias = L.at(R_LIM + 5 + side);
             const T sg = side == 0 ? T(1) : T(-1);  // lo: jb = +axw; hi: jb = -axw
-            const T rate = sg * (wc_a - wp_a);
-            const T pred = d * (bias - rate);
-            if (pred > T(0) && d > T(0)) {
+            const T pred = d * (bias - sg * (wc_a - wp_a));
+            if (d > T(0) && pred > T(0)) {
               lim_s -= d;
-              T jb[6] = {0, 0, 0, sg * axw.x, sg * axw.y, sg * axw.z};
+              const T jb[6] = {0, 0, 0, sg * axw.x, sg * axw.y, sg * axw.z};
               sym_add(H, jb, d);
               const T db = d * bias;
               rhs[3] += jb[3] * db;
@@ -572,16 +740,18 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
                 pl[3] += d * axw.z * axw.x;
                 pl[4] += d * axw.z * axw.y;
                 pl[5] += d * axw.z * axw.z;
-                pl[6] += -sg * axw.x * db;
-                pl[7] += -sg * axw.y * db;
-                pl[8] += -sg * axw.z * db;
+                pl[6] -= sg * axw.x * db;
+                pl[7] -= sg * axw.y * db;
+                pl[8] -= sg * axw.z * db;
               }
             }
           }
+          L.lim_a = axw;
         }
+        L.lim_s = lim_s;
         {
           T got[9];
-          tree.gather<9>(pl, got);
+          L.gather<9>(pl, got);
           H[tri(3, 3)] += got[0];
           H[tri(4, 3)] += got[1];
           H[tri(4, 4)] += got[2];
@@ -592,28 +762,28 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
           rhs[4] += got[7];
           rhs[5] += got[8];
         }
-        tree.lim_s = lim_s;
-        tree.lim_a = axw;
         // contacts: normal + smoothed Coulomb friction (:311-327)
 #pragma unroll
         for (int k = 0; k < CPB; ++k) {
           if (k < nc) {
-            const v3<T> n = c_n[k];
-            const v3<T> rn = cross(c_r[k], n);
+            const int r0 = R_CT + 11 * k;
+            const v3<T> n{L.at(r0), L.at(r0 + 1), L.at(r0 + 2)};
+            const v3<T> rr{L.at(r0 + 3), L.at(r0 + 4), L.at(r0 + 5)};
+            const T cd = L.at(r0 + 9), cb = L.at(r0 + 10);
+            const v3<T> rn = cross(rr, n);
             const T jn[6] = {n.x, n.y, n.z, rn.x, rn.y, rn.z};
-            const T rate = dot6(jn, u);
-            const T pred = c_d[k] * (c_b[k] - rate);
+            const T pred = cd * (cb - dot6(jn, u));
             if (pred > T(0)) {
-              const v3<T> ta = c_t1[k], tb = cross(n, ta);
-              const v3<T> rta = cross(c_r[k], ta), rtb = cross(c_r[k], tb);
+              const v3<T> ta{L.at(r0 + 6), L.at(r0 + 7), L.at(r0 + 8)};
+              const v3<T> tb = cross(n, ta);
+              const v3<T> rta = cross(rr, ta), rtb = cross(rr, tb);
               const T j1[6] = {ta.x, ta.y, ta.z, rta.x, rta.y, rta.z};
               const T j2[6] = {tb.x, tb.y, tb.z, rtb.x, rtb.y, rtb.z};
               const T vt1 = dot6(j1, u), vt2 = dot6(j2, u);
-              const T vt = sqrt(vt1 * vt1 + vt2 * vt2);
-              const T fw = fric_weight(pred, vt, cf.epsf);
-              if (c_d[k] > T(0)) {
-                sym_add(H, jn, c_d[k]);
-                const T db = c_d[k] * c_b[k];
+              const T fw = fric_weight(pred, sqrt(vt1 * vt1 + vt2 * vt2), cf.epsf);
+              if (cd > T(0)) {
+                sym_add(H, jn, cd);
+                const T db = cd * cb;
 #pragma unroll
                 for (int r = 0; r < 6; ++r) rhs[r] += jn[r] * db;
               }
@@ -631,38 +801,34 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
         for (int k = 0; k < 21; ++k) fin = fin && isfinite(H[k]);
 #pragma unroll
         for (int k = 0; k < 6; ++k) fin = fin && isfinite(rhs[k]);
-        if (tree.has_off) {
-          for (int k = 0; k < 36; ++k) fin = fin && isfinite(tree.hoff[k * 32 + lane]);
-        }
-        if (!__all_sync(mask, fin)) {  // reference throws (krylov.cpp:113-114)
+        ++newton_done;
+        if (!off_ok || !__all_sync(mask, fin)) {  // reference throws (krylov.cpp:113-114)
           step_failed = true;
-          ++newton_done;
           break;
         }
-        const T bn = sqrt(seg_sum<W>(dot6(rhs, rhs), mask));
-        ++newton_done;
-        if (bn == T(0)) {
+        const T bb = seg_sum<W>(dot6(rhs, rhs), mask);
+        if (bb == T(0)) {
 #pragma unroll
           for (int k = 0; k < 6; ++k) u[k] = T(0);
           continue;
         }
-        T L[21], rinv[6];
-        const bool ok = dyn && chol6(H, L, rinv);
-        T r[6], z[6], p[6], ap[6], tmp[6];
-        tree.apply(H, u, tmp);
+        T P[21];
+        block_inverse(H, P, dyn);
+        T r[6], z[6], p[6], ap[6];
+        L.apply(H, u, r);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) r[k] = dyn ? rhs[k] - tmp[k] : T(0);
-        psolve(ok, L, rinv, r, z);
+        for (int k = 0; k < 6; ++k) r[k] = dyn ? rhs[k] - r[k] : T(0);
+        symv(P, r, z);
 #pragma unroll
         for (int k = 0; k < 6; ++k) p[k] = z[k];
-        tree.apply(H, z, ap);
-        T zaz = seg_sum<W>(dot6(z, ap), mask);
-        const T tol_abs = cf.tol * bn;
-        T rn = sqrt(seg_sum<W>(dot6(r, r), mask));
+        L.apply(H, z, ap);
+        T zaz = dot6(z, ap), rr = dot6(r, r);
+        seg_sum2<W>(zaz, rr, mask);
+        const T tol2 = cf.tol * cf.tol * bb;  // ||r|| > tol ||b||, compared squared
         int kk = 0;
-        while (kk < cf.kmax && rn > tol_abs) {
+        while (kk < cf.kmax && rr > tol2) {
           T map[6];
-          psolve(ok, L, rinv, ap, map);
+          symv(P, ap, map);
           const T denom = seg_sum<W>(dot6(ap, map), mask);
           if (!(denom > T(0)) || !(zaz > T(0))) break;  // breakdown (:144)
           const T alpha = zaz / denom;
@@ -672,12 +838,13 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
             r[k] -= alpha * ap[k];
           }
           ++kk;
-          psolve(ok, L, rinv, r, z);
-          rn = sqrt(seg_sum<W>(dot6(r, r), mask));
-          if (rn <= tol_abs) break;
+          symv(P, r, z);
           T az[6];
-          tree.apply(H, z, az);
-          const T zn = seg_sum<W>(dot6(z, az), mask);
+          L.apply(H, z, az);  // computed before the exit test: one spare product at exit
+          T zn = dot6(z, az);
+          rr = dot6(r, r);
+          seg_sum2<W>(rr, zn, mask);
+          if (rr <= tol2) break;
           const T beta = zn / zaz;
           zaz = zn;
 #pragma unroll
@@ -697,6 +864,21 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
       }
     }
 
+    // pre-step pose, origin and task state back from global memory
+    if (act) {
+      x = {a.state[sbase + 0 * W], a.state[sbase + 1 * W], a.state[sbase + 2 * W]};
+      q = {a.state[sbase + 3 * W], a.state[sbase + 4 * W], a.state[sbase + 5 * W], a.state[sbase + 6 * W]};
+      v = {a.state[sbase + 7 * W], a.state[sbase + 8 * W], a.state[sbase + 9 * W]};
+      w = {a.state[sbase + 10 * W], a.state[sbase + 11 * W], a.state[sbase + 12 * W]};
+    }
+    load_counters(cnt);
+    ox = a.origin[2 * e];
+    oy = a.origin[2 * e + 1];
+    tx = a.target ? a.target[2 * e] : T(0);
+    ty = a.target ? a.target[2 * e + 1] : T(0);
+    ltau = (jnt >= 0 && a.last_tau) ? a.last_tau[size_t(e) * J + jnt] : T(0);
+    feet_bits = a.feet ? a.feet[e] : 0u;
+
     // ---------------- impulse report (report_impulses, :365-391) ----------
     if (a.record) {
       int off = nc;
@@ -711,36 +893,41 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
 #pragma unroll
       for (int k = 0; k < CPB; ++k) {
         if (k < nc && off + k < a.cap) {
-          const v3<T> n = c_n[k];
-          const v3<T> rn = cross(c_r[k], n);
+          const int r0 = R_CT + 11 * k;
+          const v3<T> n{L.at(r0), L.at(r0 + 1), L.at(r0 + 2)};
+          const v3<T> rr{L.at(r0 + 3), L.at(r0 + 4), L.at(r0 + 5)};
+          const T cd = L.at(r0 + 9), cb = L.at(r0 + 10);
+          const v3<T> rn = cross(rr, n);
           const T jn[6] = {n.x, n.y, n.z, rn.x, rn.y, rn.z};
-          const T pn = max(T(0), c_d[k] * (c_b[k] - dot6(jn, u)));
+          const T pn = max(T(0), cd * (cb - dot6(jn, u)));
           v3<T> pt{0, 0, 0};
           if (pn > T(0)) {
-            const v3<T> ta = c_t1[k], tb = cross(n, ta);
-            const v3<T> rta = cross(c_r[k], ta), rtb = cross(c_r[k], tb);
+            const v3<T> ta{L.at(r0 + 6), L.at(r0 + 7), L.at(r0 + 8)};
+            const v3<T> tb = cross(n, ta);
+            const v3<T> rta = cross(rr, ta), rtb = cross(rr, tb);
             const T j1[6] = {ta.x, ta.y, ta.z, rta.x, rta.y, rta.z};
             const T j2[6] = {tb.x, tb.y, tb.z, rtb.x, rtb.y, rtb.z};
             const T vt1 = dot6(j1, u), vt2 = dot6(j2, u);
-            const T vt = sqrt(vt1 * vt1 + vt2 * vt2);
-            const T fw = fric_weight(pn, vt, cf.epsf);
+            const T fw = fric_weight(pn, sqrt(vt1 * vt1 + vt2 * vt2), cf.epsf);
             pt = ta * (-fw * vt1) + tb * (-fw * vt2);
           }
           const size_t slot = size_t(e) * a.cap + off + k;
           a.c_body[slot] = b;
-          double* cd = a.c_data + slot * kCData;
-          const v3<T> pw = x + c_r[k];
-          cd[0] = ox + double(pw.x);
-          cd[1] = oy + double(pw.y);
-          cd[2] = double(pw.z);
-          cd[3] = double(n.x);
-          cd[4] = double(n.y);
-          cd[5] = double(n.z);
-          cd[6] = double(c_sep[k]);
-          cd[7] = double(pn);
-          cd[8] = double(pt.x);
-          cd[9] = double(pt.y);
-          cd[10] = double(pt.z);
+          double* cdp = a.c_data + slot * kCData;
+          const v3<T> pw = x + rr;
+          // separation: recovered from the bias row (unilateral_bias is invertible)
+          const T sep = cb > T(0) ? -cb * cf.dt / cf.beta : -cb * cf.dt;
+          cdp[0] = ox + double(pw.x);
+          cdp[1] = oy + double(pw.y);
+          cdp[2] = double(pw.z);
+          cdp[3] = double(n.x);
+          cdp[4] = double(n.y);
+          cdp[5] = double(n.z);
+          cdp[6] = double(sep);
+          cdp[7] = double(pn);
+          cdp[8] = double(pt.x);
+          cdp[9] = double(pt.y);
+          cdp[10] = double(pt.z);
         }
       }
     }
@@ -767,11 +954,14 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
   // ---------------- K3: task epilogue (env_step) ---------
   if (a.mode == 1) {
     const int R = M.root;
+    const T prev_rx = a.state[size_t(e) * kStateFields * W + 0 * W + R];
+    const T prev_ry = a.state[size_t(e) * kStateFields * W + 1 * W + R];
     const v3<T> xr = from<W>(x, R, mask);
     const qt<T> qr = from<W>(q, R, mask);
     // feet-ground flags: foot has >= 1 static contact this step
     const unsigned fb = __ballot_sync(mask, act && nc > 0 && ((M.feet_mask >> b) & 1)) >> base;
     T rew = T(0);
+    const qt<T> qpn = from<W>(q, par_src, mask);
     if (!step_failed) {
       // compute_reward
       const T ox_ = tx - prev_rx, oy_ = ty - prev_ry;
@@ -784,7 +974,6 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
       const T cvert = T(1) - T(2) * (qr.x * qr.x + qr.y * qr.y);
       const T rstand = cvert > T(0.93) ? T(1) : T(0);
       T tc = T(0), uc = T(0), nl = T(0);
-      const qt<T> qpn = from<W>(q, par_src, mask);
       if (jnt >= 0) {
         const T uu = T(act_u);
         tc = fabs(min(max(uu, T(-1)), T(1)));
@@ -793,8 +982,7 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
                                   ldv(M.ax_c, b));
         nl = (ang - M.lim_lo[b] < cf.lim_act || M.lim_hi[b] - ang < cf.lim_act) ? T(1) : T(0);
       }
-      tc = seg_sum<W>(tc, mask);
-      uc = seg_sum<W>(uc, mask);
+      seg_sum2<W>(tc, uc, mask);
       nl = seg_sum<W>(nl, mask);
       const T nfeet = T(__popc(fb));
       rew = M.alive_bonus + S + T(0.5) * rhead + T(0.05) * rstand - T(4) * tc - T(0.5) * uc - T(0.2) * nl - nfeet;
@@ -951,7 +1139,7 @@ __global__ void __launch_bounds__(128) k_env_step(const KArgs<T> a) {
 template <class T, int W, int CPB>
 static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
   constexpr int threads = 128;
-  const size_t smem = size_t(threads / 32) * 64 * 32 * sizeof(T);
+  const size_t smem = size_t(threads / 32) * smem_rows<CPB>() * 32 * sizeof(T);
   static bool configured = false;
   if (!configured) {
     cudaError_t err = cudaFuncSetAttribute(k_env_step<T, W, CPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
