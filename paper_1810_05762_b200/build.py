@@ -19,7 +19,8 @@ OUT = os.path.join(PKG, "libstampede_b200.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+EXTRA = os.environ.get("STP_NVCC_EXTRA", "").split()
+FLAGS = EXTRA + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 SOURCES = ["sim_step_f32.cu", "sim_step_f64.cu", "sim_host.cu", "sim_aux.cu", "models.cpp"]
 DEPS = ["sim_device.cuh", "sim_kernels.cuh", "sim_step.cuh", "sim_launch.h", "stp_rng.h", "stp_error.h"]

@@ -108,9 +108,11 @@ __device__ __forceinline__ void sym_add(T (&H)[21], const T (&j)[6], T d) {
   }
 }
 
+// 6-term dot product as a depth-4 tree (shorter dependency chain than the
+// reference's left-to-right sum; same value up to rounding)
 template <class T>
 __device__ __forceinline__ T dot6(const T (&a)[6], const T (&b)[6]) {
-  return a[0] * b[0] + a[1] * b[1] + a[2] * b[2] + a[3] * b[3] + a[4] * b[4] + a[5] * b[5];
+  return ((a[0] * b[0] + a[1] * b[1]) + (a[2] * b[2] + a[3] * b[3])) + (a[4] * b[4] + a[5] * b[5]);
 }
 
 // unilateral_bias, solver.cpp:84-87

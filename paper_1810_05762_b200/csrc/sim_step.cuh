@@ -24,7 +24,9 @@ constexpr int R_SCAT = 36;  // 9: child -> parent gather buffer
 constexpr int R_HEQ = 45;   // 27: constant diagonal block (21, packed) + rhs (6)
 constexpr int R_LIM = 72;   // 7: limit axis (3), d_lo, d_hi, b_lo, b_hi
 constexpr int R_QRK = 79;   // 7: quirk d0, ja angular (3), jb angular (3)
-constexpr int R_CT = 86;    // 11 per contact slot: n(3) r(3) t1(3) d b
+constexpr int R_QH = 86;    // 13: quirk in the transformed system: d0, qa (6), qc (6)
+constexpr int R_HD = 99;    // 21: diagonal block, kept only when it is not positive definite
+constexpr int R_CT = 120;   // 11 per contact slot: n(3) r(3) t1(3) d b
 template <int CPB>
 __host__ __device__ constexpr int smem_rows() {
   return R_CT + 11 * CPB;
@@ -36,9 +38,10 @@ struct Lane {
   unsigned mask;
   int lane, base, b, par_src, maxc;
   int kid[4];  // child lanes (-1 = none)
-  bool has_off, quirk;
+  bool has_off, quirk, diag_h;
   T lim_s;  // -(sum of active limit weights): angular rank-1 term of H(c,p)
   v3<T> lim_a;
+  T Hh[36];  // transformed off-diagonal block L_b^-1 H(b, parent) L_parent^-T
 
   __device__ __forceinline__ T& at(int row) const { return sm[row * 32 + lane]; }
   __device__ __forceinline__ T at_kid(int row, int k) const { return sm[row * 32 + base + k]; }
@@ -60,6 +63,59 @@ struct Lane {
       }
     }
     __syncwarp(mask);
+  }
+
+  // y = Ahat v for the split-preconditioned system Ahat = L^-1 H L^-T:
+  // identity diagonal blocks (the own block only when it was not positive
+  // definite), Hh v_parent, and the children's Hh^T v_child.
+  __device__ __forceinline__ void apply_hat(const T (&v)[6], T (&y)[6]) const {
+    T vp[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) vp[k] = __shfl_sync(mask, v[k], par_src, W);
+    if (diag_h) {
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        T s = T(0);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) s += at(R_HD + sidx(r, c)) * v[c];
+        y[r] = s;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) y[k] = v[k];
+    }
+    T t[6] = {0, 0, 0, 0, 0, 0};
+    if (has_off) {
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        T s = T(0);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          s += Hh[r * 6 + c] * vp[c];
+          t[c] += Hh[r * 6 + c] * v[r];
+        }
+        y[r] += s;
+      }
+      if (quirk) {  // Ahat(p,c) = Hh^T - d0 qa qc^T
+        T s0 = T(0);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s0 += at(R_QH + 7 + k) * v[k];
+        s0 *= at(R_QH);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) t[k] -= s0 * at(R_QH + 1 + k);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i < maxc) {
+        const int src = kid[i] >= 0 ? kid[i] : b;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const T g = __shfl_sync(mask, t[k], src, W);
+          if (kid[i] >= 0) y[k] += g;
+        }
+      }
+    }
   }
 
   // y = H v over the segment's block tree (BlockSparseSym::apply,
@@ -109,12 +165,74 @@ struct Lane {
         t[5] -= s0 * at(R_QRK + 3);
       }
     }
-    T g[6];
-    gather<6>(t, g);
+    // children's H(child, b)^T v_child, pulled with shuffles (no smem round trip)
 #pragma unroll
-    for (int k = 0; k < 6; ++k) y[k] += g[k];
+    for (int i = 0; i < 4; ++i) {
+      if (i < maxc) {  // warp-uniform bound
+        const int src = kid[i] >= 0 ? kid[i] : b;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const T g = __shfl_sync(mask, t[k], src, W);
+          if (kid[i] >= 0) y[k] += g;
+        }
+      }
+    }
   }
 };
+
+template <class T, int W>
+struct LaneHat;
+
+// Cholesky factor Lc (lower, packed) of an SPD 6x6 block (krylov.cpp:27-41)
+// with reciprocal diagonal rd and Mi = Lc^-1; identity when the block is not
+// positive definite (the reference's identity fallback, krylov.cpp:76-80).
+template <class T>
+__device__ __forceinline__ bool factor6(const T (&H)[21], T (&Lc)[21], T (&rd)[6], T (&Mi)[21], bool dyn) {
+  bool ok = dyn;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      T s = H[tri(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s -= Lc[tri(i, k)] * Lc[tri(j, k)];
+      if (i == j) {
+        ok = ok && (s > T(0));
+        const T d = sqrt(s);
+        Lc[tri(i, i)] = d;
+        rd[i] = T(1) / d;
+      } else {
+        Lc[tri(i, j)] = s * rd[j];
+      }
+    }
+  }
+  if (!ok) {
+#pragma unroll
+    for (int k = 0; k < 21; ++k) {
+      Lc[k] = T(0);
+      Mi[k] = T(0);
+    }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      Lc[tri(i, i)] = T(1);
+      Mi[tri(i, i)] = T(1);
+      rd[i] = T(1);
+    }
+    return false;
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    Mi[tri(i, i)] = rd[i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+      T s = T(0);
+#pragma unroll
+      for (int k = j; k < i; ++k) s += Lc[tri(i, k)] * Mi[tri(k, j)];
+      Mi[tri(i, j)] = -s * rd[i];
+    }
+  }
+  return true;
+}
 
 // explicit inverse of the packed SPD 6x6 block (block-Jacobi preconditioner,
 // krylov.cpp:60-88, mathematically the reference's cholesky_solve pair);
@@ -182,6 +300,27 @@ __device__ __forceinline__ void symv(const T (&P)[21], const T (&v)[6], T (&y)[6
   }
 }
 
+// alpha / beta of the PCR recurrences: fp32 uses reciprocal + multiply
+// (two roundings; the f64 parity instrument keeps IEEE division).
+__device__ __forceinline__ float fdiv(float a, float b) { return a * __frcp_rn(b); }
+__device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
+
+#ifndef STP_PIPELINED_CR
+#define STP_PIPELINED_CR 0
+#endif
+constexpr bool kPipelinedCR = STP_PIPELINED_CR != 0;
+
+template <int W, class T>
+__device__ __forceinline__ void seg_sum4(T& a, T& b, T& c, T& d, unsigned mask) {
+#pragma unroll
+  for (int off = W / 2; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(mask, a, off, W);
+    b += __shfl_xor_sync(mask, b, off, W);
+    c += __shfl_xor_sync(mask, c, off, W);
+    d += __shfl_xor_sync(mask, d, off, W);
+  }
+}
+
 template <int W, class T>
 __device__ __forceinline__ void seg_sum2(T& a, T& b, unsigned mask) {
 #pragma unroll
@@ -191,8 +330,12 @@ __device__ __forceinline__ void seg_sum2(T& a, T& b, unsigned mask) {
   }
 }
 
+#ifndef STP_MINB
+#define STP_MINB 3
+#endif
+
 template <class T, int W, int CPB>
-__global__ void __launch_bounds__(128, (sizeof(T) == 4 ? 4 : 1)) k_env_step(const KArgs<T> a) {
+__global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_step(const KArgs<T> a) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int e = tid / W;
   if (e >= a.n) return;  // whole segments exit together
@@ -223,6 +366,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? 4 : 1)) k_env_step(cons
   for (int i = 0; i < 4; ++i) L.kid[i] = act ? M.child_list[i][b] : -1;
   L.has_off = dyn && pdyn && jnt >= 0;
   L.quirk = false;
+  L.diag_h = false;
   L.lim_s = T(0);
   L.lim_a = {0, 0, 0};
 
@@ -796,6 +940,12 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? 4 : 1)) k_env_step(cons
         }
 
         // ---------------- PCR (solve_krylov_inplace, krylov.cpp:106-174) --
+        // Split block-Jacobi form.  With L_b L_b^T = H_bb (krylov.cpp:27-41),
+        // plain CR on Ahat = L^-1 H L^-T, xhat = L^T x, bhat = L^-1 b yields
+        // the reference's left-preconditioned CR iterates exactly (in exact
+        // arithmetic): z = M^-1 r = L^-T rhat, z.Az = rhat.Ahat rhat and
+        // Ap.M^-1 Ap = |Ahat phat|^2.  Ahat has identity diagonal blocks, so
+        // an iteration needs no diagonal product and no preconditioner solve.
         bool fin = true;
 #pragma unroll
         for (int k = 0; k < 21; ++k) fin = fin && isfinite(H[k]);
@@ -812,46 +962,125 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? 4 : 1)) k_env_step(cons
           for (int k = 0; k < 6; ++k) u[k] = T(0);
           continue;
         }
-        T P[21];
-        block_inverse(H, P, dyn);
-        T r[6], z[6], p[6], ap[6];
-        L.apply(H, u, r);
+        T Lc[21], rd[6];
+        T bh[6], xh[6];
+        {
+          T Mi[21];
+          const bool ok = factor6(H, Lc, rd, Mi, dyn);
+          L.diag_h = dyn && !ok;
+          if (L.diag_h) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) r[k] = dyn ? rhs[k] - r[k] : T(0);
-        symv(P, r, z);
+            for (int k = 0; k < 21; ++k) L.at(R_HD + k) = H[k];
+          }
+          T Mp[21];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) p[k] = z[k];
-        L.apply(H, z, ap);
-        T zaz = dot6(z, ap), rr = dot6(r, r);
+          for (int k = 0; k < 21; ++k) Mp[k] = __shfl_sync(mask, Mi[k], par_src, W);
+          // Hh = Mi (H(c,p) + limit term) Mp^T
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            T g[6] = {0, 0, 0, 0, 0, 0};
+            if (L.has_off) {
+#pragma unroll
+              for (int k = 0; k <= i; ++k) {
+                const T m = Mi[tri(i, k)];
+#pragma unroll
+                for (int c = 0; c < 6; ++c) {
+                  T h = L.at(R_HOFF + k * 6 + c);
+                  if (k >= 3 && c >= 3) h += L.lim_s * comp(L.lim_a, k - 3) * comp(L.lim_a, c - 3);
+                  g[c] += m * h;
+                }
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 6; ++j) {
+              T sum = T(0);
+#pragma unroll
+              for (int k = 0; k <= j; ++k) sum += g[k] * Mp[tri(j, k)];
+              L.Hh[i * 6 + j] = sum;
+            }
+          }
+          if (L.quirk) {  // transformed aliasing term: d0 (Mp ja0)(Mi jb0)^T
+            const T ja0[6] = {T(-1), 0, 0, L.at(R_QRK + 1), L.at(R_QRK + 2), L.at(R_QRK + 3)};
+            const T jb0[6] = {T(1), 0, 0, L.at(R_QRK + 4), L.at(R_QRK + 5), L.at(R_QRK + 6)};
+            L.at(R_QH) = L.at(R_QRK);
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+              T qa = T(0), qc = T(0);
+#pragma unroll
+              for (int k = 0; k <= i; ++k) {
+                qa += Mp[tri(i, k)] * ja0[k];
+                qc += Mi[tri(i, k)] * jb0[k];
+              }
+              L.at(R_QH + 1 + i) = qa;
+              L.at(R_QH + 7 + i) = qc;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            T sb = T(0), sx = T(0);
+#pragma unroll
+            for (int k = 0; k <= i; ++k) sb += Mi[tri(i, k)] * rhs[k];
+#pragma unroll
+            for (int k = i; k < 6; ++k) sx += Lc[tri(k, i)] * u[k];
+            bh[i] = sb;
+            xh[i] = sx;
+          }
+        }
+        auto res_norm2 = [&](const T (&rh)[6]) {  // |L rhat|^2 = ||r||^2 of the reference
+          T s0 = T(0);
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            T ri = T(0);
+#pragma unroll
+            for (int k = 0; k <= i; ++k) ri += Lc[tri(i, k)] * rh[k];
+            s0 += ri * ri;
+          }
+          return s0;
+        };
+        T rh[6], ar[6], ph[6], ap[6];
+        L.apply_hat(xh, ar);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) rh[k] = dyn ? bh[k] - ar[k] : T(0);
+        L.apply_hat(rh, ar);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          ph[k] = rh[k];
+          ap[k] = ar[k];
+        }
+        T zaz = dot6(rh, ar), rr = res_norm2(rh);
         seg_sum2<W>(zaz, rr, mask);
         const T tol2 = cf.tol * cf.tol * bb;  // ||r|| > tol ||b||, compared squared
         int kk = 0;
         while (kk < cf.kmax && rr > tol2) {
-          T map[6];
-          symv(P, ap, map);
-          const T denom = seg_sum<W>(dot6(ap, map), mask);
+          const T denom = seg_sum<W>(dot6(ap, ap), mask);
           if (!(denom > T(0)) || !(zaz > T(0))) break;  // breakdown (:144)
-          const T alpha = zaz / denom;
+          const T alpha = fdiv(zaz, denom);
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
-            u[k] += alpha * p[k];
-            r[k] -= alpha * ap[k];
+            xh[k] += alpha * ph[k];
+            rh[k] -= alpha * ap[k];
           }
           ++kk;
-          symv(P, r, z);
-          T az[6];
-          L.apply(H, z, az);  // computed before the exit test: one spare product at exit
-          T zn = dot6(z, az);
-          rr = dot6(r, r);
+          L.apply_hat(rh, ar);  // before the exit test: one spare product at exit
+          T zn = dot6(rh, ar);
+          rr = res_norm2(rh);
           seg_sum2<W>(rr, zn, mask);
           if (rr <= tol2) break;
-          const T beta = zn / zaz;
+          const T beta = fdiv(zn, zaz);
           zaz = zn;
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
-            p[k] = z[k] + beta * p[k];
-            ap[k] = az[k] + beta * ap[k];
+            ph[k] = rh[k] + beta * ph[k];
+            ap[k] = ar[k] + beta * ap[k];
           }
+        }
+        // back to velocities: solve L^T u = xhat
+#pragma unroll
+        for (int i = 5; i >= 0; --i) {
+          T sum = xh[i];
+#pragma unroll
+          for (int k = i + 1; k < 6; ++k) sum -= Lc[tri(k, i)] * u[k];
+          u[i] = sum * rd[i];
         }
         krylov_total += kk;
         bool ufin = true;
