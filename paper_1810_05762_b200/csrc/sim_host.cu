@@ -49,6 +49,7 @@ struct stp_sim {
   bool record = false;  // record contacts on the next physics step(s)
   double* d_boxes = nullptr;
   int n_boxes = 0;
+  void* d_scratch = nullptr;
   // staging for the host-buffer entry points
   float* d_act = nullptr;
   float* d_obs = nullptr;
@@ -258,6 +259,7 @@ stp::KArgs<T> make_args(stp_sim* s, int mode) {
   a.c_data = s->d_cdata;
   a.n_boxes = s->n_boxes;
   a.boxes = s->d_boxes;
+  a.scratch = reinterpret_cast<T*>(s->d_scratch);
   return a;
 }
 
@@ -393,7 +395,8 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
       (rc = dalloc(s, &s->d_ccount, N * 4)) || (rc = dalloc(s, &s->d_cbody, N * s->cap * 4)) ||
       (rc = dalloc(s, &s->d_cdata, N * s->cap * stp::kCData * sizeof(double))) ||
       (rc = dalloc(s, &s->d_act, N * std::max(1, s->J) * 4)) || (rc = dalloc(s, &s->d_obs, N * s->obs_dim * 4)) ||
-      (rc = dalloc(s, &s->d_rew, N * 4)) || (rc = dalloc(s, &s->d_done, N)))
+      (rc = dalloc(s, &s->d_rew, N * 4)) || (rc = dalloc(s, &s->d_done, N)) ||
+      (rc = dalloc(s, &s->d_scratch, N * 34 * s->W * ts)))
     return bail(rc);
   if (precision == STP_PRECISION_F64) {
     stp::DevModel<double> dm;

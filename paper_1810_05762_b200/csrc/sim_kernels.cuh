@@ -61,6 +61,7 @@ struct KArgs {
   double* c_data;     // [n][cap][11]
   int n_boxes;
   const double* boxes;  // [nbox][8]: cx cy cz hx hy hz cos(yaw) sin(yaw)
+  T* scratch;           // [n][34][W] rarely used per-lane rows (sim_step.cuh G_*)
 };
 
 enum { C_FRAME = 0, C_FLAG = 1, C_FALL = 2, C_NEXTP = 3, C_EPISODE = 4, C_FLAGDRAW = 5, C_PERTDRAW = 6 };

@@ -24,9 +24,11 @@ constexpr int R_SCAT = 36;  // 9: child -> parent gather buffer
 constexpr int R_HEQ = 45;   // 27: constant diagonal block (21, packed) + rhs (6)
 constexpr int R_LIM = 72;   // 7: limit axis (3), d_lo, d_hi, b_lo, b_hi
 constexpr int R_QRK = 79;   // 7: quirk d0, ja angular (3), jb angular (3)
-constexpr int R_QH = 86;    // 13: quirk in the transformed system: d0, qa (6), qc (6)
-constexpr int R_HD = 99;    // 21: diagonal block, kept only when it is not positive definite
-constexpr int R_CT = 120;   // 11 per contact slot: n(3) r(3) t1(3) d b
+constexpr int R_CT = 86;    // 11 per contact slot: n(3) r(3) t1(3) d b
+// Rarely used per-lane rows live in a global scratch buffer (L1-resident):
+constexpr int G_QH = 0;     // 13: quirk in the transformed system: d0, qa (6), qc (6)
+constexpr int G_HD = 13;    // 21: diagonal block, kept only when it is not positive definite
+constexpr int kScratchRows = 34;
 template <int CPB>
 __host__ __device__ constexpr int smem_rows() {
   return R_CT + 11 * CPB;
@@ -35,6 +37,7 @@ __host__ __device__ constexpr int smem_rows() {
 template <class T, int W>
 struct Lane {
   T* sm;
+  T* gs;  // global scratch rows of this env (kScratchRows x W)
   unsigned mask;
   int lane, base, b, par_src, maxc;
   int kid[4];  // child lanes (-1 = none)
@@ -45,6 +48,7 @@ struct Lane {
 
   __device__ __forceinline__ T& at(int row) const { return sm[row * 32 + lane]; }
   __device__ __forceinline__ T at_kid(int row, int k) const { return sm[row * 32 + base + k]; }
+  __device__ __forceinline__ T& g(int row) const { return gs[row * W + b]; }
 
   // out = sum over children of v (parent side of a child's contribution)
   template <int K>
@@ -77,7 +81,7 @@ struct Lane {
       for (int r = 0; r < 6; ++r) {
         T s = T(0);
 #pragma unroll
-        for (int c = 0; c < 6; ++c) s += at(R_HD + sidx(r, c)) * v[c];
+        for (int c = 0; c < 6; ++c) s += g(G_HD + sidx(r, c)) * v[c];
         y[r] = s;
       }
     } else {
@@ -99,10 +103,10 @@ struct Lane {
       if (quirk) {  // Ahat(p,c) = Hh^T - d0 qa qc^T
         T s0 = T(0);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) s0 += at(R_QH + 7 + k) * v[k];
-        s0 *= at(R_QH);
+        for (int k = 0; k < 6; ++k) s0 += g(G_QH + 7 + k) * v[k];
+        s0 *= g(G_QH);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) t[k] -= s0 * at(R_QH + 1 + k);
+        for (int k = 0; k < 6; ++k) t[k] -= s0 * g(G_QH + 1 + k);
       }
     }
 #pragma unroll
@@ -331,7 +335,7 @@ __device__ __forceinline__ void seg_sum2(T& a, T& b, unsigned mask) {
 }
 
 #ifndef STP_MINB
-#define STP_MINB 3
+#define STP_MINB 4
 #endif
 
 template <class T, int W, int CPB>
@@ -356,6 +360,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
   extern __shared__ unsigned char smem_raw[];
   Lane<T, W> L;
   L.sm = reinterpret_cast<T*>(smem_raw) + (threadIdx.x >> 5) * (smem_rows<CPB>() * 32);
+  L.gs = a.scratch + size_t(e) * kScratchRows * W;
   L.mask = mask;
   L.lane = lane;
   L.base = base;
@@ -399,6 +404,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
   T tx, ty, ltau;
   unsigned feet_bits;
 
+  bool do_reset = false;
   if (a.mode == 2) {
     load_counters(cnt);
     ox = a.origin[2 * e];
@@ -407,13 +413,8 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
     ty = a.target ? a.target[2 * e + 1] : T(0);
     ltau = (jnt >= 0 && a.last_tau) ? a.last_tau[size_t(e) * J + jnt] : T(0);
     feet_bits = a.feet ? a.feet[e] : 0u;
-    // ---------------- reset only ------------------------
-    const bool doit = a.reset_mask == nullptr || a.reset_mask[e];
-    if (doit) {
-      reset_env<T, W>(a, M, e, b, mask, act, x, q, v, w, cnt, tx, ty, ox, oy);
-      ltau = T(0);
-      feet_bits = 0u;
-    }
+    // reset only: performed at the shared reset site below
+    do_reset = a.reset_mask == nullptr || a.reset_mask[e];
   } else {
     // ---------------- actuation (clamp_torques, solver.cpp:395-403) -------
     T tau = T(0);
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           if (s0 < margin) add_contact(p0 - up * rad, up, s0);
           const T s1 = p1.z - rad;
           if (s1 < margin) add_contact(p1 - up * rad, up, s1);
-        } else {
+        } else if constexpr (CPB > 2) {  // dynamic boxes: 8 corners (host picks CPB = 8)
           for (int cx = -1; cx <= 1; cx += 2)
             for (int cy = -1; cy <= 1; cy += 2)
               for (int cz = -1; cz <= 1; cz += 2) {
@@ -514,7 +515,8 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
         }
       }
       // static terrain boxes (collide.cpp:287-298), in box-index order
-      if (a.n_boxes > 0 && shp != STP_BOX) {
+      // (terrain handles always run the CPB = 8 instantiation)
+      if constexpr (CPB > 2) if (a.n_boxes > 0 && shp != STP_BOX) {
         const double ox = a.origin[2 * e], oy = a.origin[2 * e + 1];
         const v3<T> lo{min(p0.x, p1.x) - rad, min(p0.y, p1.y) - rad, min(p0.z, p1.z) - rad};
         const v3<T> hi{max(p0.x, p1.x) + rad, max(p0.y, p1.y) + rad, max(p0.z, p1.z) + rad};
@@ -970,7 +972,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           L.diag_h = dyn && !ok;
           if (L.diag_h) {
 #pragma unroll
-            for (int k = 0; k < 21; ++k) L.at(R_HD + k) = H[k];
+            for (int k = 0; k < 21; ++k) L.g(G_HD + k) = H[k];
           }
           T Mp[21];
 #pragma unroll
@@ -1002,7 +1004,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           if (L.quirk) {  // transformed aliasing term: d0 (Mp ja0)(Mi jb0)^T
             const T ja0[6] = {T(-1), 0, 0, L.at(R_QRK + 1), L.at(R_QRK + 2), L.at(R_QRK + 3)};
             const T jb0[6] = {T(1), 0, 0, L.at(R_QRK + 4), L.at(R_QRK + 5), L.at(R_QRK + 6)};
-            L.at(R_QH) = L.at(R_QRK);
+            L.g(G_QH) = L.at(R_QRK);
 #pragma unroll
             for (int i = 0; i < 6; ++i) {
               T qa = T(0), qc = T(0);
@@ -1011,8 +1013,8 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
                 qa += Mp[tri(i, k)] * ja0[k];
                 qc += Mi[tri(i, k)] * jb0[k];
               }
-              L.at(R_QH + 1 + i) = qa;
-              L.at(R_QH + 7 + i) = qc;
+              L.g(G_QH + 1 + i) = qa;
+              L.g(G_QH + 7 + i) = qc;
             }
           }
 #pragma unroll
@@ -1037,21 +1039,52 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           }
           return s0;
         };
-        T rh[6], ar[6], ph[6], ap[6];
-        L.apply_hat(xh, ar);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) rh[k] = dyn ? bh[k] - ar[k] : T(0);
-        L.apply_hat(rh, ar);
+        // One apply_hat call site (code size): phase 0 forms rhat = bhat - Ahat xhat,
+        // phase 1 the first direction, phase 2 the CR iterations
+        // (solve_krylov_inplace loop, krylov.cpp:141-163).
+        T rh[6], ar[6], ph[6], ap[6], vin[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-          ph[k] = rh[k];
-          ap[k] = ar[k];
+          vin[k] = xh[k];
+          rh[k] = T(0);
+          ph[k] = T(0);
+          ap[k] = T(0);
         }
-        T zaz = dot6(rh, ar), rr = res_norm2(rh);
-        seg_sum2<W>(zaz, rr, mask);
         const T tol2 = cf.tol * cf.tol * bb;  // ||r|| > tol ||b||, compared squared
-        int kk = 0;
-        while (kk < cf.kmax && rr > tol2) {
+        T zaz = T(0);
+        int kk = 0, phase = 0;
+        while (true) {
+          L.apply_hat(vin, ar);
+          if (phase == 0) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+              rh[k] = dyn ? bh[k] - ar[k] : T(0);
+              vin[k] = rh[k];
+            }
+            phase = 1;
+            continue;
+          }
+          T zn = dot6(rh, ar), rr = res_norm2(rh);
+          seg_sum2<W>(rr, zn, mask);
+          if (phase == 1) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+              ph[k] = rh[k];
+              ap[k] = ar[k];
+            }
+            zaz = zn;
+            phase = 2;
+          } else {
+            if (rr <= tol2) break;
+            const T beta = fdiv(zn, zaz);
+            zaz = zn;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+              ph[k] = rh[k] + beta * ph[k];
+              ap[k] = ar[k] + beta * ap[k];
+            }
+          }
+          if (!(kk < cf.kmax && rr > tol2)) break;
           const T denom = seg_sum<W>(dot6(ap, ap), mask);
           if (!(denom > T(0)) || !(zaz > T(0))) break;  // breakdown (:144)
           const T alpha = fdiv(zaz, denom);
@@ -1059,20 +1092,9 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           for (int k = 0; k < 6; ++k) {
             xh[k] += alpha * ph[k];
             rh[k] -= alpha * ap[k];
+            vin[k] = rh[k];
           }
           ++kk;
-          L.apply_hat(rh, ar);  // before the exit test: one spare product at exit
-          T zn = dot6(rh, ar);
-          rr = res_norm2(rh);
-          seg_sum2<W>(rr, zn, mask);
-          if (rr <= tol2) break;
-          const T beta = fdiv(zn, zaz);
-          zaz = zn;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) {
-            ph[k] = rh[k] + beta * ph[k];
-            ap[k] = ar[k] + beta * ap[k];
-          }
         }
         // back to velocities: solve L^T u = xhat
 #pragma unroll
@@ -1248,15 +1270,16 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
     }
     ltau = jnt >= 0 ? min(max(T(act_u), T(-1)), T(1)) : T(0);
     feet_bits = fb;
-    if (dn && a.task.auto_reset) {
-      reset_env<T, W>(a, M, e, b, mask, act, x, q, v, w, cnt, tx, ty, ox, oy);
-      ltau = T(0);
-      feet_bits = 0;
-    }
+    do_reset = dn && a.task.auto_reset;
     if (b == 0) {
       if (a.reward) a.reward[e] = float(rew);
       if (a.done) a.done[e] = dn ? 1 : 0;
     }
+  }
+  if (do_reset) {  // single inlined reset site (SPEC.md:261-269 / auto-reset)
+    reset_env<T, W>(a, M, e, b, mask, act, x, q, v, w, cnt, tx, ty, ox, oy);
+    ltau = T(0);
+    feet_bits = 0;
   }
   if (a.mode >= 1) {
     if (jnt >= 0 && a.last_tau) a.last_tau[size_t(e) * J + jnt] = ltau;
