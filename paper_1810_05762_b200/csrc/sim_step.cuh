@@ -970,6 +970,8 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           T Mi[21];
           const bool ok = factor6(H, Lc, rd, Mi, dyn);
           L.diag_h = dyn && !ok;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) L.at(R_SCAT + k) = rd[k];
           if (L.diag_h) {
 #pragma unroll
             for (int k = 0; k < 21; ++k) L.g(G_HD + k) = H[k];
@@ -1042,11 +1044,10 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
         // One apply_hat call site (code size): phase 0 forms rhat = bhat - Ahat xhat,
         // phase 1 the first direction, phase 2 the CR iterations
         // (solve_krylov_inplace loop, krylov.cpp:141-163).
-        T rh[6], ar[6], ph[6], ap[6], vin[6];
+        T rh[6], ar[6], ph[6], ap[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-          vin[k] = xh[k];
-          rh[k] = T(0);
+          rh[k] = xh[k];  // phase 0 applies Ahat to xhat
           ph[k] = T(0);
           ap[k] = T(0);
         }
@@ -1054,13 +1055,10 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
         T zaz = T(0);
         int kk = 0, phase = 0;
         while (true) {
-          L.apply_hat(vin, ar);
+          L.apply_hat(rh, ar);
           if (phase == 0) {
 #pragma unroll
-            for (int k = 0; k < 6; ++k) {
-              rh[k] = dyn ? bh[k] - ar[k] : T(0);
-              vin[k] = rh[k];
-            }
+            for (int k = 0; k < 6; ++k) rh[k] = dyn ? bh[k] - ar[k] : T(0);
             phase = 1;
             continue;
           }
@@ -1092,17 +1090,16 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           for (int k = 0; k < 6; ++k) {
             xh[k] += alpha * ph[k];
             rh[k] -= alpha * ap[k];
-            vin[k] = rh[k];
           }
           ++kk;
         }
-        // back to velocities: solve L^T u = xhat
+        // back to velocities: solve L^T u = xhat (reciprocal diagonal parked in R_SCAT)
 #pragma unroll
         for (int i = 5; i >= 0; --i) {
           T sum = xh[i];
 #pragma unroll
           for (int k = i + 1; k < 6; ++k) sum -= Lc[tri(k, i)] * u[k];
-          u[i] = sum * rd[i];
+          u[i] = sum * L.at(R_SCAT + i);
         }
         krylov_total += kk;
         bool ufin = true;
