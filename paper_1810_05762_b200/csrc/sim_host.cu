@@ -50,6 +50,12 @@ struct stp_sim {
   double* d_boxes = nullptr;
   int n_boxes = 0;
   void* d_scratch = nullptr;
+  // terrain broadphase grid
+  int grid_nx = 0, grid_ny = 0;
+  double grid_x0 = 0, grid_y0 = 0, grid_inv = 0;
+  int* d_cell_start = nullptr;
+  int* d_cell_list = nullptr;
+  int4* d_box_cells = nullptr;
   // staging for the host-buffer entry points
   float* d_act = nullptr;
   float* d_obs = nullptr;
@@ -260,6 +266,14 @@ stp::KArgs<T> make_args(stp_sim* s, int mode) {
   a.n_boxes = s->n_boxes;
   a.boxes = s->d_boxes;
   a.scratch = reinterpret_cast<T*>(s->d_scratch);
+  a.grid_nx = s->grid_nx;
+  a.grid_ny = s->grid_ny;
+  a.grid_x0 = s->grid_x0;
+  a.grid_y0 = s->grid_y0;
+  a.grid_inv = s->grid_inv;
+  a.cell_start = s->d_cell_start;
+  a.cell_list = s->d_cell_list;
+  a.box_cells = s->d_box_cells;
   return a;
 }
 
@@ -458,6 +472,64 @@ int stp_set_terrain(stp_sim* s, const stp_static_box* boxes, int32_t n) {
   CK(cudaMemcpyAsync(s->d_boxes, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
   CK(cudaStreamSynchronize(s->stream));
   s->n_boxes = n;
+  // Uniform xy grid over the boxes' loose footprints (the reference's box
+  // broadphase box, collide.cpp:289-290: centre +- (hx+hy, hx+hy)); each box
+  // is listed, in index order, in every cell its footprint overlaps.
+  for (void* p : {(void*)s->d_cell_start, (void*)s->d_cell_list, (void*)s->d_box_cells}) {
+    if (!p) continue;
+    CK(cudaFree(p));
+    s->allocations.erase(std::remove(s->allocations.begin(), s->allocations.end(), p), s->allocations.end());
+  }
+  s->d_cell_start = nullptr;
+  s->d_cell_list = nullptr;
+  s->d_box_cells = nullptr;
+  s->grid_nx = s->grid_ny = 0;
+  if (n > 0) {
+    const double cell = 2.0;
+    double x0 = 1e300, y0 = 1e300, x1 = -1e300, y1 = -1e300;
+    for (int i = 0; i < n; ++i) {
+      const double ex = boxes[i].half_extents[0] + boxes[i].half_extents[1];
+      x0 = std::min(x0, boxes[i].center[0] - ex);
+      x1 = std::max(x1, boxes[i].center[0] + ex);
+      y0 = std::min(y0, boxes[i].center[1] - ex);
+      y1 = std::max(y1, boxes[i].center[1] + ex);
+    }
+    const int nx = std::max(1, int(std::ceil((x1 - x0) / cell)) + 1);
+    const int ny = std::max(1, int(std::ceil((y1 - y0) / cell)) + 1);
+    if (double(nx) * ny > 16e6) return fail(STP_EINVAL, "set_terrain: terrain extent too large for the grid");
+    const double inv = 1.0 / cell;
+    auto cl = [](int c, int m) { return c < 0 ? 0 : (c >= m ? m - 1 : c); };
+    std::vector<int4> bc(n);
+    std::vector<int> count(size_t(nx) * ny + 1, 0);
+    for (int i = 0; i < n; ++i) {
+      const double ex = boxes[i].half_extents[0] + boxes[i].half_extents[1];
+      bc[i].x = cl(int(std::floor((boxes[i].center[0] - ex - x0) * inv)), nx);
+      bc[i].y = cl(int(std::floor((boxes[i].center[1] - ex - y0) * inv)), ny);
+      bc[i].z = cl(int(std::floor((boxes[i].center[0] + ex - x0) * inv)), nx);
+      bc[i].w = cl(int(std::floor((boxes[i].center[1] + ex - y0) * inv)), ny);
+      for (int cy = bc[i].y; cy <= bc[i].w; ++cy)
+        for (int cx = bc[i].x; cx <= bc[i].z; ++cx) ++count[size_t(cy) * nx + cx + 1];
+    }
+    for (size_t c = 1; c < count.size(); ++c) count[c] += count[c - 1];
+    std::vector<int> fill(count.begin(), count.end() - 1), list(count.back());
+    for (int i = 0; i < n; ++i)
+      for (int cy = bc[i].y; cy <= bc[i].w; ++cy)
+        for (int cx = bc[i].x; cx <= bc[i].z; ++cx) list[fill[size_t(cy) * nx + cx]++] = i;
+    if ((rc = dalloc(s, &s->d_cell_start, count.size() * sizeof(int))) ||
+        (rc = dalloc(s, &s->d_cell_list, std::max<size_t>(1, list.size()) * sizeof(int))) ||
+        (rc = dalloc(s, &s->d_box_cells, bc.size() * sizeof(int4))))
+      return rc;
+    CK(cudaMemcpyAsync(s->d_cell_start, count.data(), count.size() * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    if (!list.empty())
+      CK(cudaMemcpyAsync(s->d_cell_list, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->d_box_cells, bc.data(), bc.size() * sizeof(int4), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    s->grid_nx = nx;
+    s->grid_ny = ny;
+    s->grid_x0 = x0;
+    s->grid_y0 = y0;
+    s->grid_inv = inv;
+  }
   if (n > 0 && s->cpb < 8) {
     // terrain contacts need more slots per body: grow the recorded list too
     s->cpb = 8;

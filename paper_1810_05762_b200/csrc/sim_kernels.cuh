@@ -62,6 +62,12 @@ struct KArgs {
   int n_boxes;
   const double* boxes;  // [nbox][8]: cx cy cz hx hy hz cos(yaw) sin(yaw)
   T* scratch;           // [n][34][W] rarely used per-lane rows (sim_step.cuh G_*)
+  // uniform grid over the boxes' loose xy footprints (stp_set_terrain)
+  int grid_nx, grid_ny;
+  double grid_x0, grid_y0, grid_inv;
+  const int* cell_start;  // [nx*ny + 1]
+  const int* cell_list;   // box indices, ascending within a cell
+  const int4* box_cells;  // per box: first/last cell (x0, y0, x1, y1)
 };
 
 enum { C_FRAME = 0, C_FLAG = 1, C_FALL = 2, C_NEXTP = 3, C_EPISODE = 4, C_FLAGDRAW = 5, C_PERTDRAW = 6 };
@@ -383,6 +389,25 @@ __device__ __forceinline__ double terrain_height_dev(const double* boxes, int n,
   double h = 0.0;
   for (int i = 0; i < n; ++i) {
     const double* bx = boxes + 8 * i;
+    const double dx = x - bx[0], dy = y - bx[1];
+    const double lx = bx[6] * dx + bx[7] * dy;
+    const double ly = -bx[7] * dx + bx[6] * dy;
+    if (fabs(lx) <= bx[3] && fabs(ly) <= bx[4]) h = fmax(h, bx[2] + bx[5]);
+  }
+  return h;
+}
+
+// terrain_height through the grid: the box footprints covering (x, y)
+// are all registered in the cell containing it.
+template <class T>
+__device__ __forceinline__ double terrain_height_grid(const KArgs<T>& a, double x, double y) {
+  if (a.grid_nx <= 0) return terrain_height_dev(a.boxes, a.n_boxes, x, y);
+  const int cx = int(floor((x - a.grid_x0) * a.grid_inv)), cy = int(floor((y - a.grid_y0) * a.grid_inv));
+  if (cx < 0 || cy < 0 || cx >= a.grid_nx || cy >= a.grid_ny) return 0.0;
+  const int c = cy * a.grid_nx + cx;
+  double h = 0.0;
+  for (int k = a.cell_start[c]; k < a.cell_start[c + 1]; ++k) {
+    const double* bx = a.boxes + 8 * a.cell_list[k];
     const double dx = x - bx[0], dy = y - bx[1];
     const double lx = bx[6] * dx + bx[7] * dy;
     const double ly = -bx[7] * dx + bx[6] * dy;

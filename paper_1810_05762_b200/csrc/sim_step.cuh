@@ -452,10 +452,11 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
 
     // ---------------- K1: contacts (detect_contacts, collide.cpp:270-299) -
     // slot k of this lane: rows R_CT + 11k: n(3) r(3) t1(3) d b; sep kept in d's row until rows are built
-    auto add_contact = [&](v3<T> p, v3<T> n, T sep) {
+    auto add_contact = [&](v3<T> p, v3<T> n, T sep, int key = -1) {
       if (nc < CPB) {
         const int r0 = R_CT + 11 * nc;
         const v3<T> r = p - x;
+        L.at(r0 + 6) = T(key);
         L.at(r0 + 0) = n.x;
         L.at(r0 + 1) = n.y;
         L.at(r0 + 2) = n.z;
@@ -499,9 +500,9 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           if (sep < margin) add_contact(p0 - up * rad, up, sep);
         } else if (shp == STP_CAPSULE) {
           const T s0 = p0.z - rad;
-          if (s0 < margin) add_contact(p0 - up * rad, up, s0);
+          if (s0 < margin) add_contact(p0 - up * rad, up, s0, -2);
           const T s1 = p1.z - rad;
-          if (s1 < margin) add_contact(p1 - up * rad, up, s1);
+          if (s1 < margin) add_contact(p1 - up * rad, up, s1, -1);
         } else if constexpr (CPB > 2) {  // dynamic boxes: 8 corners (host picks CPB = 8)
           for (int cx = -1; cx <= 1; cx += 2)
             for (int cy = -1; cy <= 1; cy += 2)
@@ -520,14 +521,14 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
         const double ox = a.origin[2 * e], oy = a.origin[2 * e + 1];
         const v3<T> lo{min(p0.x, p1.x) - rad, min(p0.y, p1.y) - rad, min(p0.z, p1.z) - rad};
         const v3<T> hi{max(p0.x, p1.x) + rad, max(p0.y, p1.y) + rad, max(p0.z, p1.z) + rad};
-        for (int i = 0; i < a.n_boxes; ++i) {
+        auto test_box = [&](int i) {
           const double* bx = a.boxes + 8 * i;
           const v3<T> c{T(bx[0] - ox), T(bx[1] - oy), T(bx[2])};  // relative to the env origin
           const v3<T> h{T(bx[3]), T(bx[4]), T(bx[5])};
           const T ex = h.x + h.y;
           if (hi.x + margin < c.x - ex || lo.x - margin > c.x + ex || hi.y + margin < c.y - ex ||
               lo.y - margin > c.y + ex || hi.z + margin < c.z - h.z || lo.z - margin > c.z + h.z)
-            continue;
+            return;
           const T cs = T(bx[6]), sn = T(bx[7]);
           // point_obb, collide.cpp:140-173
           auto point_box = [&](v3<T> p, v3<T>& nrm, v3<T>& surf) -> T {
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           v3<T> nrm, surf;
           if (shp == STP_SPHERE) {
             const T d = point_box(p0, nrm, surf);
-            if (d - rad < margin) add_contact(surf, nrm, d - rad);
+            if (d - rad < margin) add_contact(surf, nrm, d - rad, 4 * i);
           } else {
             // collide_capsule_obb, collide.cpp:183-214
             const v3<T> seg = p1 - p0;
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
             {
               const T d = point_box(p0 + seg * tmid, nrm, surf);
               if (d - rad < margin) {
-                add_contact(surf, nrm, d - rad);
+                add_contact(surf, nrm, d - rad, 4 * i);
                 mid_added = true;
               }
             }
@@ -598,9 +599,48 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
               const T tt = T(te);
               if (mid_added && fabs(tt - tmid) < T(0.05)) continue;
               const T d = point_box(p0 + seg * tt, nrm, surf);
-              if (d - rad < margin) add_contact(surf, nrm, d - rad);
+              if (d - rad < margin) add_contact(surf, nrm, d - rad, 4 * i + 1 + te);
             }
           }
+        };
+        if (a.grid_nx > 0) {
+          // uniform-grid broadphase over the boxes' loose footprints; each box is
+          // visited once (in the first shared cell) and the slots are re-sorted
+          // by (box index, mid/end) afterwards: the reference's all-boxes loop
+          // order (collide.cpp:287-298) is restored exactly.
+          const double wx0 = ox + double(lo.x) - double(margin), wx1 = ox + double(hi.x) + double(margin);
+          const double wy0 = oy + double(lo.y) - double(margin), wy1 = oy + double(hi.y) + double(margin);
+          auto cell = [&](double w, double g0, int n) {
+            const int c = int(floor((w - g0) * a.grid_inv));
+            return c < 0 ? 0 : (c >= n ? n - 1 : c);
+          };
+          const int cx0 = cell(wx0, a.grid_x0, a.grid_nx), cx1 = cell(wx1, a.grid_x0, a.grid_nx);
+          const int cy0 = cell(wy0, a.grid_y0, a.grid_ny), cy1 = cell(wy1, a.grid_y0, a.grid_ny);
+          for (int cy = cy0; cy <= cy1; ++cy)
+            for (int cx = cx0; cx <= cx1; ++cx) {
+              const int c = cy * a.grid_nx + cx;
+              for (int k = a.cell_start[c]; k < a.cell_start[c + 1]; ++k) {
+                const int i = a.cell_list[k];
+                const int4 bc = a.box_cells[i];
+                if (cx != max(bc.x, cx0) || cy != max(bc.y, cy0)) continue;  // visited in an earlier cell
+                test_box(i);
+              }
+            }
+          // insertion sort of this lane's slots by key (plane contacts keep key < 0)
+          for (int s1 = 1; s1 < nc && s1 < CPB; ++s1) {
+            for (int s2 = s1; s2 > 0; --s2) {
+              const int ra = R_CT + 11 * (s2 - 1), rb = R_CT + 11 * s2;
+              if (!(L.at(ra + 6) > L.at(rb + 6))) break;
+#pragma unroll
+              for (int f = 0; f < 11; ++f) {
+                const T tmp = L.at(ra + f);
+                L.at(ra + f) = L.at(rb + f);
+                L.at(rb + f) = tmp;
+              }
+            }
+          }
+        } else {
+          for (int i = 0; i < a.n_boxes; ++i) test_box(i);
         }
       }
     }
@@ -1327,7 +1367,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           const double fx = geo_offset(i - 7), fy = geo_offset(jj - 5);
           const double px = rx + double(cy) * fx - double(sy) * fy;
           const double py = ry + double(sy) * fx + double(cy) * fy;
-          o[11 + 3 * J + M.n_feet + k] = float(terrain_height_dev(a.boxes, a.n_boxes, px, py) - double(xr2.z));
+          o[11 + 3 * J + M.n_feet + k] = float(terrain_height_grid(a, px, py) - double(xr2.z));
         }
       }
     }

@@ -222,3 +222,56 @@ def test_full_size_properties():
     assert rep["overflow"].sum() == 0
     assert rep["failed"].sum() == 0
     assert (rep["newton_iterations"] == 4).all()
+
+
+def _terrain(n_boxes=160, seed=3):
+    spec = abi.TerrainSpec(count=n_boxes, dim_lo=0.2, dim_hi=1.0, x_lo=-3.0, x_hi=66.0, y_lo=-3.0, y_hi=3.0,
+                           yaw_lo=0.0, yaw_hi=3.141592653589793, seed=seed)
+    boxes = (abi.StaticBox * n_boxes)()
+    assert abi.load().stp_generate_terrain(spec, boxes, n_boxes) == n_boxes
+    return list(boxes)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_terrain_contacts_and_height_map(precision):
+    """HFH on complex terrain (config C4 shape): capsule/sphere vs yaw-rotated
+    static boxes (collide.cpp:175-214) and the 15x11 height map
+    (terrain_height, collide.cpp:348-359), teacher-forced against the oracle."""
+    n = 32
+    boxes = _terrain()
+    g = VecEnv("hfh_terrain", n_envs=n, precision=precision, seed=13, terrain=boxes)
+    o = oracle.OracleEnv(g.model, g.task, g.cfg, n, seed=13, terrain=boxes)
+    tm = np.array([g.model.joints[j].max_torque for j in range(g.action_dim)])
+    box_contacts = 0
+    mism = 0
+    for t in range(20):
+        # drop the humanoids from 0.5 m so they land on the boxes
+        s = o.get_state()
+        if t == 0:
+            s[..., 2] += 0.5
+            o.set_state(s)
+        g.set_state(s)
+        tq = o.random_actions(t) * tm
+        o.physics_step(tq)
+        g.physics_step(tq)
+        co, cg = o.contact_arrays(g.contact_capacity), g.contact_arrays()
+        box_contacts += int((np.abs(co["normal"][..., 2] - 1.0) > 1e-9).sum())
+        for e in range(n):
+            c = co["count"][e]
+            if c != cg["count"][e] or not np.array_equal(co["body_a"][e, :c], cg["body_a"][e, :c]):
+                near = np.abs(co["separation"][e, :c] - g.cfg.contact_margin).min(initial=1.0)
+                if precision == "f64" or near > 1e-4:
+                    mism += 1
+        if precision == "f64":
+            assert np.abs(o.get_state()[..., :3] - g.get_state()[..., :3]).max() <= 1e-6
+    assert box_contacts > 0  # the boxes were actually hit
+    assert mism == 0
+    assert g.report()["overflow"].sum() == 0
+    # height map: obs tail equals terrain_height(sample) - root z
+    o.set_state(g.get_state())
+    ts = g.task_state()
+    o.set_task_state(ts["target"], ts["counters"], ts["last_tau"])
+    og = g.reset(np.zeros(n, np.uint8)).cpu().numpy()
+    oo = o.observe()
+    assert np.abs(og[:, -165:] - oo[:, -165:]).max() <= 1e-4
+    assert (np.abs(oo[:, -165:] + oo[:, :1]) > 1e-3).any()  # some samples see a box
