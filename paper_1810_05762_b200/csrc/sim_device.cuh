@@ -30,6 +30,13 @@ struct DevModel {
   int max_depth;
   int child_list[4][32];  // up to 4 child bodies per body (-1 = none)
   int max_children;
+  // shuffle schedule of the child -> parent sum in the PCR matvec (host-built,
+  // sim_host.cu gather_schedule): per round a source lane and two 0/1 weights,
+  // into the receiver's y (parent sum) or its own t (sibling pre-accumulation)
+  int gather_rounds;
+  int gather_has_t[4];
+  int gather_src[4][32];
+  T gather_wy[4][32], gather_wt[4][32];
   int lane_of_joint[STP_MAX_JOINTS];
   T radius[32], half_len[32], hext[3][32], lpos[3][32], lrot[4][32];
   T mass[32], inv_mass[32], inertia[3][32], inv_inertia[3][32];

@@ -113,6 +113,72 @@ bool single_island(const stp_model& m) {
   return true;
 }
 
+// Child -> parent summation schedule for the PCR matvec.  Every round each
+// lane pulls one value (one shuffle); a parent needs the sum of its
+// children's contributions, so a parent with m children needs m rounds unless
+// siblings are pre-added: with R rounds, children are paired (head, tail), the
+// head adds the tail's value into its own contribution in round 0 and the
+// parent reads the head in a later round.  R is the smallest count that fits
+// (2 for the Humanoid: torso and pelvis; 3 for the Ant's 4-legged torso).
+template <class T>
+void gather_schedule(const stp_model& m, stp::DevModel<T>& d) {
+  const int n = m.n_bodies;
+  std::vector<std::vector<int>> kids(n);
+  for (int j = 0; j < m.n_joints; ++j) kids[m.joints[j].parent].push_back(m.joints[j].child);
+  for (int R = 1; R <= 4; ++R) {
+    int slot_src[4][32], slot_kind[4][32];  // kind 0 none, 1 Y, 2 T
+    for (int r = 0; r < 4; ++r)
+      for (int b = 0; b < 32; ++b) {
+        slot_src[r][b] = b;
+        slot_kind[r][b] = 0;
+      }
+    bool ok = true;
+    std::vector<std::vector<int>> sources(n);  // what each parent reads (Y)
+    std::vector<int> min_round(32, 0);
+    for (int p = 0; p < n && ok; ++p) {
+      const auto& k = kids[p];
+      if (int(k.size()) <= R) {
+        sources[p] = k;
+        continue;
+      }
+      for (size_t i = 0; i < k.size(); i += 2) {
+        sources[p].push_back(k[i]);
+        if (i + 1 < k.size()) {
+          if (slot_kind[0][k[i]] != 0) ok = false;
+          slot_src[0][k[i]] = k[i + 1];
+          slot_kind[0][k[i]] = 2;
+          min_round[k[i]] = 1;
+        }
+      }
+      if (int(sources[p].size()) > R) ok = false;
+    }
+    for (int p = 0; p < n && ok; ++p) {
+      for (int s : sources[p]) {
+        int r = min_round[s];
+        while (r < R && slot_kind[r][p] != 0) ++r;
+        if (r >= R) {
+          ok = false;
+          break;
+        }
+        slot_src[r][p] = s;
+        slot_kind[r][p] = 1;
+      }
+    }
+    if (!ok) continue;
+    d.gather_rounds = R;
+    for (int r = 0; r < 4; ++r) {
+      d.gather_has_t[r] = 0;
+      for (int b = 0; b < 32; ++b) {
+        d.gather_src[r][b] = slot_src[r][b];
+        d.gather_wy[r][b] = T(slot_kind[r][b] == 1 ? 1 : 0);
+        d.gather_wt[r][b] = T(slot_kind[r][b] == 2 ? 1 : 0);
+        if (slot_kind[r][b] == 2) d.gather_has_t[r] = 1;
+      }
+    }
+    return;
+  }
+}
+
 template <class T>
 void build_dev_model(const stp_model& m, const stp_step_config& cfg, stp::DevModel<T>& d) {
   std::memset(&d, 0, sizeof(d));
@@ -187,6 +253,7 @@ void build_dev_model(const stp_model& m, const stp_step_config& cfg, stp::DevMod
       if ((d.child_mask[b] >> c) & 1) d.child_list[n++ < 4 ? n - 1 : 3][b] = c;
     d.max_children = std::max(d.max_children, n);
   }
+  gather_schedule(m, d);
   int maxd = 0;
   for (int b = 0; b < m.n_bodies; ++b) {  // topological order: parent < child
     d.depth[b] = d.parent[b] < 0 ? 0 : d.depth[d.parent[b]] + 1;

@@ -42,6 +42,11 @@ struct Lane {
   int lane, base, b, par_src, maxc;
   int kid[4];  // child lanes (-1 = none)
   bool has_off, quirk, diag_h;
+  bool any_quirk, any_diag;  // segment-uniform guards of the rare paths
+  int grounds;               // child-gather schedule (DevModel::gather_*)
+  unsigned gsrc;             // 8-bit source lane per round
+  T gwy[4], gwt[4];
+  int ghas_t[4];
   T lim_s;  // -(sum of active limit weights): angular rank-1 term of H(c,p)
   v3<T> lim_a;
   T Hh[36];  // transformed off-diagonal block L_b^-1 H(b, parent) L_parent^-T
@@ -76,31 +81,33 @@ struct Lane {
     T vp[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) vp[k] = __shfl_sync(mask, v[k], par_src, W);
-    if (diag_h) {
 #pragma unroll
-      for (int r = 0; r < 6; ++r) {
-        T s = T(0);
+    for (int k = 0; k < 6; ++k) y[k] = v[k];
+    if (any_diag) {  // segment-uniform: some own block was not positive definite
+      if (diag_h) {
 #pragma unroll
-        for (int c = 0; c < 6; ++c) s += g(G_HD + sidx(r, c)) * v[c];
-        y[r] = s;
-      }
-    } else {
+        for (int r = 0; r < 6; ++r) {
+          T s = T(0);
 #pragma unroll
-      for (int k = 0; k < 6; ++k) y[k] = v[k];
-    }
-    T t[6] = {0, 0, 0, 0, 0, 0};
-    if (has_off) {
-#pragma unroll
-      for (int r = 0; r < 6; ++r) {
-        T s = T(0);
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          s += Hh[r * 6 + c] * vp[c];
-          t[c] += Hh[r * 6 + c] * v[r];
+          for (int c = 0; c < 6; ++c) s += g(G_HD + sidx(r, c)) * v[c];
+          y[r] = s;
         }
-        y[r] += s;
       }
-      if (quirk) {  // Ahat(p,c) = Hh^T - d0 qa qc^T
+    }
+    // Hh is zero on lanes without a parent block: no branch
+    T t[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      T s = T(0);
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        s += Hh[r * 6 + c] * vp[c];
+        t[c] += Hh[r * 6 + c] * v[r];
+      }
+      y[r] += s;
+    }
+    if (any_quirk) {  // segment-uniform; Ahat(p,c) = Hh^T - d0 qa qc^T
+      if (quirk) {
         T s0 = T(0);
 #pragma unroll
         for (int k = 0; k < 6; ++k) s0 += g(G_QH + 7 + k) * v[k];
@@ -109,14 +116,16 @@ struct Lane {
         for (int k = 0; k < 6; ++k) t[k] -= s0 * g(G_QH + 1 + k);
       }
     }
+    // children's contributions: scheduled rounds of shuffles (DevModel::gather_*)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (i < maxc) {
-        const int src = kid[i] >= 0 ? kid[i] : b;
+    for (int r = 0; r < 4; ++r) {
+      if (r < grounds) {
+        const int src = int((gsrc >> (8 * r)) & 0xffu);
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-          const T g = __shfl_sync(mask, t[k], src, W);
-          if (kid[i] >= 0) y[k] += g;
+          const T gk = __shfl_sync(mask, t[k], src, W);
+          y[k] += gwy[r] * gk;
+          if (ghas_t[r]) t[k] += gwt[r] * gk;
         }
       }
     }
@@ -306,7 +315,7 @@ __device__ __forceinline__ void symv(const T (&P)[21], const T (&v)[6], T (&y)[6
 
 // alpha / beta of the PCR recurrences: fp32 uses reciprocal + multiply
 // (two roundings; the f64 parity instrument keeps IEEE division).
-__device__ __forceinline__ float fdiv(float a, float b) { return a * __frcp_rn(b); }
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdividef(a, b); }
 __device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
 
 #ifndef STP_PIPELINED_CR
@@ -372,6 +381,17 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
   L.has_off = dyn && pdyn && jnt >= 0;
   L.quirk = false;
   L.diag_h = false;
+  L.any_quirk = false;
+  L.any_diag = false;
+  L.grounds = M.gather_rounds;
+  L.gsrc = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    L.gsrc |= unsigned(M.gather_src[r][b] & 0xff) << (8 * r);
+    L.gwy[r] = M.gather_wy[r][b];
+    L.gwt[r] = M.gather_wt[r][b];
+    L.ghas_t[r] = M.gather_has_t[r];
+  }
   L.lim_s = T(0);
   L.lim_a = {0, 0, 0};
 
@@ -1010,6 +1030,8 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           T Mi[21];
           const bool ok = factor6(H, Lc, rd, Mi, dyn);
           L.diag_h = dyn && !ok;
+          L.any_diag = __any_sync(mask, L.diag_h);
+          L.any_quirk = __any_sync(mask, L.quirk);
 #pragma unroll
           for (int k = 0; k < 6; ++k) L.at(R_SCAT + k) = rd[k];
           if (L.diag_h) {
@@ -1081,50 +1103,23 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           }
           return s0;
         };
-        // One apply_hat call site (code size): phase 0 forms rhat = bhat - Ahat xhat,
-        // phase 1 the first direction, phase 2 the CR iterations
-        // (solve_krylov_inplace loop, krylov.cpp:141-163).
         T rh[6], ar[6], ph[6], ap[6];
+        L.apply_hat(xh, ar);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) rh[k] = dyn ? bh[k] - ar[k] : T(0);
+        L.apply_hat(rh, ar);
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-          rh[k] = xh[k];  // phase 0 applies Ahat to xhat
-          ph[k] = T(0);
-          ap[k] = T(0);
+          ph[k] = rh[k];
+          ap[k] = ar[k];
         }
+        T zaz = dot6(rh, ar), rr = res_norm2(rh);
+        seg_sum2<W>(zaz, rr, mask);
         const T tol2 = cf.tol * cf.tol * bb;  // ||r|| > tol ||b||, compared squared
-        T zaz = T(0);
-        int kk = 0, phase = 0;
-        while (true) {
-          L.apply_hat(rh, ar);
-          if (phase == 0) {
-#pragma unroll
-            for (int k = 0; k < 6; ++k) rh[k] = dyn ? bh[k] - ar[k] : T(0);
-            phase = 1;
-            continue;
-          }
-          T zn = dot6(rh, ar), rr = res_norm2(rh);
-          seg_sum2<W>(rr, zn, mask);
-          if (phase == 1) {
-#pragma unroll
-            for (int k = 0; k < 6; ++k) {
-              ph[k] = rh[k];
-              ap[k] = ar[k];
-            }
-            zaz = zn;
-            phase = 2;
-          } else {
-            if (rr <= tol2) break;
-            const T beta = fdiv(zn, zaz);
-            zaz = zn;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) {
-              ph[k] = rh[k] + beta * ph[k];
-              ap[k] = ar[k] + beta * ap[k];
-            }
-          }
-          if (!(kk < cf.kmax && rr > tol2)) break;
+        int kk = 0;
+        while (kk < cf.kmax && rr > tol2) {
           const T denom = seg_sum<W>(dot6(ap, ap), mask);
-          if (!(denom > T(0)) || !(zaz > T(0))) break;  // breakdown (:144)
+          if (!(denom > T(0)) || !(zaz > T(0))) break;  // breakdown (krylov.cpp:144)
           const T alpha = fdiv(zaz, denom);
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
@@ -1132,6 +1127,18 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
             rh[k] -= alpha * ap[k];
           }
           ++kk;
+          L.apply_hat(rh, ar);  // before the exit test: one spare product at exit
+          T zn = dot6(rh, ar);
+          rr = res_norm2(rh);
+          seg_sum2<W>(rr, zn, mask);
+          if (rr <= tol2) break;
+          const T beta = fdiv(zn, zaz);
+          zaz = zn;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            ph[k] = rh[k] + beta * ph[k];
+            ap[k] = ar[k] + beta * ap[k];
+          }
         }
         // back to velocities: solve L^T u = xhat (reciprocal diagonal parked in R_SCAT)
 #pragma unroll
