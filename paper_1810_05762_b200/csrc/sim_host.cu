@@ -477,7 +477,7 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
       (rc = dalloc(s, &s->d_cdata, N * s->cap * stp::kCData * sizeof(double))) ||
       (rc = dalloc(s, &s->d_act, N * std::max(1, s->J) * 4)) || (rc = dalloc(s, &s->d_obs, N * s->obs_dim * 4)) ||
       (rc = dalloc(s, &s->d_rew, N * 4)) || (rc = dalloc(s, &s->d_done, N)) ||
-      (rc = dalloc(s, &s->d_scratch, N * 34 * s->W * ts)))
+      (rc = dalloc(s, &s->d_scratch, N * 55 * s->W * ts)))
     return bail(rc);
   if (precision == STP_PRECISION_F64) {
     stp::DevModel<double> dm;

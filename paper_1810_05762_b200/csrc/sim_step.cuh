@@ -28,7 +28,8 @@ constexpr int R_CT = 86;    // 11 per contact slot: n(3) r(3) t1(3) d b
 // Rarely used per-lane rows live in a global scratch buffer (L1-resident):
 constexpr int G_QH = 0;     // 13: quirk in the transformed system: d0, qa (6), qc (6)
 constexpr int G_HD = 13;    // 21: diagonal block, kept only when it is not positive definite
-constexpr int kScratchRows = 34;
+constexpr int G_LC = 34;    // 21: Cholesky factor L of the own block (exact residual test, back-substitution)
+constexpr int kScratchRows = 55;
 template <int CPB>
 __host__ __device__ constexpr int smem_rows() {
   return R_CT + 11 * CPB;
@@ -1026,9 +1027,20 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
         }
         T Lc[21], rd[6];
         T bh[6], xh[6];
+        T lbw;
         {
           T Mi[21];
           const bool ok = factor6(H, Lc, rd, Mi, dyn);
+          {
+            // sigma_min(L)^2 >= 1 / ||L^-1||_F^2: per-lane weight of the cheap
+            // lower bound sum_b lbw_b |rhat_b|^2 <= ||r||^2 (see the PCR loop)
+            T f = T(0);
+#pragma unroll
+            for (int k = 0; k < 21; ++k) f += Mi[k] * Mi[k];
+            lbw = dyn ? T(1) / f : T(0);
+          }
+#pragma unroll
+          for (int k = 0; k < 21; ++k) L.g(G_LC + k) = Lc[k];
           L.diag_h = dyn && !ok;
           L.any_diag = __any_sync(mask, L.diag_h);
           L.any_quirk = __any_sync(mask, L.quirk);
@@ -1092,16 +1104,24 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
             xh[i] = sx;
           }
         }
-        auto res_norm2 = [&](const T (&rh)[6]) {  // |L rhat|^2 = ||r||^2 of the reference
+        // Exit test of the reference, ||r|| > tol ||b|| (krylov.cpp:141, :154),
+        // compared squared.  ||r|| = |L rhat| costs 27 FMA per lane, so each
+        // iteration first reduces the rigorous lower bound
+        // sum_b |rhat_b|^2 / ||L_b^-1||_F^2 <= ||r||^2; only when that bound
+        // does not already exceed tol^2 ||b||^2 (by a rounding margin) is the
+        // exact norm formed.  The exit decisions are the reference's.
+        const T tol2 = cf.tol * cf.tol * bb;
+        const T tol2_safe = tol2 * T(1.0001);
+        auto res_exact = [&](const T (&rh)[6]) {  // |L rhat|^2, L from the scratch rows
           T s0 = T(0);
 #pragma unroll
           for (int i = 0; i < 6; ++i) {
             T ri = T(0);
 #pragma unroll
-            for (int k = 0; k <= i; ++k) ri += Lc[tri(i, k)] * rh[k];
+            for (int k = 0; k <= i; ++k) ri += L.g(G_LC + tri(i, k)) * rh[k];
             s0 += ri * ri;
           }
-          return s0;
+          return seg_sum<W>(s0, mask);
         };
         T rh[6], ar[6], ph[6], ap[6];
         L.apply_hat(xh, ar);
@@ -1113,11 +1133,11 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           ph[k] = rh[k];
           ap[k] = ar[k];
         }
-        T zaz = dot6(rh, ar), rr = res_norm2(rh);
-        seg_sum2<W>(zaz, rr, mask);
-        const T tol2 = cf.tol * cf.tol * bb;  // ||r|| > tol ||b||, compared squared
+        T zaz = dot6(rh, ar), lb = lbw * dot6(rh, rh);
+        seg_sum2<W>(zaz, lb, mask);
+        bool above = lb > tol2_safe || res_exact(rh) > tol2;
         int kk = 0;
-        while (kk < cf.kmax && rr > tol2) {
+        while (kk < cf.kmax && above) {
           const T denom = seg_sum<W>(dot6(ap, ap), mask);
           if (!(denom > T(0)) || !(zaz > T(0))) break;  // breakdown (krylov.cpp:144)
           const T alpha = fdiv(zaz, denom);
@@ -1129,9 +1149,10 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           ++kk;
           L.apply_hat(rh, ar);  // before the exit test: one spare product at exit
           T zn = dot6(rh, ar);
-          rr = res_norm2(rh);
-          seg_sum2<W>(rr, zn, mask);
-          if (rr <= tol2) break;
+          lb = lbw * dot6(rh, rh);
+          seg_sum2<W>(lb, zn, mask);
+          above = lb > tol2_safe || res_exact(rh) > tol2;
+          if (!above) break;
           const T beta = fdiv(zn, zaz);
           zaz = zn;
 #pragma unroll
@@ -1145,7 +1166,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
         for (int i = 5; i >= 0; --i) {
           T sum = xh[i];
 #pragma unroll
-          for (int k = i + 1; k < 6; ++k) sum -= Lc[tri(k, i)] * u[k];
+          for (int k = i + 1; k < 6; ++k) sum -= L.g(G_LC + tri(k, i)) * u[k];
           u[i] = sum * L.at(R_SCAT + i);
         }
         krylov_total += kk;
