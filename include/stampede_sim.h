@@ -250,8 +250,22 @@ int stp_get_task_state(stp_sim* sim, double* target, int32_t* counters, double* 
 int stp_set_task_state(stp_sim* sim, const double* target, const int32_t* counters,
                        const double* last_torque);
 
-/* Force the deterministic CPU-side pieces to be identical across ranks:
- * nothing here talks to other GPUs (no env-state exchange). */
+/* --- K4: rollout policy forward on tcgen05 tensor cores ---------------------
+ * SPEC.md:366-409 (SELU MLP, Gaussian policy) and :446-454 (whitening):
+ *   x = clip((obs - mean) / std, +-10);  mean = MLP_pi(x);  value = MLP_v(x);
+ *   action = mean + exp(log_std) * eps (eps ~ N(0,1), counter-based,
+ *   derive_seed(seed, 6, env<<32 | step)); logp = log N(action; mean, std).
+ * dims_* = {in, h1, h2, h3, out} (widths <= 256); w_*[l] = packed bf16
+ * weights of layer l, K-major core-matrix layout [ceil16(in)/8][ceil16(out)][8]
+ * (paper_1810_05762_b200/policy.py pack_linear); b_*[l] = fp32 bias padded to
+ * ceil16(out).  All pointers are device pointers; asynchronous on `stream`.
+ * action_out / logp_out / value_out may be NULL. */
+int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_dim, const float* obs_mean,
+                       const float* obs_std, const int32_t* dims_pi, const void* const* w_pi,
+                       const float* const* b_pi, const int32_t* dims_v, const void* const* w_v,
+                       const float* const* b_v, const float* log_std, uint64_t seed, uint64_t step,
+                       int64_t env_offset, float* mean_out, float* action_out, float* logp_out,
+                       float* value_out, void* stream);
 
 #ifdef __cplusplus
 }

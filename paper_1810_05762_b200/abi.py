@@ -165,6 +165,8 @@ SIGNATURES = [
     ("stp_get_report", _I, [_P, _P, _P, _P, _P]),
     ("stp_get_task_state", _I, [_P, _P, _P, _P]),
     ("stp_set_task_state", _I, [_P, _P, _P, _P]),
+    ("stp_policy_forward", _I, [_P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_uint64, C.c_uint64,
+                                C.c_int64, _P, _P, _P, _P, _P]),
 ]
 
 _lib = None

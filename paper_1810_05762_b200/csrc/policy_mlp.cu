@@ -1,0 +1,366 @@
+// K4: rollout policy forward on the 5th-generation tensor cores.
+//
+// SPEC.md:366-409 (SELU MLP, Gaussian policy), :446-454 (observation
+// whitening), Table 4 (Humanoid [256, 128, 64], Ant [128, 64, 32]).
+// One CTA = 128 environments = one M=128 tcgen05 tile:
+//   obs (fp32, HBM) -> whiten + clip(+-10) -> bf16 operand in smem
+//   -> 4 x tcgen05.mma (bf16 x bf16 -> fp32 accumulator in TMEM)
+//   -> tcgen05.ld epilogue: bias + SELU -> bf16 -> next layer's smem operand
+//   -> last layer: mean (+ log_std, counter-based Gaussian sample, log-prob)
+// for the policy net, then the same chain for the value net.  Weights (packed
+// bf16, K-major 8x16B core-matrix layout) are staged into smem with TMA bulk
+// copies (cp.async.bulk) completing on an mbarrier.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "stampede_sim.h"
+#include "stp_error.h"
+#include "stp_rng.h"
+
+namespace {
+
+constexpr int kM = 128;  // rows (envs) per CTA = UMMA M
+constexpr float kSeluL = 1.0507009873554805f, kSeluA = 1.6732632423543772f;
+
+struct MlpDims {
+  int k[4];  // padded input width of layer l (multiple of 16)
+  int n[4];  // padded output width of layer l (multiple of 16)
+  int out;   // real output width of the last layer
+};
+
+struct NetPtrs {
+  const __nv_bfloat16* w[4];  // packed [k/8][n][8] bf16
+  const float* bias[4];       // padded to n
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_NONE K-major canonical layout
+// (cute/arch/mma_sm100_desc.hpp SmemDescriptor): core matrix = 8 rows x 16 B
+// contiguous; LBO = byte stride between K-adjacent core matrices, SBO = byte
+// stride between 8-row groups.  Our packing [k/8][rows][8] gives SBO = 128 B
+// and LBO = rows * 16 B.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3fff);
+  d |= uint64_t((lbo >> 4) & 0x3fff) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3fff) << 32;
+  d |= uint64_t(1) << 46;  // version = 1 (Blackwell)
+  // base_offset 0, lbo_mode 0, layout_type 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// Instruction descriptor kind::f16: bf16 x bf16 -> f32, both K-major
+// (cute/arch/mma_sm100_desc.hpp InstrDescriptor).
+__device__ __forceinline__ uint32_t umma_idesc(int m, int n) {
+  uint32_t d = 0;
+  d |= 1u << 4;                    // c_format = F32
+  d |= 1u << 7;                    // a_format = BF16
+  d |= 1u << 10;                   // b_format = BF16
+  d |= uint32_t(n >> 3) << 17;     // n_dim
+  d |= uint32_t(m >> 4) << 24;     // m_dim
+  return d;
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, int acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+// 1-D TMA bulk copy global -> shared, completing tx bytes on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+
+// 16 fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float selu(float x) { return x > 0.f ? kSeluL * x : kSeluL * kSeluA * expm1f(x); }
+
+// Write 8 bf16 (16 B) of row `row`, K-chunk `kc` into a [k/8][128][8] operand.
+__device__ __forceinline__ void st_chunk(__nv_bfloat16* buf, int kc, int row, const float* x8) {
+  __nv_bfloat162 p[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(x8[2 * i], x8[2 * i + 1]);
+  *reinterpret_cast<uint4*>(buf + (size_t(kc) * kM + row) * 8) = *reinterpret_cast<uint4*>(p);
+}
+
+struct Smem {
+  uint64_t bar_w;    // weights landed
+  uint64_t bar_mma;  // layer accumulator ready
+  uint32_t tmem;
+};
+
+// One 4-layer net over the CTA's 128 rows; A operand of layer 0 already in abuf0.
+// Returns with the final accumulator (n[3] columns) in TMEM.
+__device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4], __nv_bfloat16* abuf0,
+                        __nv_bfloat16* abuf1, Smem* sh, uint32_t& wphase, uint32_t& mphase, int tid) {
+  const int warp = tid >> 5;
+  // stage the 4 weight blobs (one TMA bulk copy each, one barrier)
+  if (tid == 0) {
+    uint32_t bytes = 0;
+    for (int l = 0; l < 4; ++l) bytes += uint32_t(D.k[l]) * D.n[l] * 2;
+    mbar_expect_tx(&sh->bar_w, bytes);
+    for (int l = 0; l < 4; ++l) bulk_g2s(wsm[l], P.w[l], uint32_t(D.k[l]) * D.n[l] * 2, &sh->bar_w);
+  }
+  mbar_wait(&sh->bar_w, wphase);
+  wphase ^= 1;
+  __nv_bfloat16* a_in = abuf0;
+  __nv_bfloat16* a_out = abuf1;
+  for (int l = 0; l < 4; ++l) {
+    fence_async_smem();  // generic-proxy operand writes -> visible to the tensor core
+    __syncthreads();
+    if (tid == 0) {
+      tc_after_sync();
+      const uint32_t idesc = umma_idesc(kM, D.n[l]);
+      const uint32_t a0 = smem_u32(a_in), b0 = smem_u32(wsm[l]);
+      for (int ks = 0; ks < D.k[l] / 16; ++ks) {
+        // K step of 16 = two 8-element core-matrix columns
+        const uint64_t da = umma_desc(a0 + uint32_t(ks) * 2 * kM * 16, kM * 16, 128);
+        const uint64_t db = umma_desc(b0 + uint32_t(ks) * 2 * D.n[l] * 16, uint32_t(D.n[l]) * 16, 128);
+        mma_bf16(sh->tmem, da, db, idesc, ks > 0);
+      }
+      umma_commit(&sh->bar_mma);
+    }
+    mbar_wait(&sh->bar_mma, mphase);
+    mphase ^= 1;
+    tc_after_sync();
+    if (l == 3) break;
+    // epilogue: bias + SELU -> bf16 -> next operand (this thread's row)
+    const uint32_t tbase = sh->tmem + (uint32_t(warp * 32) << 16);
+    for (int c0 = 0; c0 < D.n[l]; c0 += 16) {
+      float v[16];
+      tmem_ld16(tbase + uint32_t(c0), v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = selu(v[i] + P.bias[l][c0 + i]);
+      st_chunk(a_out, c0 / 8, tid, v);
+      st_chunk(a_out, c0 / 8 + 1, tid, v + 8);
+    }
+    tc_before_sync();
+    __nv_bfloat16* t = a_in;
+    a_in = a_out;
+    a_out = t;
+  }
+}
+
+// K4 kernel.  dims/pointers for the policy (pi) and value (v) nets.
+__global__ void __launch_bounds__(kM, 1)
+    k_policy_mlp(const float* __restrict__ obs, int n_envs, int obs_dim, const float* __restrict__ mean,
+                 const float* __restrict__ stdv, MlpDims Dpi, NetPtrs Ppi, MlpDims Dv, NetPtrs Pv,
+                 const float* __restrict__ log_std, uint64_t seed, uint64_t step, long long env_offset,
+                 float* __restrict__ mu_out, float* __restrict__ act_out, float* __restrict__ logp_out,
+                 float* __restrict__ v_out, int a0_elems, int a1_elems) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  Smem* sh = reinterpret_cast<Smem*>(smem);
+  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(smem + 1024);
+  // operand ping-pong: abuf0 holds layer 0/2 inputs, abuf1 layer 1/3 inputs
+  __nv_bfloat16* abuf0 = base;
+  __nv_bfloat16* abuf1 = base + a0_elems;
+  __nv_bfloat16* wbase = base + a0_elems + a1_elems;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int row = blockIdx.x * kM + tid;
+
+  if (tid == 0) {
+    mbar_init(&sh->bar_w, 1);
+    mbar_init(&sh->bar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {  // TMEM: 256 columns (max layer width)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&sh->tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+
+  // whitened, clipped observation row -> bf16 operand (RunningStat)
+  auto stage_obs = [&](int kpad) {
+    for (int kc = 0; kc < kpad / 8; ++kc) {
+      float x8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = kc * 8 + i;
+        float x = 0.f;
+        if (row < n_envs && c < obs_dim) {
+          x = (obs[size_t(row) * obs_dim + c] - mean[c]) / stdv[c];
+          x = fminf(fmaxf(x, -10.f), 10.f);
+        }
+        x8[i] = x;
+      }
+      st_chunk(abuf0, kc, tid, x8);
+    }
+  };
+  __nv_bfloat16* wsm[4];
+  uint32_t wphase = 0, mphase = 0;
+  const uint32_t tbase = sh->tmem + (uint32_t(warp * 32) << 16);
+
+  // ---- policy mean + Gaussian sample ------------------------
+  {
+    int off = 0;
+    for (int l = 0; l < 4; ++l) {
+      wsm[l] = wbase + off;
+      off += Dpi.k[l] * Dpi.n[l];
+    }
+    stage_obs(Dpi.k[0]);
+    run_net(Dpi, Ppi, wsm, abuf0, abuf1, sh, wphase, mphase, tid);
+    const uint64_t genv = uint64_t(env_offset + row);
+    const uint64_t s = stp_derive_seed(seed, 6 /* policy noise */, (genv << 32) | uint32_t(step));
+    float lp = 0.f;
+    for (int c0 = 0; c0 < Dpi.n[3]; c0 += 16) {
+      float v[16];
+      tmem_ld16(tbase + uint32_t(c0), v);
+      if (row < n_envs) {
+        for (int i = 0; i < 16; ++i) {
+          const int c = c0 + i;
+          if (c >= Dpi.out) break;
+          const float m = v[i] + Ppi.bias[3][c];
+          mu_out[size_t(row) * Dpi.out + c] = m;
+          if (act_out) {
+            // Box-Muller on two 24-bit counter-based uniforms
+            const float u1 = fmaxf(stp_uniformf(s, 2 * c), 1e-7f), u2 = stp_uniformf(s, 2 * c + 1);
+            const float eps = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+            const float sd = expf(log_std[c]);
+            act_out[size_t(row) * Dpi.out + c] = m + sd * eps;
+            lp += -0.5f * eps * eps - log_std[c] - 0.91893853320467274f;
+          }
+        }
+      }
+    }
+    if (logp_out && row < n_envs) logp_out[row] = lp;
+    tc_before_sync();
+  }
+  // ---- value net ---------------------------------------------------------------
+  if (v_out) {
+    __syncthreads();
+    int off = 0;
+    for (int l = 0; l < 4; ++l) {
+      wsm[l] = wbase + off;
+      off += Dv.k[l] * Dv.n[l];
+    }
+    stage_obs(Dv.k[0]);
+    run_net(Dv, Pv, wsm, abuf0, abuf1, sh, wphase, mphase, tid);
+    float v[16];
+    tmem_ld16(tbase, v);
+    if (row < n_envs) v_out[row] = v[0] + Pv.bias[3][0];
+    tc_before_sync();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_after_sync();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(sh->tmem));
+  }
+}
+
+}  // namespace
+
+extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_dim, const float* obs_mean,
+                                  const float* obs_std, const int32_t* dims_pi, const void* const* w_pi,
+                                  const float* const* b_pi, const int32_t* dims_v, const void* const* w_v,
+                                  const float* const* b_v, const float* log_std, uint64_t seed, uint64_t step,
+                                  int64_t env_offset, float* mean_out, float* action_out, float* logp_out,
+                                  float* value_out, void* stream) {
+  if (!obs || n_envs <= 0 || !dims_pi || !w_pi || !b_pi || !mean_out || !obs_mean || !obs_std)
+    return stp::fail(STP_EINVAL, "stp_policy_forward: bad arguments");
+  MlpDims Dpi{}, Dv{};
+  NetPtrs Ppi{}, Pv{};
+  // dims: [in, h1, h2, h3, out] real sizes
+  auto fill = [](const int32_t* d, MlpDims& D) {
+    auto pad16 = [](int x) { return (x + 15) / 16 * 16; };
+    for (int l = 0; l < 4; ++l) {
+      D.k[l] = pad16(d[l]);
+      D.n[l] = pad16(d[l + 1]);
+    }
+    D.out = d[4];
+  };
+  fill(dims_pi, Dpi);
+  for (int l = 0; l < 4; ++l) {
+    Ppi.w[l] = static_cast<const __nv_bfloat16*>(w_pi[l]);
+    Ppi.bias[l] = b_pi[l];
+  }
+  if (value_out) {
+    if (!dims_v || !w_v || !b_v) return stp::fail(STP_EINVAL, "stp_policy_forward: value net missing");
+    fill(dims_v, Dv);
+    for (int l = 0; l < 4; ++l) {
+      Pv.w[l] = static_cast<const __nv_bfloat16*>(w_v[l]);
+      Pv.bias[l] = b_v[l];
+    }
+  }
+  auto check = [](const MlpDims& D) {
+    for (int l = 0; l < 4; ++l)
+      if (D.n[l] > 256 || D.k[l] > 256) return false;  // one UMMA N per layer, 256 TMEM columns
+    return true;
+  };
+  if (!check(Dpi) || (value_out && !check(Dv)))
+    return stp::fail(STP_EINVAL, "stp_policy_forward: layer widths must be <= 256");
+  if (Dpi.k[0] != (obs_dim + 15) / 16 * 16) return stp::fail(STP_EINVAL, "stp_policy_forward: obs_dim mismatch");
+  auto welems = [](const MlpDims& D) {
+    int s = 0;
+    for (int l = 0; l < 4; ++l) s += D.k[l] * D.n[l];
+    return s;
+  };
+  const int wmax = value_out ? (welems(Dpi) > welems(Dv) ? welems(Dpi) : welems(Dv)) : welems(Dpi);
+  auto mx = [](int a, int b) { return a > b ? a : b; };
+  int c0 = mx(Dpi.k[0], Dpi.k[2]), c1 = mx(Dpi.k[1], Dpi.k[3]);
+  if (value_out) {
+    c0 = mx(c0, mx(Dv.k[0], Dv.k[2]));
+    c1 = mx(c1, mx(Dv.k[1], Dv.k[3]));
+  }
+  const int a0 = kM * c0, a1 = kM * c1;
+  const size_t smem = 1024 + size_t(a0 + a1 + wmax) * 2;
+  if (smem > 227 * 1024) return stp::fail(STP_EINVAL, "stp_policy_forward: network too large for shared memory");
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_policy_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_policy_mlp attr: ") + cudaGetErrorString(e));
+    configured = smem;
+  }
+  const int blocks = (n_envs + kM - 1) / kM;
+  k_policy_mlp<<<blocks, kM, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      obs, n_envs, obs_dim, obs_mean, obs_std, Dpi, Ppi, Dv, Pv, log_std, seed, step, env_offset, mean_out,
+      action_out, logp_out, value_out, a0, a1);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_policy_mlp: ") + cudaGetErrorString(e));
+  return STP_OK;
+}
