@@ -10,12 +10,9 @@
 //       auto-reset via hinge FK, observation
 // so the body state is read from HBM once and written once per step.
 //
-// The system matrix is never materialised in HBM: each lane keeps its 6x6
-// diagonal block (packed symmetric, 21 values) and its Cholesky factor in
-// registers and its off-diagonal block H(child, parent) in shared memory;
-// H(parent, child) = H(child, parent)^T is applied by the child lane and
-// gathered by the parent through shared memory (the articulation is a tree).
-// Dot products are segment reductions over warp shuffles.
+// The system matrix is never materialised in HBM (see sim_step.cuh for the
+// per-lane block layout and the split block-Jacobi PCR).  Dot products are
+// segment reductions over warp shuffles.
 #pragma once
 
 #include <type_traits>
@@ -80,12 +77,6 @@ __device__ __forceinline__ T seg_sum(T v, unsigned mask) {
   return v;
 }
 template <int W, class T>
-__device__ __forceinline__ T seg_max(T v, unsigned mask) {
-#pragma unroll
-  for (int off = W / 2; off > 0; off >>= 1) v = max(v, __shfl_xor_sync(mask, v, off, W));
-  return v;
-}
-template <int W, class T>
 __device__ __forceinline__ T from(T v, int src, unsigned mask) {
   return __shfl_sync(mask, v, src, W);
 }
@@ -97,11 +88,6 @@ template <int W, class T>
 __device__ __forceinline__ qt<T> from(qt<T> v, int src, unsigned mask) {
   return {__shfl_sync(mask, v.w, src, W), __shfl_sync(mask, v.x, src, W), __shfl_sync(mask, v.y, src, W),
           __shfl_sync(mask, v.z, src, W)};
-}
-
-template <class T>
-__device__ __forceinline__ T rcp_or_div(T num, T den) {
-  return num / den;
 }
 
 // packed symmetric 6x6 rank-1 update H += d j j^T (assemble, solver.cpp:337-338)
@@ -154,149 +140,6 @@ __device__ __forceinline__ T hinge_angle(qt<T> qp, qt<T> qc, qt<T> rest, v3<T> a
 template <class T>
 __device__ __forceinline__ v3<T> ldv(const T (&a)[3][32], int b) {
   return {a[0][b], a[1][b], a[2][b]};
-}
-
-// ---------------------------------------------------------------------------
-// Block-tree matrix-vector product y = H v (BlockSparseSym::apply,
-// block_sparse.cpp:233-251) for the segment.
-// ---------------------------------------------------------------------------
-template <class T, int W>
-struct Tree {
-  unsigned mask;
-  int lane, base, b, par_src;
-  bool has_off;
-  uint32_t cmask;
-  T* hoff;  // smem [36][32]
-  T* scat;  // smem [28][32]
-  // rank-1 terms applied on top of the stored blocks
-  T lim_s;        // -sum of active limit weights (angular block -s a a^T)
-  v3<T> lim_a;
-  bool quirk;     // H(p,c) misses anchor row 0 (reference aliasing quirk)
-  T q_d0;
-  T q_ja[6], q_jb[6];
-
-  __device__ __forceinline__ void apply(const T (&H)[21], const T (&v)[6], T (&y)[6]) const {
-#pragma unroll
-    for (int r = 0; r < 6; ++r) {
-      T s = T(0);
-#pragma unroll
-      for (int c = 0; c < 6; ++c) s += H[sidx(r, c)] * v[c];
-      y[r] = s;
-    }
-    T vp[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) vp[k] = __shfl_sync(mask, v[k], par_src, W);
-    T t[6] = {0, 0, 0, 0, 0, 0};
-    if (has_off) {
-#pragma unroll
-      for (int r = 0; r < 6; ++r) {
-        T s = T(0);
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const T h = hoff[(r * 6 + c) * 32 + lane];
-          s += h * vp[c];
-          t[c] += h * v[r];
-        }
-        y[r] += s;
-      }
-      if (lim_s != T(0)) {
-        const T ap = lim_a.x * vp[3] + lim_a.y * vp[4] + lim_a.z * vp[5];
-        const T ac = lim_a.x * v[3] + lim_a.y * v[4] + lim_a.z * v[5];
-        y[3] += lim_s * lim_a.x * ap;
-        y[4] += lim_s * lim_a.y * ap;
-        y[5] += lim_s * lim_a.z * ap;
-        t[3] += lim_s * lim_a.x * ac;
-        t[4] += lim_s * lim_a.y * ac;
-        t[5] += lim_s * lim_a.z * ac;
-      }
-      if (quirk) {
-        const T s0 = q_d0 * dot6(q_jb, v);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) t[k] -= s0 * q_ja[k];
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 6; ++k) scat[k * 32 + lane] = t[k];
-    __syncwarp(mask);
-    uint32_t cm = cmask;
-    while (cm) {
-      const int c = __ffs(cm) - 1;
-      cm &= cm - 1;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) y[k] += scat[k * 32 + base + c];
-    }
-    __syncwarp(mask);
-  }
-
-  // Gather sum over children of K values into out (parent side scatter).
-  template <int K>
-  __device__ __forceinline__ void gather(const T (&v)[K], T (&out)[K]) const {
-#pragma unroll
-    for (int k = 0; k < K; ++k) scat[k * 32 + lane] = v[k];
-    __syncwarp(mask);
-#pragma unroll
-    for (int k = 0; k < K; ++k) out[k] = T(0);
-    uint32_t cm = cmask;
-    while (cm) {
-      const int c = __ffs(cm) - 1;
-      cm &= cm - 1;
-#pragma unroll
-      for (int k = 0; k < K; ++k) out[k] += scat[k * 32 + base + c];
-    }
-    __syncwarp(mask);
-  }
-};
-
-// 6x6 Cholesky of a packed SPD block (krylov.cpp:27-41); rinv = 1/diag.
-template <class T>
-__device__ __forceinline__ bool chol6(const T (&H)[21], T (&L)[21], T (&rinv)[6]) {
-  bool ok = true;
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-#pragma unroll
-    for (int j = 0; j <= i; ++j) {
-      T s = H[tri(i, j)];
-#pragma unroll
-      for (int k = 0; k < j; ++k) s -= L[tri(i, k)] * L[tri(j, k)];
-      if (i == j) {
-        ok = ok && (s > T(0));
-        const T d = sqrt(s);
-        L[tri(i, i)] = d;
-        rinv[i] = T(1) / d;
-      } else {
-        if constexpr (std::is_same<T, double>::value) L[tri(i, j)] = s / L[tri(j, j)];
-        else L[tri(i, j)] = s * rinv[j];
-      }
-    }
-  }
-  return ok;
-}
-
-// block-Jacobi apply (cholesky_solve, krylov.cpp:43-56)
-template <class T>
-__device__ __forceinline__ void psolve(bool ok, const T (&L)[21], const T (&rinv)[6], const T (&r)[6],
-                                       T (&z)[6]) {
-  if (!ok) {
-#pragma unroll
-    for (int k = 0; k < 6; ++k) z[k] = r[k];
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    T s = r[i];
-#pragma unroll
-    for (int k = 0; k < i; ++k) s -= L[tri(i, k)] * z[k];
-    if constexpr (std::is_same<T, double>::value) z[i] = s / L[tri(i, i)];
-    else z[i] = s * rinv[i];
-  }
-#pragma unroll
-  for (int i = 5; i >= 0; --i) {
-    T s = z[i];
-#pragma unroll
-    for (int k = i + 1; k < 6; ++k) s -= L[tri(k, i)] * z[k];
-    if constexpr (std::is_same<T, double>::value) z[i] = s / L[tri(i, i)];
-    else z[i] = s * rinv[i];
-  }
 }
 
 // ---------------------------------------------------------------------------

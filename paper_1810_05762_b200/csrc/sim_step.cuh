@@ -1,13 +1,16 @@
-// Fused environment-step kernel (K1 contacts + K2 solve + K3 epilogue), v2.
+// Fused environment-step kernel (K1 contacts + K2 solve + K3 epilogue).
 //
-// Execution model (DESIGN.md §Kernels): one warp segment of W lanes = one env,
-// lane b = body b.  Per-lane state that persists across the Newton loop but
-// is read only once per Newton iteration (constant part of the diagonal
-// block, constraint-row data, contacts) lives in shared memory, so the PCR
-// inner loop keeps only its vectors, the diagonal block and the explicit
-// block-Jacobi inverse in registers (occupancy: 4 blocks x 4 warps / SM).
-// Per PCR iteration there are two segment reductions (the reference's
-// ||r|| and z.Az are fused into one butterfly).
+// Execution model (DESIGN.md §4): one warp segment of W lanes = one env,
+// lane b = body b.  Per-lane data that persists across the Newton loop but is
+// read once per Newton iteration (constant part of the diagonal block and
+// rhs, H(child, parent), limit / contact rows) lives in shared memory; rarely
+// used rows (non-PD fallback, aliasing quirk, L) in a global scratch buffer.
+// The PCR is run in split block-Jacobi form: per Newton iteration each lane
+// factors its diagonal block H_bb = L L^T and forms the transformed block
+// Hh = L_b^-1 H(b, parent) L_parent^-T in registers, so a CR iteration on
+// Ahat = L^-1 H L^-T needs one 6x6 block product per lane (identity
+// diagonal blocks), a 2-round shuffle schedule for the children's terms and
+// two segment reductions.
 //
 // Instantiated per precision in sim_step_f32.cu / sim_step_f64.cu.
 #pragma once
@@ -132,70 +135,7 @@ struct Lane {
     }
   }
 
-  // y = H v over the segment's block tree (BlockSparseSym::apply,
-  // block_sparse.cpp:233-251): own diagonal block, H(b, parent) v_parent,
-  // and sum over children of H(child, b)^T v_child (+ the rank-1 limit and
-  // aliasing-quirk terms).
-  __device__ __forceinline__ void apply(const T (&H)[21], const T (&v)[6], T (&y)[6]) const {
-    T vp[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) vp[k] = __shfl_sync(mask, v[k], par_src, W);
-#pragma unroll
-    for (int r = 0; r < 6; ++r) {
-      T s = T(0);
-#pragma unroll
-      for (int c = 0; c < 6; ++c) s += H[sidx(r, c)] * v[c];
-      y[r] = s;
-    }
-    T t[6] = {0, 0, 0, 0, 0, 0};
-    if (has_off) {
-#pragma unroll
-      for (int r = 0; r < 6; ++r) {
-        T s = T(0);
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const T h = at(R_HOFF + r * 6 + c);
-          s += h * vp[c];
-          t[c] += h * v[r];
-        }
-        y[r] += s;
-      }
-      if (lim_s != T(0)) {
-        const T ap = lim_a.x * vp[3] + lim_a.y * vp[4] + lim_a.z * vp[5];
-        const T ac = lim_a.x * v[3] + lim_a.y * v[4] + lim_a.z * v[5];
-        y[3] += lim_s * lim_a.x * ap;
-        y[4] += lim_s * lim_a.y * ap;
-        y[5] += lim_s * lim_a.z * ap;
-        t[3] += lim_s * lim_a.x * ac;
-        t[4] += lim_s * lim_a.y * ac;
-        t[5] += lim_s * lim_a.z * ac;
-      }
-      if (quirk) {  // H(p,c) = H(c,p)^T - d0 ja0 jb0^T, ja0 = (-e_x, a), jb0 = (e_x, c)
-        const T d0 = at(R_QRK);
-        const T s0 = d0 * (v[0] + at(R_QRK + 4) * v[3] + at(R_QRK + 5) * v[4] + at(R_QRK + 6) * v[5]);
-        t[0] += s0;
-        t[3] -= s0 * at(R_QRK + 1);
-        t[4] -= s0 * at(R_QRK + 2);
-        t[5] -= s0 * at(R_QRK + 3);
-      }
-    }
-    // children's H(child, b)^T v_child, pulled with shuffles (no smem round trip)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (i < maxc) {  // warp-uniform bound
-        const int src = kid[i] >= 0 ? kid[i] : b;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          const T g = __shfl_sync(mask, t[k], src, W);
-          if (kid[i] >= 0) y[k] += g;
-        }
-      }
-    }
-  }
 };
-
-template <class T, int W>
-struct LaneHat;
 
 // Cholesky factor Lc (lower, packed) of an SPD 6x6 block (krylov.cpp:27-41)
 // with reciprocal diagonal rd and Mi = Lc^-1; identity when the block is not
@@ -248,92 +188,10 @@ __device__ __forceinline__ bool factor6(const T (&H)[21], T (&Lc)[21], T (&rd)[6
   return true;
 }
 
-// explicit inverse of the packed SPD 6x6 block (block-Jacobi preconditioner,
-// krylov.cpp:60-88, mathematically the reference's cholesky_solve pair);
-// identity when the block is not positive definite (krylov.cpp:76-80).
-template <class T>
-__device__ __forceinline__ void block_inverse(const T (&H)[21], T (&P)[21], bool dyn) {
-  T L[21];
-  bool ok = dyn;
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-#pragma unroll
-    for (int j = 0; j <= i; ++j) {
-      T s = H[tri(i, j)];
-#pragma unroll
-      for (int k = 0; k < j; ++k) s -= L[tri(i, k)] * L[tri(j, k)];
-      if (i == j) {
-        ok = ok && (s > T(0));
-        L[tri(i, i)] = T(1) / sqrt(s);  // store the reciprocal diagonal
-      } else {
-        L[tri(i, j)] = s * L[tri(j, j)];
-      }
-    }
-  }
-  if (!ok) {
-#pragma unroll
-    for (int k = 0; k < 21; ++k) P[k] = T(0);
-#pragma unroll
-    for (int i = 0; i < 6; ++i) P[tri(i, i)] = T(1);
-    return;
-  }
-  // M = L^-1 (lower), L has reciprocal diagonal stored
-  T M[21];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    M[tri(i, i)] = L[tri(i, i)];
-#pragma unroll
-    for (int j = 0; j < i; ++j) {
-      T s = T(0);
-#pragma unroll
-      for (int k = j; k < i; ++k) s += L[tri(i, k)] * M[tri(k, j)];
-      M[tri(i, j)] = -s * L[tri(i, i)];
-    }
-  }
-  // P = M^T M
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-#pragma unroll
-    for (int j = 0; j <= i; ++j) {
-      T s = T(0);
-#pragma unroll
-      for (int k = i; k < 6; ++k) s += M[tri(k, i)] * M[tri(k, j)];
-      P[tri(i, j)] = s;
-    }
-  }
-}
-
-template <class T>
-__device__ __forceinline__ void symv(const T (&P)[21], const T (&v)[6], T (&y)[6]) {
-#pragma unroll
-  for (int r = 0; r < 6; ++r) {
-    T s = T(0);
-#pragma unroll
-    for (int c = 0; c < 6; ++c) s += P[sidx(r, c)] * v[c];
-    y[r] = s;
-  }
-}
-
 // alpha / beta of the PCR recurrences: fp32 uses reciprocal + multiply
 // (two roundings; the f64 parity instrument keeps IEEE division).
 __device__ __forceinline__ float fdiv(float a, float b) { return __fdividef(a, b); }
 __device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
-
-#ifndef STP_PIPELINED_CR
-#define STP_PIPELINED_CR 0
-#endif
-constexpr bool kPipelinedCR = STP_PIPELINED_CR != 0;
-
-template <int W, class T>
-__device__ __forceinline__ void seg_sum4(T& a, T& b, T& c, T& d, unsigned mask) {
-#pragma unroll
-  for (int off = W / 2; off > 0; off >>= 1) {
-    a += __shfl_xor_sync(mask, a, off, W);
-    b += __shfl_xor_sync(mask, b, off, W);
-    c += __shfl_xor_sync(mask, c, off, W);
-    d += __shfl_xor_sync(mask, d, off, W);
-  }
-}
 
 template <int W, class T>
 __device__ __forceinline__ void seg_sum2(T& a, T& b, unsigned mask) {
