@@ -55,55 +55,56 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    Polls NVML every ~2 ms from a thread (nvidia-smi -lms is too coarse for a
+    sub-second region); falls back to nvidia-smi when NVML is unavailable."""
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple[float, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.err = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except (FileNotFoundError, OSError):
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.device]) if vis else self.device
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception as ex:  # reported, never fatal
+            self.err = repr(ex)
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                                     int(get_reasons(self.h))))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self.err is not None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml unavailable: {self.err}"]}
+        self._stop.set()
+        self.t.join(timeout=1)
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        reasons = sorted({k for _, r in self.samples for k, b in bits.items() if r & b})
+        mhz = [m for m, _ in self.samples]
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(mhz)}
 
 
 def cpu_reference_rate(n_envs: int, steps: int, warmup: int, threads: int, budget_s: float = 20.0):
@@ -222,6 +223,38 @@ def run_ours(args, world, rank, local):
     value = world * N_ENVS * K / (job_ms / 1e3)
     ms_per_step = job_ms / K
 
+    # ---- rollout: env_step + tcgen05 policy forward (K4) per step, device-timed
+    rollout = None
+    try:
+        from paper_1810_05762_b200.policy import HIDDEN, ActorCritic, PolicyKernel, RunningStat
+        torch.manual_seed(0)
+        model = ActorCritic(env.obs_dim, env.action_dim, HIDDEN[TASK]).to(dev)
+        kern = PolicyKernel(model, dev)
+        st = RunningStat(env.obs_dim, device=dev)
+        st.push(obs)
+        m_, s_ = st.mean.float(), st.std.float()
+        for s in range(3):
+            _, a, _, _ = kern.forward(obs, m_, s_, seed=SEED, step=s)
+            env.step(a.clamp(-1, 1), obs, rew, done)
+        torch.cuda.synchronize()
+        r0, r1, p0 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        r0.record()
+        for s in range(K):
+            _, a, _, _ = kern.forward(obs, m_, s_, seed=SEED, step=3 + s)
+            env.step(a.clamp(-1, 1), obs, rew, done)
+        r1.record()
+        for s in range(K):
+            kern.forward(obs, m_, s_, seed=SEED, step=3 + s)
+        p0.record()
+        torch.cuda.synchronize()
+        roll_ms = r0.elapsed_time(r1) / K
+        pol_ms = r1.elapsed_time(p0) / K
+        rollout = {"env_steps_per_s": N_ENVS / (roll_ms / 1e3), "ms_per_step": roll_ms,
+                   "policy_forward_ms": pol_ms, "policy": f"tcgen05 SELU MLP pi+V {HIDDEN[TASK]} bf16",
+                   "l2": "not flushed"}
+    except Exception as ex:
+        rollout = {"error": repr(ex)}
+
     # ---- e2e through the reference-facing C-ABI call with pinned host buffers
     h_act = torch.empty((N_ENVS, env.action_dim), dtype=torch.float32, pin_memory=True)
     h_obs = torch.empty((N_ENVS, env.obs_dim), dtype=torch.float32, pin_memory=True)
@@ -277,7 +310,7 @@ def run_ours(args, world, rank, local):
                            "l2": "flushed between timed steps (256 MiB write)", "auto_reset": True},
                 "e2e": {"value": e2e_value, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "path": "stp_step_host (pinned host buffers)"},
-                "gpu_launches": K, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+                "gpu_launches": K, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "rollout": rollout,
                 "wall_s_timed_region": wall, "failed_envs_last_step": failed}
         print(json.dumps(line), flush=True)
     env.close()
