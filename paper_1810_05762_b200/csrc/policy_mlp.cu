@@ -20,7 +20,8 @@
 
 namespace {
 
-constexpr int kM = 128;  // rows (envs) per CTA = UMMA M
+constexpr int kM = 128;        // rows (envs) per CTA = UMMA M
+constexpr int kThreads = 256;  // 8 warps: warps w and w+4 share TMEM lanes 32(w%4).. by column halves
 constexpr float kSeluL = 1.0507009873554805f, kSeluA = 1.6732632423543772f;
 
 struct MlpDims {
@@ -116,7 +117,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float selu(float x) { return x > 0.f ? kSeluL * x : kSeluL * kSeluA * expm1f(x); }
+// SELU with the fast exponential: the result is rounded to bf16 for the next
+// layer anyway (8 significant bits), so __expf's ~2 ulp fp32 error is invisible.
+__device__ __forceinline__ float selu(float x) { return x > 0.f ? kSeluL * x : kSeluL * kSeluA * (__expf(x) - 1.f); }
 
 // Write 8 bf16 (16 B) of row `row`, K-chunk `kc` into a [k/8][128][8] operand.
 __device__ __forceinline__ void st_chunk(__nv_bfloat16* buf, int kc, int row, const float* x8) {
@@ -137,6 +140,8 @@ struct Smem {
 __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4], __nv_bfloat16* abuf0,
                         __nv_bfloat16* abuf1, Smem* sh, uint32_t& wphase, uint32_t& mphase, int tid) {
   const int warp = tid >> 5;
+  const int row = (warp & 3) * 32 + (tid & 31);  // TMEM lane = tile row
+  const int half = warp >> 2;                    // column half of the epilogue
   // stage the 4 weight blobs (one TMA bulk copy each, one barrier)
   if (tid == 0) {
     uint32_t bytes = 0;
@@ -167,15 +172,18 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
     mphase ^= 1;
     tc_after_sync();
     if (l == 3) break;
-    // epilogue: bias + SELU -> bf16 -> next operand (this thread's row)
-    const uint32_t tbase = sh->tmem + (uint32_t(warp * 32) << 16);
-    for (int c0 = 0; c0 < D.n[l]; c0 += 16) {
+    // epilogue: bias + SELU -> bf16 -> next operand (this thread's row and column half)
+    const uint32_t tbase = sh->tmem + (uint32_t((warp & 3) * 32) << 16);
+    const int ncols = D.n[l];
+    const int c_lo = ncols >= 32 ? half * (ncols / 2) : 0;
+    const int c_hi = ncols >= 32 ? c_lo + ncols / 2 : (half == 0 ? ncols : 0);
+    for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
       float v[16];
       tmem_ld16(tbase + uint32_t(c0), v);
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = selu(v[i] + P.bias[l][c0 + i]);
-      st_chunk(a_out, c0 / 8, tid, v);
-      st_chunk(a_out, c0 / 8 + 1, tid, v + 8);
+      st_chunk(a_out, c0 / 8, row, v);
+      st_chunk(a_out, c0 / 8 + 1, row, v + 8);
     }
     tc_before_sync();
     __nv_bfloat16* t = a_in;
@@ -184,8 +192,8 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
   }
 }
 
-// K4 kernel.  dims/pointers for the policy (pi) and value (v) nets.
-__global__ void __launch_bounds__(kM, 1)
+// K4 kernel: blockIdx.x = 128-env tile, blockIdx.y = net (0 policy, 1 value).
+__global__ void __launch_bounds__(kThreads, 1)
     k_policy_mlp(const float* __restrict__ obs, int n_envs, int obs_dim, const float* __restrict__ mean,
                  const float* __restrict__ stdv, MlpDims Dpi, NetPtrs Ppi, MlpDims Dv, NetPtrs Pv,
                  const float* __restrict__ log_std, uint64_t seed, uint64_t step, long long env_offset,
@@ -200,7 +208,11 @@ __global__ void __launch_bounds__(kM, 1)
   __nv_bfloat16* wbase = base + a0_elems + a1_elems;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int row = blockIdx.x * kM + tid;
+  const bool value_net = blockIdx.y == 1;
+  const MlpDims& D = value_net ? Dv : Dpi;
+  const NetPtrs& P = value_net ? Pv : Ppi;
+  const int lrow = (warp & 3) * 32 + (tid & 31);  // TMEM lane / tile row of this thread
+  const int row = blockIdx.x * kM + lrow;
 
   if (tid == 0) {
     mbar_init(&sh->bar_w, 1);
@@ -215,77 +227,65 @@ __global__ void __launch_bounds__(kM, 1)
   __syncthreads();
   tc_after_sync();
 
-  // whitened, clipped observation row -> bf16 operand (RunningStat)
-  auto stage_obs = [&](int kpad) {
-    for (int kc = 0; kc < kpad / 8; ++kc) {
-      float x8[8];
+  // whitened, clipped observation row -> bf16 operand (RunningStat);
+  // the two thread halves split the K chunks
+  for (int kc = warp >> 2; kc < D.k[0] / 8; kc += 2) {
+    float x8[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int c = kc * 8 + i;
-        float x = 0.f;
-        if (row < n_envs && c < obs_dim) {
-          x = (obs[size_t(row) * obs_dim + c] - mean[c]) / stdv[c];
-          x = fminf(fmaxf(x, -10.f), 10.f);
-        }
-        x8[i] = x;
+    for (int i = 0; i < 8; ++i) {
+      const int c = kc * 8 + i;
+      float x = 0.f;
+      if (row < n_envs && c < obs_dim) {
+        x = (obs[size_t(row) * obs_dim + c] - mean[c]) * (1.f / stdv[c]);
+        x = fminf(fmaxf(x, -10.f), 10.f);
       }
-      st_chunk(abuf0, kc, tid, x8);
+      x8[i] = x;
     }
-  };
+    st_chunk(abuf0, kc, lrow, x8);
+  }
   __nv_bfloat16* wsm[4];
+  int off = 0;
+  for (int l = 0; l < 4; ++l) {
+    wsm[l] = wbase + off;
+    off += D.k[l] * D.n[l];
+  }
   uint32_t wphase = 0, mphase = 0;
-  const uint32_t tbase = sh->tmem + (uint32_t(warp * 32) << 16);
-
-  // ---- policy mean + Gaussian sample ------------------------
-  {
-    int off = 0;
-    for (int l = 0; l < 4; ++l) {
-      wsm[l] = wbase + off;
-      off += Dpi.k[l] * Dpi.n[l];
-    }
-    stage_obs(Dpi.k[0]);
-    run_net(Dpi, Ppi, wsm, abuf0, abuf1, sh, wphase, mphase, tid);
-    const uint64_t genv = uint64_t(env_offset + row);
-    const uint64_t s = stp_derive_seed(seed, 6 /* policy noise */, (genv << 32) | uint32_t(step));
-    float lp = 0.f;
-    for (int c0 = 0; c0 < Dpi.n[3]; c0 += 16) {
-      float v[16];
-      tmem_ld16(tbase + uint32_t(c0), v);
-      if (row < n_envs) {
-        for (int i = 0; i < 16; ++i) {
-          const int c = c0 + i;
-          if (c >= Dpi.out) break;
-          const float m = v[i] + Ppi.bias[3][c];
-          mu_out[size_t(row) * Dpi.out + c] = m;
-          if (act_out) {
-            // Box-Muller on two 24-bit counter-based uniforms
-            const float u1 = fmaxf(stp_uniformf(s, 2 * c), 1e-7f), u2 = stp_uniformf(s, 2 * c + 1);
-            const float eps = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
-            const float sd = expf(log_std[c]);
-            act_out[size_t(row) * Dpi.out + c] = m + sd * eps;
-            lp += -0.5f * eps * eps - log_std[c] - 0.91893853320467274f;
+  run_net(D, P, wsm, abuf0, abuf1, sh, wphase, mphase, tid);
+  const uint32_t tbase = sh->tmem + (uint32_t((warp & 3) * 32) << 16);
+  if (warp < 4) {  // last layer: 32 (policy) / 16 (value) columns, one warp per TMEM lane group
+    if (!value_net) {
+      // policy mean + Gaussian sample
+      const uint64_t genv = uint64_t(env_offset + row);
+      const uint64_t s = stp_derive_seed(seed, 6 /* policy noise */, (genv << 32) | uint32_t(step));
+      float lp = 0.f;
+      for (int c0 = 0; c0 < D.n[3]; c0 += 16) {
+        float v[16];
+        tmem_ld16(tbase + uint32_t(c0), v);
+        if (row < n_envs) {
+          for (int i = 0; i < 16; ++i) {
+            const int c = c0 + i;
+            if (c >= D.out) break;
+            const float m = v[i] + P.bias[3][c];
+            mu_out[size_t(row) * D.out + c] = m;
+            if (act_out) {
+              // Box-Muller on two 24-bit counter-based uniforms
+              const float u1 = fmaxf(stp_uniformf(s, 2 * c), 1e-7f), u2 = stp_uniformf(s, 2 * c + 1);
+              const float eps = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+              const float sd = expf(log_std[c]);
+              act_out[size_t(row) * D.out + c] = m + sd * eps;
+              lp += -0.5f * eps * eps - log_std[c] - 0.91893853320467274f;
+            }
           }
         }
       }
+      if (logp_out && row < n_envs) logp_out[row] = lp;
+    } else {
+      float v[16];
+      tmem_ld16(tbase, v);
+      if (row < n_envs) v_out[row] = v[0] + P.bias[3][0];
     }
-    if (logp_out && row < n_envs) logp_out[row] = lp;
-    tc_before_sync();
   }
-  // ---- value net ---------------------------------------------------------------
-  if (v_out) {
-    __syncthreads();
-    int off = 0;
-    for (int l = 0; l < 4; ++l) {
-      wsm[l] = wbase + off;
-      off += Dv.k[l] * Dv.n[l];
-    }
-    stage_obs(Dv.k[0]);
-    run_net(Dv, Pv, wsm, abuf0, abuf1, sh, wphase, mphase, tid);
-    float v[16];
-    tmem_ld16(tbase, v);
-    if (row < n_envs) v_out[row] = v[0] + Pv.bias[3][0];
-    tc_before_sync();
-  }
+  tc_before_sync();
   __syncthreads();
   if (warp == 0) {
     tc_after_sync();
@@ -356,8 +356,8 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
     if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_policy_mlp attr: ") + cudaGetErrorString(e));
     configured = smem;
   }
-  const int blocks = (n_envs + kM - 1) / kM;
-  k_policy_mlp<<<blocks, kM, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+  const dim3 grid((n_envs + kM - 1) / kM, value_out ? 2 : 1);
+  k_policy_mlp<<<grid, kThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
       obs, n_envs, obs_dim, obs_mean, obs_std, Dpi, Ppi, Dv, Pv, log_std, seed, step, env_offset, mean_out,
       action_out, logp_out, value_out, a0, a1);
   const cudaError_t e = cudaGetLastError();
