@@ -36,12 +36,13 @@ if "--lines" in sys.argv:
             hdr = row; continue
         if hdr is None or not row or not row[0]:
             continue
-        try:
+        try:  # rows whose source text holds commas/quotes (inline asm) may not split cleanly
             ln = int(row[0])
-        except ValueError:
+            ie = int(float(row[hdr.index("Instructions Executed")] or 0))
+            ws = int(float(row[hdr.index("Warp Stall Sampling (All Samples)")] or 0))
+        except (ValueError, IndexError):
             continue
-        agg[(cur, ln)] = (int(row[hdr.index("Instructions Executed")]),
-                          int(row[hdr.index("Warp Stall Sampling (All Samples)")]), row[1].strip()[:80])
+        agg[(cur, ln)] = (ie, ws, row[1].strip()[:80])
     tot = sum(v[0] for v in agg.values()) or 1
     ts = sum(v[1] for v in agg.values()) or 1
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:int(sys.argv[sys.argv.index("--lines") + 1])]:
