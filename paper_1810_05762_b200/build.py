@@ -48,6 +48,14 @@ def _compile(src: str) -> tuple[str, str]:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    stamp = os.path.join(BUILD, "flags.txt")  # objects built with other flags are stale
+    flags = " ".join(ARCH + FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        for f in os.listdir(BUILD):
+            if f.endswith(".o"):
+                os.remove(os.path.join(BUILD, f))
+        with open(stamp, "w") as fh:
+            fh.write(flags)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         results = list(ex.map(_compile, SOURCES))
     objs = [o for o, _ in results]

@@ -152,7 +152,10 @@ __device__ __forceinline__ bool factor6(const T (&H)[21], T (&Lc)[21], T (&rd)[6
       for (int k = 0; k < j; ++k) s -= Lc[tri(i, k)] * Lc[tri(j, k)];
       if (i == j) {
         ok = ok && (s > T(0));
-        const T d = sqrt(s);
+        // lanes that end on the identity fallback (no body, static body, not
+        // positive definite) take sqrt/reciprocal of 1 instead of 0 / negative /
+        // NaN: same result, and no IEEE special-case slow-path call per lane
+        const T d = sqrt(ok ? s : T(1));
         Lc[tri(i, i)] = d;
         rd[i] = T(1) / d;
       } else {
@@ -203,11 +206,15 @@ __device__ __forceinline__ void seg_sum2(T& a, T& b, unsigned mask) {
 }
 
 #ifndef STP_MINB
-#define STP_MINB 4
+#define STP_MINB 3
 #endif
+#ifndef STP_TPB
+#define STP_TPB 128
+#endif
+constexpr int kStepThreads = STP_TPB;  // threads per block (whole warps, one env segment each)
 
 template <class T, int W, int CPB>
-__global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_step(const KArgs<T> a) {
+__global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_step(const KArgs<T> a) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int e = tid / W;
   if (e >= a.n) return;  // whole segments exit together
@@ -883,56 +890,76 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
           for (int k = 0; k < 6; ++k) u[k] = T(0);
           continue;
         }
-        T Lc[21], rd[6];
+        // Order keeps the register peak low: Lc, rhs, u and H die once bhat,
+        // xhat are formed, before the parent's Mi arrives for the Hh build.
         T bh[6], xh[6];
         T lbw;
         {
           T Mi[21];
-          const bool ok = factor6(H, Lc, rd, Mi, dyn);
           {
-            // sigma_min(L)^2 >= 1 / ||L^-1||_F^2: per-lane weight of the cheap
-            // lower bound sum_b lbw_b |rhat_b|^2 <= ||r||^2 (see the PCR loop)
-            T f = T(0);
+            T Lc[21], rd[6];
+            const bool ok = factor6(H, Lc, rd, Mi, dyn);
+            {
+              // sigma_min(L)^2 >= 1 / ||L^-1||_F^2: per-lane weight of the cheap
+              // lower bound sum_b lbw_b |rhat_b|^2 <= ||r||^2 (see the PCR loop)
+              T f = T(0);
 #pragma unroll
-            for (int k = 0; k < 21; ++k) f += Mi[k] * Mi[k];
-            lbw = dyn ? T(1) / f : T(0);
-          }
+              for (int k = 0; k < 21; ++k) f += Mi[k] * Mi[k];
+              lbw = dyn ? T(1) / f : T(0);
+            }
 #pragma unroll
-          for (int k = 0; k < 21; ++k) L.g(G_LC + k) = Lc[k];
-          L.diag_h = dyn && !ok;
-          L.any_diag = __any_sync(mask, L.diag_h);
-          L.any_quirk = __any_sync(mask, L.quirk);
+            for (int k = 0; k < 21; ++k) L.g(G_LC + k) = Lc[k];
+            L.diag_h = dyn && !ok;
+            L.any_diag = __any_sync(mask, L.diag_h);
+            L.any_quirk = __any_sync(mask, L.quirk);
 #pragma unroll
-          for (int k = 0; k < 6; ++k) L.at(R_SCAT + k) = rd[k];
-          if (L.diag_h) {
+            for (int k = 0; k < 6; ++k) L.at(R_SCAT + k) = rd[k];
+            if (L.diag_h) {
 #pragma unroll
-            for (int k = 0; k < 21; ++k) L.g(G_HD + k) = H[k];
+              for (int k = 0; k < 21; ++k) L.g(G_HD + k) = H[k];
+            }
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+              T sb = T(0), sx = T(0);
+#pragma unroll
+              for (int k = 0; k <= i; ++k) sb += Mi[tri(i, k)] * rhs[k];
+#pragma unroll
+              for (int k = i; k < 6; ++k) sx += Lc[tri(k, i)] * u[k];
+              bh[i] = sb;
+              xh[i] = sx;
+            }
           }
           T Mp[21];
 #pragma unroll
           for (int k = 0; k < 21; ++k) Mp[k] = __shfl_sync(mask, Mi[k], par_src, W);
-          // Hh = Mi (H(c,p) + limit term) Mp^T
+          // Hh = Mi ((H(c,p) + limit term) Mp^T): each row k of H(c,p) is read
+          // once, turned into row k of Q = H Mp^T, and scattered into the rows
+          // i >= k of Hh (Mi lower triangular)
 #pragma unroll
-          for (int i = 0; i < 6; ++i) {
-            T g[6] = {0, 0, 0, 0, 0, 0};
-            if (L.has_off) {
+          for (int k = 0; k < 36; ++k) L.Hh[k] = T(0);
+          if (L.has_off) {
 #pragma unroll
-              for (int k = 0; k <= i; ++k) {
+            for (int k = 0; k < 6; ++k) {
+              T h[6];
+#pragma unroll
+              for (int c = 0; c < 6; ++c) {
+                h[c] = L.at(R_HOFF + k * 6 + c);
+                if (k >= 3 && c >= 3) h[c] += L.lim_s * comp(L.lim_a, k - 3) * comp(L.lim_a, c - 3);
+              }
+              T qk[6];
+#pragma unroll
+              for (int j = 0; j < 6; ++j) {
+                T sum = T(0);
+#pragma unroll
+                for (int c = 0; c <= j; ++c) sum += h[c] * Mp[tri(j, c)];
+                qk[j] = sum;
+              }
+#pragma unroll
+              for (int i = k; i < 6; ++i) {
                 const T m = Mi[tri(i, k)];
 #pragma unroll
-                for (int c = 0; c < 6; ++c) {
-                  T h = L.at(R_HOFF + k * 6 + c);
-                  if (k >= 3 && c >= 3) h += L.lim_s * comp(L.lim_a, k - 3) * comp(L.lim_a, c - 3);
-                  g[c] += m * h;
-                }
+                for (int j = 0; j < 6; ++j) L.Hh[i * 6 + j] += m * qk[j];
               }
-            }
-#pragma unroll
-            for (int j = 0; j < 6; ++j) {
-              T sum = T(0);
-#pragma unroll
-              for (int k = 0; k <= j; ++k) sum += g[k] * Mp[tri(j, k)];
-              L.Hh[i * 6 + j] = sum;
             }
           }
           if (L.quirk) {  // transformed aliasing term: d0 (Mp ja0)(Mi jb0)^T
@@ -950,16 +977,6 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
               L.g(G_QH + 1 + i) = qa;
               L.g(G_QH + 7 + i) = qc;
             }
-          }
-#pragma unroll
-          for (int i = 0; i < 6; ++i) {
-            T sb = T(0), sx = T(0);
-#pragma unroll
-            for (int k = 0; k <= i; ++k) sb += Mi[tri(i, k)] * rhs[k];
-#pragma unroll
-            for (int k = i; k < 6; ++k) sx += Lc[tri(k, i)] * u[k];
-            bh[i] = sb;
-            xh[i] = sx;
           }
         }
         // Exit test of the reference, ||r|| > tol ||b|| (krylov.cpp:141, :154),
@@ -1313,7 +1330,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_st
 
 template <class T, int W, int CPB>
 static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
-  constexpr int threads = 128;
+  constexpr int threads = kStepThreads;
   const size_t smem = size_t(threads / 32) * smem_rows<CPB>() * 32 * sizeof(T);
   static bool configured = false;
   if (!configured) {

@@ -26,6 +26,17 @@ if len(r) >= 3:
               "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"):
         if k in names:
             print(f"  {k:60s} {vals[names.index(k)]}")
+    # warp stall reasons (cycles per issued instruction, largest first)
+    pre = "smsp__average_warps_issue_stalled_"
+    st = []
+    for i, n in enumerate(names):
+        if n.startswith(pre) and n.endswith("_per_issue_active.ratio"):
+            try:
+                st.append((float(vals[i]), n[len(pre):-len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    if st:
+        print("  stall reasons (cycles/issue): " + ", ".join(f"{n} {v:.2f}" for v, n in sorted(st, reverse=True)[:8]))
 if "--lines" in sys.argv:
     rows = list(csv.reader(io.StringIO(run("--page", "source", "--csv", "--print-source", "cuda,sass"))))
     cur = None; hdr = None; agg = {}
