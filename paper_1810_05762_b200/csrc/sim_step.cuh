@@ -15,6 +15,7 @@
 // Instantiated per precision in sim_step_f32.cu / sim_step_f64.cu.
 #pragma once
 #include <cuda_runtime.h>
+#include <type_traits>
 
 #include "sim_kernels.cuh"
 #include "sim_launch.h"
@@ -81,13 +82,16 @@ struct Lane {
   // y = Ahat v for the split-preconditioned system Ahat = L^-1 H L^-T:
   // identity diagonal blocks (the own block only when it was not positive
   // definite), Hh v_parent, and the children's Hh^T v_child.
+  // RARE = false drops the not-positive-definite and aliasing-quirk terms
+  // (caller checked any_diag / any_quirk); GR > 0 = exactly GR gather rounds.
+  template <bool RARE = true, int GR = 0>
   __device__ __forceinline__ void apply_hat(const T (&v)[6], T (&y)[6]) const {
     T vp[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) vp[k] = __shfl_sync(mask, v[k], par_src, W);
 #pragma unroll
     for (int k = 0; k < 6; ++k) y[k] = v[k];
-    if (any_diag) {  // segment-uniform: some own block was not positive definite
+    if (RARE && any_diag) {  // segment-uniform: some own block was not positive definite
       if (diag_h) {
 #pragma unroll
         for (int r = 0; r < 6; ++r) {
@@ -110,7 +114,7 @@ struct Lane {
       }
       y[r] += s;
     }
-    if (any_quirk) {  // segment-uniform; Ahat(p,c) = Hh^T - d0 qa qc^T
+    if (RARE && any_quirk) {  // segment-uniform; Ahat(p,c) = Hh^T - d0 qa qc^T
       if (quirk) {
         T s0 = T(0);
 #pragma unroll
@@ -122,8 +126,8 @@ struct Lane {
     }
     // children's contributions: scheduled rounds of shuffles (DevModel::gather_*)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (r < grounds) {
+    for (int r = 0; r < (GR > 0 ? GR : 4); ++r) {
+      if (GR > 0 || r < grounds) {
         const int src = int((gsrc >> (8 * r)) & 0xffu);
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
@@ -998,44 +1002,57 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
           }
           return seg_sum<W>(s0, mask);
         };
-        T rh[6], ar[6], ph[6], ap[6];
-        L.apply_hat(xh, ar);
+        // The loop is instantiated three times so the common case runs without
+        // the rare-term branches and with a compile-time gather schedule.  Exit
+        // decisions are segment-uniform by construction (reduced values) and
+        // are taken through votes so the compiler sees uniform control flow.
+        auto pcr = [&](auto rare_c, auto gr_c) -> int {
+          constexpr bool RARE = decltype(rare_c)::value;
+          constexpr int GR = decltype(gr_c)::value;
+          T rh[6], ar[6], ph[6], ap[6];
+          L.template apply_hat<RARE, GR>(xh, ar);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) rh[k] = dyn ? bh[k] - ar[k] : T(0);
-        L.apply_hat(rh, ar);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          ph[k] = rh[k];
-          ap[k] = ar[k];
-        }
-        T zaz = dot6(rh, ar), lb = lbw * dot6(rh, rh);
-        seg_sum2<W>(zaz, lb, mask);
-        bool above = lb > tol2_safe || res_exact(rh) > tol2;
-        int kk = 0;
-        while (kk < cf.kmax && above) {
-          const T denom = seg_sum<W>(dot6(ap, ap), mask);
-          if (!(denom > T(0)) || !(zaz > T(0))) break;  // breakdown (krylov.cpp:144)
-          const T alpha = fdiv(zaz, denom);
+          for (int k = 0; k < 6; ++k) rh[k] = dyn ? bh[k] - ar[k] : T(0);
+          L.template apply_hat<RARE, GR>(rh, ar);
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
-            xh[k] += alpha * ph[k];
-            rh[k] -= alpha * ap[k];
+            ph[k] = rh[k];
+            ap[k] = ar[k];
           }
-          ++kk;
-          L.apply_hat(rh, ar);  // before the exit test: one spare product at exit
-          T zn = dot6(rh, ar);
-          lb = lbw * dot6(rh, rh);
-          seg_sum2<W>(lb, zn, mask);
-          above = lb > tol2_safe || res_exact(rh) > tol2;
-          if (!above) break;
-          const T beta = fdiv(zn, zaz);
-          zaz = zn;
+          T zaz = dot6(rh, ar), lb = lbw * dot6(rh, rh);
+          seg_sum2<W>(zaz, lb, mask);
+          bool above = lb > tol2_safe || res_exact(rh) > tol2;
+          int kk = 0;
+          while (__all_sync(mask, kk < cf.kmax && above)) {
+            const T denom = seg_sum<W>(dot6(ap, ap), mask);
+            if (!__all_sync(mask, denom > T(0) && zaz > T(0))) break;  // breakdown (krylov.cpp:144)
+            const T alpha = fdiv(zaz, denom);
 #pragma unroll
-          for (int k = 0; k < 6; ++k) {
-            ph[k] = rh[k] + beta * ph[k];
-            ap[k] = ar[k] + beta * ap[k];
+            for (int k = 0; k < 6; ++k) {
+              xh[k] += alpha * ph[k];
+              rh[k] -= alpha * ap[k];
+            }
+            ++kk;
+            L.template apply_hat<RARE, GR>(rh, ar);  // before the exit test: one spare product at exit
+            T zn = dot6(rh, ar);
+            lb = lbw * dot6(rh, rh);
+            seg_sum2<W>(lb, zn, mask);
+            above = lb > tol2_safe || res_exact(rh) > tol2;
+            if (!__all_sync(mask, above)) break;
+            const T beta = fdiv(zn, zaz);
+            zaz = zn;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+              ph[k] = rh[k] + beta * ph[k];
+              ap[k] = ar[k] + beta * ap[k];
+            }
           }
-        }
+          return kk;
+        };
+        int kk;
+        if (L.any_diag || L.any_quirk) kk = pcr(std::true_type{}, std::integral_constant<int, 0>{});
+        else if (L.grounds == 2) kk = pcr(std::false_type{}, std::integral_constant<int, 2>{});
+        else kk = pcr(std::false_type{}, std::integral_constant<int, 0>{});
         // back to velocities: solve L^T u = xhat (reciprocal diagonal parked in R_SCAT)
 #pragma unroll
         for (int i = 5; i >= 0; --i) {
