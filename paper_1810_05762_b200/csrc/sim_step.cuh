@@ -106,13 +106,13 @@ struct Lane {
     T t[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
-      T s = T(0);
+      T s = y[r];
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
         s += Hh[r * 6 + c] * vp[c];
         t[c] += Hh[r * 6 + c] * v[r];
       }
-      y[r] += s;
+      y[r] = s;
     }
     if (RARE && any_quirk) {  // segment-uniform; Ahat(p,c) = Hh^T - d0 qa qc^T
       if (quirk) {
@@ -159,9 +159,15 @@ __device__ __forceinline__ bool factor6(const T (&H)[21], T (&Lc)[21], T (&rd)[6
         // lanes that end on the identity fallback (no body, static body, not
         // positive definite) take sqrt/reciprocal of 1 instead of 0 / negative /
         // NaN: same result, and no IEEE special-case slow-path call per lane
-        const T d = sqrt(ok ? s : T(1));
-        Lc[tri(i, i)] = d;
-        rd[i] = T(1) / d;
+        const T sv = ok ? s : T(1);
+        if constexpr (sizeof(T) == 4) {  // fp32: one MUFU.RSQ instead of IEEE sqrt + reciprocal
+          rd[i] = rsqrtf(sv);
+          Lc[tri(i, i)] = sv * rd[i];
+        } else {
+          const T d = sqrt(sv);
+          Lc[tri(i, i)] = d;
+          rd[i] = T(1) / d;
+        }
       } else {
         Lc[tri(i, j)] = s * rd[j];
       }
@@ -629,8 +635,6 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
       pI.xy = from<W>(Iinv.xy, par_src, mask);
       pI.xz = from<W>(Iinv.xz, par_src, mask);
       pI.yz = from<W>(Iinv.yz, par_src, mask);
-#pragma unroll
-      for (int k = 0; k < 36; ++k) L.at(R_HOFF + k) = T(0);  // H(c,p) accumulates in smem
       T up[27];  // parent-side contributions (packed diag block + rhs)
 #pragma unroll
       for (int k = 0; k < 27; ++k) up[k] = T(0);
@@ -645,6 +649,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
         const v3<T> t1 = vunit(cross(aw, ref));
         const v3<T> t2 = cross(aw, t1);
         const v3<T> err = cross(aw, bw);
+        T d5[5] = {0, 0, 0, 0, 0};  // row weights (0 = row skipped)
 #pragma unroll
         for (int rr = 0; rr < 5; ++rr) {
           T ja[6], jb[6];
@@ -672,6 +677,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
           }
           const T d = cf.kj * (wsum > T(1e-12) ? T(1) / wsum : T(0));  // effective_mass, :69-80
           if (!(d > T(0))) continue;  // assemble skips reg <= 0 (solver.cpp:331)
+          d5[rr] = d;
           sym_add(Hown, jb, d);
           const T db = d * bias;
 #pragma unroll
@@ -683,9 +689,6 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
 #pragma unroll
               for (int c = 0; c <= r; ++c) up[tri(r, c)] += dj * ja[c];
               up[21 + r] += ja[r] * db;
-              const T djb = d * jb[r];
-#pragma unroll
-              for (int c = 0; c < 6; ++c) L.at(R_HOFF + r * 6 + c) += djb * ja[c];
             }
           }
           if (rr == 0 && M.quirk[b]) {  // aliasing quirk: H(p,c) misses row 0
@@ -698,6 +701,37 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
             L.at(R_QRK + 5) = jb[4];
             L.at(R_QRK + 6) = jb[5];
           }
+        }
+        // H(c,p) = sum_r d_r jb_r ja_r^T written once in closed form: the
+        // structural zeros of the anchor rows (+-e_r on the linear part) and the
+        // axis rows (angular only) are skipped, every non-zero entry is the same
+        // fma chain in row order as the row-by-row accumulation.
+        if (pdyn) {
+          v3<T> ca[3], cb[3];
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            const v3<T> ek{T(r == 0), T(r == 1), T(r == 2)};
+            ca[r] = -cross(ra, ek);
+            cb[r] = cross(rb, ek);
+          }
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              L.at(R_HOFF + i * 6 + j) = i == j ? -d5[i] : T(0);
+              L.at(R_HOFF + i * 6 + 3 + j) = d5[i] * comp(ca[i], j);
+              L.at(R_HOFF + (3 + i) * 6 + j) = -(d5[j] * comp(cb[j], i));
+              T acc = T(0);
+#pragma unroll
+              for (int r = 0; r < 3; ++r) acc += (d5[r] * comp(cb[r], i)) * comp(ca[r], j);
+              acc += (d5[3] * comp(t1, i)) * -comp(t1, j);
+              acc += (d5[4] * comp(t2, i)) * -comp(t2, j);
+              L.at(R_HOFF + (3 + i) * 6 + 3 + j) = acc;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 36; ++k) L.at(R_HOFF + k) = T(0);
         }
         // speculative limits (solver.cpp:144-173): angular rows along the child axis
         const qt<T> rest{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]};
@@ -723,6 +757,9 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
           lim[4] = cf.kl * meff;
           lim[6] = uni_bias(hi_gap, cf.beta, cf.dt);
         }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 36; ++k) L.at(R_HOFF + k) = T(0);
       }
 #pragma unroll
       for (int k = 0; k < 7; ++k) L.at(R_LIM + k) = lim[k];
@@ -1033,7 +1070,10 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
               rh[k] -= alpha * ap[k];
             }
             ++kk;
-            L.template apply_hat<RARE, GR>(rh, ar);  // before the exit test: one spare product at exit
+            // at the iteration cap the exit is certain: the product, the norms
+            // and the exit test of this point cannot change xhat
+            if (kk >= cf.kmax) break;
+            L.template apply_hat<RARE, GR>(rh, ar);
             T zn = dot6(rh, ar);
             lb = lbw * dot6(rh, rh);
             seg_sum2<W>(lb, zn, mask);
@@ -1160,7 +1200,10 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
   }
 
   // ---------------- K3: task epilogue (env_step) ---------
+  bool reuse_angles = false, reuse_head = false;
+  T yaw_r = T(0), head_r = T(0), ang_r = T(0);
   if (a.mode == 1) {
+    const T tx_r = tx, ty_r = ty;
     const int R = M.root;
     const T prev_rx = a.state[size_t(e) * kStateFields * W + 0 * W + R];
     const T prev_ry = a.state[size_t(e) * kStateFields * W + 1 * W + R];
@@ -1170,6 +1213,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
     const unsigned fb = __ballot_sync(mask, act && nc > 0 && ((M.feet_mask >> b) & 1)) >> base;
     T rew = T(0);
     const qt<T> qpn = from<W>(q, par_src, mask);
+    // angles the observation can reuse when the env is not reset (same inputs)
     if (!step_failed) {
       // compute_reward
       const T ox_ = tx - prev_rx, oy_ = ty - prev_ry;
@@ -1177,7 +1221,9 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
       T S = T(0);
       if (od0 > T(0)) S = ((xr.x - prev_rx) * ox_ + (xr.y - prev_ry) * oy_) / od0 / cf.dt;
       const T yaw = atan2(T(2) * (qr.w * qr.z + qr.x * qr.y), T(1) - T(2) * (qr.y * qr.y + qr.z * qr.z));
-      const T cth = cos(atan2(ty - xr.y, tx - xr.x) - yaw);
+      yaw_r = yaw;
+      head_r = atan2(ty - xr.y, tx - xr.x);
+      const T cth = cos(head_r - yaw);
       const T rhead = cth > T(0.8) ? T(1) : cth / T(0.8);
       const T cvert = T(1) - T(2) * (qr.x * qr.x + qr.y * qr.y);
       const T rstand = cvert > T(0.93) ? T(1) : T(0);
@@ -1188,6 +1234,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
         uc = uu * uu;
         const T ang = hinge_angle(qpn, q, qt<T>{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]},
                                   ldv(M.ax_c, b));
+        ang_r = ang;
         nl = (ang - M.lim_lo[b] < cf.lim_act || M.lim_hi[b] - ang < cf.lim_act) ? T(1) : T(0);
       }
       seg_sum2<W>(tc, uc, mask);
@@ -1228,6 +1275,8 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
     ltau = jnt >= 0 ? min(max(T(act_u), T(-1)), T(1)) : T(0);
     feet_bits = fb;
     do_reset = dn && a.task.auto_reset;
+    reuse_angles = !step_failed && !do_reset;
+    reuse_head = reuse_angles && tx == tx_r && ty == ty_r;
     if (b == 0) {
       if (a.reward) a.reward[e] = float(rew);
       if (a.done) a.done[e] = dn ? 1 : 0;
@@ -1249,7 +1298,9 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
       const qt<T> qr2 = from<W>(q, R, mask);
       const v3<T> vr2 = from<W>(v, R, mask);
       const v3<T> wr2 = from<W>(w, R, mask);
-      const T yaw = atan2(T(2) * (qr2.w * qr2.z + qr2.x * qr2.y), T(1) - T(2) * (qr2.y * qr2.y + qr2.z * qr2.z));
+      const T yaw = reuse_angles ? yaw_r
+                                 : atan2(T(2) * (qr2.w * qr2.z + qr2.x * qr2.y),
+                                         T(1) - T(2) * (qr2.y * qr2.y + qr2.z * qr2.z));
       T sy, cy;
       sincos_(yaw, &sy, &cy);
       if (b == 0) {
@@ -1265,7 +1316,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
         o[7] = float(-sy * wr2.x + cy * wr2.y);
         o[8] = float(wr2.z);
         T sh, ch;
-        sincos_(atan2(ty - xr2.y, tx - xr2.x) - yaw, &sh, &ch);
+        sincos_((reuse_head ? head_r : atan2(ty - xr2.y, tx - xr2.x)) - yaw, &sh, &ch);
         o[9] = float(sh);
         o[10] = float(ch);
         for (int f = 0; f < M.n_feet; ++f) o[11 + 3 * J + f] = ((feet_bits >> M.feet[f]) & 1) ? 1.f : 0.f;
@@ -1274,7 +1325,9 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
       const v3<T> wpo = from<W>(w, par_src, mask);
       if (jnt >= 0) {
         const v3<T> axc = ldv(M.ax_c, b);
-        const T ang = hinge_angle(qpo, q, qt<T>{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]}, axc);
+        const T ang = reuse_angles
+                          ? ang_r
+                          : hinge_angle(qpo, q, qt<T>{M.rest[0][b], M.rest[1][b], M.rest[2][b], M.rest[3][b]}, axc);
         const T rate = dot(qrot(q, axc), w - wpo);  // joint_velocity, solver.cpp:413-417
         o[11 + jnt] = float(ang);
         o[11 + J + jnt] = float(rate);
