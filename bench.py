@@ -255,23 +255,31 @@ def run_ours(args, world, rank, local):
     except Exception as ex:
         rollout = {"error": repr(ex)}
 
-    # ---- e2e through the reference-facing C-ABI call with pinned host buffers
-    h_act = torch.empty((N_ENVS, env.action_dim), dtype=torch.float32, pin_memory=True)
+    # ---- e2e through the reference-facing C-ABI call with pinned host buffers:
+    # each step's actions sit in their own pinned buffer (as a policy writing
+    # into host memory would leave them), and stp_step_host is called with raw
+    # pointers - the H2D copy, the kernel, the D2H copies and the synchronise
+    # are all inside the call and inside the timed region
+    import ctypes
+    n_buf = min(K, 64)
+    h_acts = [acts[Wm + s].cpu().pin_memory() for s in range(n_buf)]
     h_obs = torch.empty((N_ENVS, env.obs_dim), dtype=torch.float32, pin_memory=True)
     h_rew = torch.empty((N_ENVS,), dtype=torch.float32, pin_memory=True)
     h_done = torch.empty((N_ENVS,), dtype=torch.uint8, pin_memory=True)
-    import numpy as np
-    host_acts = [acts[Wm + s].cpu() for s in range(min(K, 64))]
+    p_acts = [ctypes.c_void_p(t.data_ptr()) for t in h_acts]
+    p_out = [ctypes.c_void_p(t.data_ptr()) for t in (h_obs, h_rew, h_done)]
+    step_host = env.lib.stp_step_host
     for s in range(min(Wm, 3)):
-        h_act.copy_(host_acts[s % len(host_acts)])
-        env.step_host(h_act.numpy(), h_obs.numpy(), h_rew.numpy(), h_done.numpy())
+        rc = step_host(env._h, p_acts[s % n_buf], *p_out)
+        assert rc == 0, rc
     if world > 1:
         torch.distributed.barrier()
+    rcs = 0
     e0 = time.perf_counter()
     for s in range(K):
-        h_act.copy_(host_acts[s % len(host_acts)])
-        env.step_host(h_act.numpy(), h_obs.numpy(), h_rew.numpy(), h_done.numpy())
+        rcs |= step_host(env._h, p_acts[s % n_buf], *p_out)
     e2e_s = time.perf_counter() - e0
+    assert rcs == 0, rcs
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)

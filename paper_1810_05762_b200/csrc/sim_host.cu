@@ -61,6 +61,14 @@ struct stp_sim {
   float* d_obs = nullptr;
   float* d_rew = nullptr;
   uint8_t* d_done = nullptr;
+  // host-buffer pipelining: env chunks on their own streams so one chunk's
+  // copies overlap the other chunks' kernels (created on first use)
+#ifndef STP_HOST_CHUNKS
+#define STP_HOST_CHUNKS 4
+#endif
+  static constexpr int kChunks = STP_HOST_CHUNKS;
+  cudaStream_t cs[kChunks] = {};
+  cudaEvent_t ev_in = nullptr, ev_out[kChunks] = {};
   std::vector<void*> allocations;
 };
 
@@ -345,10 +353,12 @@ stp::KArgs<T> make_args(stp_sim* s, int mode) {
 }
 
 int launch(stp_sim* s, int mode, const float* torques, const float* actions, float* obs, float* reward,
-           uint8_t* done, const uint8_t* mask, cudaStream_t st) {
+           uint8_t* done, const uint8_t* mask, cudaStream_t st, int e_begin = 0, int e_end = -1) {
   cudaError_t e;
   if (s->precision == STP_PRECISION_F64) {
     auto a = make_args<double>(s, mode);
+    a.e_begin = e_begin;
+    if (e_end >= 0) a.n = e_end;
     a.torques = torques;
     a.actions = actions;
     a.obs = obs;
@@ -358,6 +368,8 @@ int launch(stp_sim* s, int mode, const float* torques, const float* actions, flo
     e = stp::launch_env_step<double>(a, s->W, s->cpb, st);
   } else {
     auto a = make_args<float>(s, mode);
+    a.e_begin = e_begin;
+    if (e_end >= 0) a.n = e_end;
     a.torques = torques;
     a.actions = actions;
     a.obs = obs;
@@ -507,6 +519,14 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
 void stp_destroy(stp_sim* s) {
   if (!s) return;
   if (s->stream) cudaStreamSynchronize(s->stream);
+  for (int c = 0; c < stp_sim::kChunks; ++c) {
+    if (s->cs[c]) {
+      cudaStreamSynchronize(s->cs[c]);
+      cudaStreamDestroy(s->cs[c]);
+    }
+    if (s->ev_out[c]) cudaEventDestroy(s->ev_out[c]);
+  }
+  if (s->ev_in) cudaEventDestroy(s->ev_in);
   for (void* p : s->allocations) cudaFree(p);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -630,16 +650,55 @@ int stp_step(stp_sim* s, const float* actions, float* obs, float* reward, uint8_
   return launch(s, 1, nullptr, actions, obs, reward, done, nullptr, pick(s, stream));
 }
 
+#ifndef STP_HOST_MIN_CHUNK
+#define STP_HOST_MIN_CHUNK 1024
+#endif
+constexpr size_t kMinChunk = STP_HOST_MIN_CHUNK;
+
 int stp_step_host(stp_sim* s, const float* actions, float* obs, float* reward, uint8_t* done) {
   if (!s || (s->J > 0 && !actions)) return fail(STP_EINVAL, "stp_step_host: bad arguments");
   const size_t N = size_t(s->n);
-  CK(cudaMemcpyAsync(s->d_act, actions, N * s->J * sizeof(float), cudaMemcpyHostToDevice, s->stream));
-  int rc = launch(s, 1, nullptr, s->d_act, obs ? s->d_obs : nullptr, reward ? s->d_rew : nullptr,
-                  done ? s->d_done : nullptr, nullptr, s->stream);
-  if (rc) return rc;
-  if (obs) CK(cudaMemcpyAsync(obs, s->d_obs, N * s->obs_dim * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
-  if (reward) CK(cudaMemcpyAsync(reward, s->d_rew, N * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
-  if (done) CK(cudaMemcpyAsync(done, s->d_done, N, cudaMemcpyDeviceToHost, s->stream));
+  // up to 4 chunks of >= 1024 envs (measured on B200 at 4096 envs: 4 chunks
+  // 0.234 ms, 8 chunks 0.243 ms, one launch 0.259 ms per call)
+  const int C = int(std::min<size_t>(stp_sim::kChunks, std::max<size_t>(1, N / kMinChunk)));
+  if (C == 1) {
+    CK(cudaMemcpyAsync(s->d_act, actions, N * s->J * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+    int rc = launch(s, 1, nullptr, s->d_act, obs ? s->d_obs : nullptr, reward ? s->d_rew : nullptr,
+                    done ? s->d_done : nullptr, nullptr, s->stream);
+    if (rc) return rc;
+    if (obs) CK(cudaMemcpyAsync(obs, s->d_obs, N * s->obs_dim * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+    if (reward) CK(cudaMemcpyAsync(reward, s->d_rew, N * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+    if (done) CK(cudaMemcpyAsync(done, s->d_done, N, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return STP_OK;
+  }
+  if (!s->ev_in) {
+    CK(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
+    for (int c = 0; c < stp_sim::kChunks; ++c) {
+      CK(cudaStreamCreateWithFlags(&s->cs[c], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&s->ev_out[c], cudaEventDisableTiming));
+    }
+  }
+  // every chunk starts after the work already queued on the handle's stream
+  CK(cudaEventRecord(s->ev_in, s->stream));
+  const size_t O = size_t(s->obs_dim), J = size_t(s->J);
+  const bool loads = s->loads_pending;  // pending external loads apply to every chunk
+  for (int c = 0; c < C; ++c) {
+    const size_t e0 = N * c / C, e1 = N * (c + 1) / C, n = e1 - e0;
+    cudaStream_t st = s->cs[c];
+    s->loads_pending = loads;
+    CK(cudaStreamWaitEvent(st, s->ev_in, 0));
+    if (J) CK(cudaMemcpyAsync(s->d_act + e0 * J, actions + e0 * J, n * J * sizeof(float), cudaMemcpyHostToDevice, st));
+    int rc = launch(s, 1, nullptr, s->d_act, obs ? s->d_obs : nullptr, reward ? s->d_rew : nullptr,
+                    done ? s->d_done : nullptr, nullptr, st, int(e0), int(e1));
+    if (rc) return rc;
+    if (obs) CK(cudaMemcpyAsync(obs + e0 * O, s->d_obs + e0 * O, n * O * sizeof(float), cudaMemcpyDeviceToHost, st));
+    if (reward) CK(cudaMemcpyAsync(reward + e0, s->d_rew + e0, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+    if (done) CK(cudaMemcpyAsync(done + e0, s->d_done + e0, n, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(s->ev_out[c], st));
+  }
+  // later work on the handle's stream is ordered after every chunk
+  for (int c = 0; c < C; ++c) CK(cudaStreamWaitEvent(s->stream, s->ev_out[c], 0));
   CK(cudaStreamSynchronize(s->stream));
   return STP_OK;
 }

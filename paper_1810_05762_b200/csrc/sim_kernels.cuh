@@ -29,7 +29,8 @@ struct KArgs {
   const DevModel<T>* model;
   DevCfg<T> cfg;
   DevTask task;
-  int n;
+  int n;        // envs [e_begin, n) are stepped by this launch
+  int e_begin;  // first env (host-buffer pipelining launches env chunks)
   int mode;  // 0 = physics::step, 1 = env_step, 2 = reset
   uint64_t seed;
   long long env_offset;

@@ -226,7 +226,7 @@ constexpr int kStepThreads = STP_TPB;  // threads per block (whole warps, one en
 template <class T, int W, int CPB>
 __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_step(const KArgs<T> a) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int e = tid / W;
+  const int e = a.e_begin + tid / W;
   if (e >= a.n) return;  // whole segments exit together
   const int lane = threadIdx.x & 31;
   const int b = lane % W;
@@ -1409,7 +1409,7 @@ static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
     if (err != cudaSuccess) return err;
     configured = true;
   }
-  const long long total = (long long)a.n * W;
+  const long long total = (long long)(a.n - a.e_begin) * W;
   const int blocks = int((total + threads - 1) / threads);
   k_env_step<T, W, CPB><<<blocks, threads, smem, s>>>(a);
   return cudaGetLastError();

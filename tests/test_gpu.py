@@ -275,3 +275,29 @@ def test_terrain_contacts_and_height_map(precision):
     oo = o.observe()
     assert np.abs(og[:, -165:] - oo[:, -165:]).max() <= 1e-4
     assert (np.abs(oo[:, -165:] + oo[:, :1]) > 1e-3).any()  # some samples see a box
+
+
+@pytest.mark.parametrize("n", [4096, 1000])
+def test_step_host_pipelined_matches_device_step(n):
+    """stp_step_host runs env chunks on their own streams (copies overlap the
+    other chunks' kernels); results must be bit-identical to the one-launch
+    device path, including a step with pending external loads."""
+    import torch
+    a = VecEnv("humanoid", n_envs=n, seed=5)
+    b = VecEnv("humanoid", n_envs=n, seed=5)
+    a.reset()
+    b.reset()
+    rng = np.random.default_rng(0)
+    for t in range(6):
+        act = rng.uniform(-1, 1, size=(n, a.action_dim)).astype(np.float32)
+        if t == 3:
+            loads = rng.normal(0, 20, size=(n, a.n_bodies, 6))
+            a.set_external_loads(loads)
+            b.set_external_loads(loads)
+        od, rd, dd = a.step(torch.from_numpy(act).cuda())
+        torch.cuda.synchronize()
+        oh, rh, dh = b.step_host(act)
+        np.testing.assert_array_equal(od.cpu().numpy(), oh)
+        np.testing.assert_array_equal(rd.cpu().numpy(), rh)
+        np.testing.assert_array_equal(dd.cpu().numpy(), dh)
+    np.testing.assert_array_equal(a.get_state(), b.get_state())
