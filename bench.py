@@ -46,6 +46,19 @@ F_PCR_SOLVE16 = 179_114.0
 F_PCR_ITER = F_PCR_SOLVE16 / 16.0
 
 
+def _traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed `ncu --set full` capture (profiles/traffic.json, written by
+    tools/ncu_traffic.py); null when no capture is recorded."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)[kernel]
+        return {"bytes_per_launch": t["dram_read_bytes"] + t["dram_write_bytes"],
+                "read": t["dram_read_bytes"], "write": t["dram_write_bytes"], "source": t["capture"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -293,7 +306,7 @@ def run_ours(args, world, rank, local):
     f_env = F_ENV_STEP - F_PCR_ITER * (64.0 - kry_mean)  # live Krylov count
     achieved = N_ENVS * f_env / (ms_per_step / 1e3) / 1e12
     roof = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": achieved / fp32_peak, "traffic": None,
+            "frac": achieved / fp32_peak, "traffic": _traffic("k_env_step<float,32,2>"),
             "kernel": "k_env_step<float,32,2>",
             "flop_per_env_step": f_env, "krylov_iters_per_env_step": kry_mean,
             "peak_source": f"148 SM x 128 FP32 lanes x 2 x sm_max_mhz {sm_max:.0f} ({src})",
