@@ -139,7 +139,90 @@ struct Lane {
     }
   }
 
+  // fp32 form of apply_hat on packed pairs (v = (v0,v1),(v2,v3),(v4,v5)):
+  // FFMA2/FMUL2 do two lanes' worth of FP32 work per issue slot (B200: same
+  // 4.4-cycle latency and 128 FMA/clk/SM pipe rate as FFMA).  Hp[3c + rp] =
+  // (Hh[2rp][c], Hh[2rp+1][c]): Hh v_parent accumulates row pairs against the
+  // broadcast v_parent[c] in the same order as the scalar form; Hh^T v is
+  // formed per column as even/odd row partial sums plus one add.
+  template <bool RARE, int GR>
+  __device__ __forceinline__ void apply_hat_p(const float2 (&v)[3], float2 (&y)[3], const float2 (&Hp)[18]) const {
+    float vp[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      vp[2 * k] = __shfl_sync(mask, v[k].x, par_src, W);
+      vp[2 * k + 1] = __shfl_sync(mask, v[k].y, par_src, W);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) y[k] = v[k];
+    if (RARE && any_diag) {
+      if (diag_h) {
+        const float vs[6] = {v[0].x, v[0].y, v[1].x, v[1].y, v[2].x, v[2].y};
+        float ys[6];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+          float s = 0.f;
+#pragma unroll
+          for (int c = 0; c < 6; ++c) s += float(g(G_HD + sidx(r, c))) * vs[c];
+          ys[r] = s;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) y[k] = make_float2(ys[2 * k], ys[2 * k + 1]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+#pragma unroll
+      for (int rp = 0; rp < 3; ++rp) y[rp] = __ffma2_rn(Hp[3 * c + rp], make_float2(vp[c], vp[c]), y[rp]);
+    }
+    float t[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      float2 acc = __fmul2_rn(Hp[3 * c], v[0]);
+      acc = __ffma2_rn(Hp[3 * c + 1], v[1], acc);
+      acc = __ffma2_rn(Hp[3 * c + 2], v[2], acc);
+      t[c] = acc.x + acc.y;
+    }
+    if (RARE && any_quirk) {
+      if (quirk) {
+        const float vs[6] = {v[0].x, v[0].y, v[1].x, v[1].y, v[2].x, v[2].y};
+        float s0 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s0 += float(g(G_QH + 7 + k)) * vs[k];
+        s0 *= float(g(G_QH));
+#pragma unroll
+        for (int k = 0; k < 6; ++k) t[k] -= s0 * float(g(G_QH + 1 + k));
+      }
+    }
+    float2 tp[3] = {make_float2(t[0], t[1]), make_float2(t[2], t[3]), make_float2(t[4], t[5])};
+#pragma unroll
+    for (int r = 0; r < (GR > 0 ? GR : 4); ++r) {
+      if (GR > 0 || r < grounds) {
+        const int src = int((gsrc >> (8 * r)) & 0xffu);
+        float2 gp[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          gp[k].x = __shfl_sync(mask, tp[k].x, src, W);
+          gp[k].y = __shfl_sync(mask, tp[k].y, src, W);
+        }
+        const float wy = float(gwy[r]), wt = float(gwt[r]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) y[k] = __ffma2_rn(gp[k], make_float2(wy, wy), y[k]);
+        if (ghas_t[r]) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) tp[k] = __ffma2_rn(gp[k], make_float2(wt, wt), tp[k]);
+        }
+      }
+    }
+  }
 };
+
+__device__ __forceinline__ float dot6p(const float2 (&a)[3], const float2 (&b)[3]) {
+  float2 p = __fmul2_rn(a[0], b[0]);
+  p = __ffma2_rn(a[1], b[1], p);
+  p = __ffma2_rn(a[2], b[2], p);
+  return p.x + p.y;
+}
 
 // Cholesky factor Lc (lower, packed) of an SPD 6x6 block (krylov.cpp:27-41)
 // with reciprocal diagonal rd and Mi = Lc^-1; identity when the block is not
@@ -205,6 +288,36 @@ __device__ __forceinline__ bool factor6(const T (&H)[21], T (&Lc)[21], T (&rd)[6
 // (two roundings; the f64 parity instrument keeps IEEE division).
 __device__ __forceinline__ float fdiv(float a, float b) { return __fdividef(a, b); }
 __device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
+
+template <int W, class T>
+__device__ __forceinline__ void seg_sum4(T& a, T& b, T& c, T& d, unsigned mask) {
+#pragma unroll
+  for (int off = W / 2; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(mask, a, off, W);
+    b += __shfl_xor_sync(mask, b, off, W);
+    c += __shfl_xor_sync(mask, c, off, W);
+    d += __shfl_xor_sync(mask, d, off, W);
+  }
+}
+
+template <int W, class T>
+__device__ __forceinline__ void seg_sum3(T& a, T& b, T& c, unsigned mask) {
+#pragma unroll
+  for (int off = W / 2; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(mask, a, off, W);
+    b += __shfl_xor_sync(mask, b, off, W);
+    c += __shfl_xor_sync(mask, c, off, W);
+  }
+}
+
+#ifndef STP_PACKED_PCR
+#define STP_PACKED_PCR 1
+#endif
+constexpr bool kPackedPCR = STP_PACKED_PCR != 0;
+
+#ifndef STP_ONE_REDUCTION
+#define STP_ONE_REDUCTION 1
+#endif
 
 template <int W, class T>
 __device__ __forceinline__ void seg_sum2(T& a, T& b, unsigned mask) {
@@ -1046,6 +1159,75 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
         auto pcr = [&](auto rare_c, auto gr_c) -> int {
           constexpr bool RARE = decltype(rare_c)::value;
           constexpr int GR = decltype(gr_c)::value;
+          if constexpr (sizeof(T) == 4 && kPackedPCR) {
+            // fp32: the loop on packed pairs (see Lane::apply_hat_p)
+            float2 Hp[18];
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+#pragma unroll
+              for (int rp = 0; rp < 3; ++rp) Hp[3 * c + rp] = make_float2(L.Hh[(2 * rp) * 6 + c], L.Hh[(2 * rp + 1) * 6 + c]);
+            }
+            float2 x2[3], rh[3], ar[3], ph[3], ap[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) x2[k] = make_float2(xh[2 * k], xh[2 * k + 1]);
+            L.template apply_hat_p<RARE, GR>(x2, ar, Hp);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              rh[k] = dyn ? make_float2(bh[2 * k] - ar[k].x, bh[2 * k + 1] - ar[k].y) : make_float2(0.f, 0.f);
+            }
+            L.template apply_hat_p<RARE, GR>(rh, ar, Hp);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              ph[k] = rh[k];
+              ap[k] = ar[k];
+            }
+            auto res_exact_p = [&]() {
+              const T r6[6] = {rh[0].x, rh[0].y, rh[1].x, rh[1].y, rh[2].x, rh[2].y};
+              return res_exact(r6);
+            };
+            T zaz = dot6p(rh, ar), lb = lbw * dot6p(rh, rh), denom = dot6p(ar, ar);
+            seg_sum3<W>(zaz, lb, denom, mask);
+            int kk = 0;
+            bool above = lb > tol2_safe || res_exact_p() > tol2;
+            while (__all_sync(mask, kk < cf.kmax && above)) {
+              if (!__all_sync(mask, denom > T(0) && zaz > T(0))) break;  // breakdown (krylov.cpp:144)
+              const float alpha = fdiv(zaz, denom);
+#pragma unroll
+              for (int k = 0; k < 3; ++k) {
+                x2[k] = __ffma2_rn(ph[k], make_float2(alpha, alpha), x2[k]);
+                rh[k] = __ffma2_rn(ap[k], make_float2(-alpha, -alpha), rh[k]);
+              }
+              ++kk;
+              if (kk >= cf.kmax) break;  // exit certain: the rest cannot change xhat
+              L.template apply_hat_p<RARE, GR>(rh, ar, Hp);
+              // one reduction per trip: (lb, zn) and (aa, ax) as two pairs
+              float2 q0 = make_float2(lbw * dot6p(rh, rh), dot6p(rh, ar));
+              float2 q1 = make_float2(dot6p(ar, ar), dot6p(ar, ap));
+#pragma unroll
+              for (int off = W / 2; off > 0; off >>= 1) {
+                q0 = __fadd2_rn(q0, make_float2(__shfl_xor_sync(mask, q0.x, off, W), __shfl_xor_sync(mask, q0.y, off, W)));
+                q1 = __fadd2_rn(q1, make_float2(__shfl_xor_sync(mask, q1.x, off, W), __shfl_xor_sync(mask, q1.y, off, W)));
+              }
+              lb = q0.x;
+              const float zn = q0.y, aa = q1.x, ax = q1.y;
+              above = lb > tol2_safe || res_exact_p() > tol2;
+              if (!__all_sync(mask, above)) break;
+              const float beta = fdiv(zn, zaz);
+              zaz = zn;
+              denom = aa + beta * (2.f * ax + beta * denom);
+#pragma unroll
+              for (int k = 0; k < 3; ++k) {
+                ph[k] = __ffma2_rn(ph[k], make_float2(beta, beta), rh[k]);
+                ap[k] = __ffma2_rn(ap[k], make_float2(beta, beta), ar[k]);
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              xh[2 * k] = x2[k].x;
+              xh[2 * k + 1] = x2[k].y;
+            }
+            return kk;
+          } else {
           T rh[6], ar[6], ph[6], ap[6];
           L.template apply_hat<RARE, GR>(xh, ar);
 #pragma unroll
@@ -1057,9 +1239,45 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
             ap[k] = ar[k];
           }
           T zaz = dot6(rh, ar), lb = lbw * dot6(rh, rh);
+          int kk = 0;
+#if STP_ONE_REDUCTION
+          // One reduction per trip: |Ahat p|^2 of the next trip follows from
+          // |Ahat r|^2, Ahat r . Ahat p and |Ahat p|^2 of this one
+          // (Ahat p' = Ahat r + beta Ahat p); ap itself is still updated
+          // explicitly, only its norm is formed by the expansion.
+          T denom = dot6(ar, ar);
+          seg_sum3<W>(zaz, lb, denom, mask);
+          bool above = lb > tol2_safe || res_exact(rh) > tol2;
+          while (__all_sync(mask, kk < cf.kmax && above)) {
+            if (!__all_sync(mask, denom > T(0) && zaz > T(0))) break;  // breakdown (krylov.cpp:144)
+            const T alpha = fdiv(zaz, denom);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+              xh[k] += alpha * ph[k];
+              rh[k] -= alpha * ap[k];
+            }
+            ++kk;
+            // at the iteration cap the exit is certain: the product, the norms
+            // and the exit test of this point cannot change xhat
+            if (kk >= cf.kmax) break;
+            L.template apply_hat<RARE, GR>(rh, ar);
+            T zn = dot6(rh, ar), aa = dot6(ar, ar), ax = dot6(ar, ap);
+            lb = lbw * dot6(rh, rh);
+            seg_sum4<W>(lb, zn, aa, ax, mask);
+            above = lb > tol2_safe || res_exact(rh) > tol2;
+            if (!__all_sync(mask, above)) break;
+            const T beta = fdiv(zn, zaz);
+            zaz = zn;
+            denom = aa + beta * (T(2) * ax + beta * denom);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+              ph[k] = rh[k] + beta * ph[k];
+              ap[k] = ar[k] + beta * ap[k];
+            }
+          }
+#else
           seg_sum2<W>(zaz, lb, mask);
           bool above = lb > tol2_safe || res_exact(rh) > tol2;
-          int kk = 0;
           while (__all_sync(mask, kk < cf.kmax && above)) {
             const T denom = seg_sum<W>(dot6(ap, ap), mask);
             if (!__all_sync(mask, denom > T(0) && zaz > T(0))) break;  // breakdown (krylov.cpp:144)
@@ -1087,7 +1305,9 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
               ap[k] = ar[k] + beta * ap[k];
             }
           }
+#endif
           return kk;
+          }
         };
         int kk;
         if (L.any_diag || L.any_quirk) kk = pcr(std::true_type{}, std::integral_constant<int, 0>{});
