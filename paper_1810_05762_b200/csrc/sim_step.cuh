@@ -286,7 +286,13 @@ __device__ __forceinline__ bool factor6(const T (&H)[21], T (&Lc)[21], T (&rd)[6
 
 // alpha / beta of the PCR recurrences: fp32 uses reciprocal + multiply
 // (two roundings; the f64 parity instrument keeps IEEE division).
-__device__ __forceinline__ float fdiv(float a, float b) { return __fdividef(a, b); }
+// (rcp.approx.ftz + multiply: the value __fdividef gives for normal-range
+// divisors, without its large-divisor range checks)
+__device__ __forceinline__ float fdiv(float a, float b) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
+  return a * r;
+}
 __device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
 
 template <int W, class T>
@@ -1188,37 +1194,43 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
             T zaz = dot6p(rh, ar), lb = lbw * dot6p(rh, rh), denom = dot6p(ar, ar);
             seg_sum3<W>(zaz, lb, denom, mask);
             int kk = 0;
-            bool above = lb > tol2_safe || res_exact_p() > tol2;
-            while (__all_sync(mask, kk < cf.kmax && above)) {
-              if (!__all_sync(mask, denom > T(0) && zaz > T(0))) break;  // breakdown (krylov.cpp:144)
-              const float alpha = fdiv(zaz, denom);
+            // Exit tests of krylov.cpp: ||r|| <= tol ||b|| (:141, :154) and the
+            // breakdown test (:144) of the next trip are decided together at
+            // the end of a trip (both just leave the loop); all operands are
+            // segment-uniform, so every test is one vote.
+            auto go_on = [&](float lbv, float zv, float dv) {
+              bool above = lbv > tol2_safe;
+              if (!__all_sync(mask, above)) above = res_exact_p() > tol2;  // near convergence only
+              return __all_sync(mask, above && dv > 0.f && zv > 0.f);
+            };
+            if (kk < cf.kmax && go_on(lb, zaz, denom)) {
+              for (;;) {
+                const float alpha = fdiv(zaz, denom);
 #pragma unroll
-              for (int k = 0; k < 3; ++k) {
-                x2[k] = __ffma2_rn(ph[k], make_float2(alpha, alpha), x2[k]);
-                rh[k] = __ffma2_rn(ap[k], make_float2(-alpha, -alpha), rh[k]);
-              }
-              ++kk;
-              if (kk >= cf.kmax) break;  // exit certain: the rest cannot change xhat
-              L.template apply_hat_p<RARE, GR>(rh, ar, Hp);
-              // one reduction per trip: (lb, zn) and (aa, ax) as two pairs
-              float2 q0 = make_float2(lbw * dot6p(rh, rh), dot6p(rh, ar));
-              float2 q1 = make_float2(dot6p(ar, ar), dot6p(ar, ap));
+                for (int k = 0; k < 3; ++k) {
+                  x2[k] = __ffma2_rn(ph[k], make_float2(alpha, alpha), x2[k]);
+                  rh[k] = __ffma2_rn(ap[k], make_float2(-alpha, -alpha), rh[k]);
+                }
+                if (++kk >= cf.kmax) break;  // exit certain: the rest cannot change xhat
+                L.template apply_hat_p<RARE, GR>(rh, ar, Hp);
+                // one reduction per trip: (lb, zn) and (aa, ax) as two pairs
+                float2 q0 = make_float2(lbw * dot6p(rh, rh), dot6p(rh, ar));
+                float2 q1 = make_float2(dot6p(ar, ar), dot6p(ar, ap));
 #pragma unroll
-              for (int off = W / 2; off > 0; off >>= 1) {
-                q0 = __fadd2_rn(q0, make_float2(__shfl_xor_sync(mask, q0.x, off, W), __shfl_xor_sync(mask, q0.y, off, W)));
-                q1 = __fadd2_rn(q1, make_float2(__shfl_xor_sync(mask, q1.x, off, W), __shfl_xor_sync(mask, q1.y, off, W)));
-              }
-              lb = q0.x;
-              const float zn = q0.y, aa = q1.x, ax = q1.y;
-              above = lb > tol2_safe || res_exact_p() > tol2;
-              if (!__all_sync(mask, above)) break;
-              const float beta = fdiv(zn, zaz);
-              zaz = zn;
-              denom = aa + beta * (2.f * ax + beta * denom);
+                for (int off = W / 2; off > 0; off >>= 1) {
+                  q0 = __fadd2_rn(q0, make_float2(__shfl_xor_sync(mask, q0.x, off, W), __shfl_xor_sync(mask, q0.y, off, W)));
+                  q1 = __fadd2_rn(q1, make_float2(__shfl_xor_sync(mask, q1.x, off, W), __shfl_xor_sync(mask, q1.y, off, W)));
+                }
+                const float zn = q0.y, aa = q1.x, ax = q1.y;
+                const float beta = fdiv(zn, zaz);
+                denom = aa + beta * (2.f * ax + beta * denom);
+                if (!go_on(q0.x, zn, denom)) break;
+                zaz = zn;
 #pragma unroll
-              for (int k = 0; k < 3; ++k) {
-                ph[k] = __ffma2_rn(ph[k], make_float2(beta, beta), rh[k]);
-                ap[k] = __ffma2_rn(ap[k], make_float2(beta, beta), ar[k]);
+                for (int k = 0; k < 3; ++k) {
+                  ph[k] = __ffma2_rn(ph[k], make_float2(beta, beta), rh[k]);
+                  ap[k] = __ffma2_rn(ap[k], make_float2(beta, beta), ar[k]);
+                }
               }
             }
 #pragma unroll
