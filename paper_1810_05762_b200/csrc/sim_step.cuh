@@ -931,7 +931,10 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
 
     // ---------------- Newton loop (solver.cpp:540-548) ---------------------
     T u[6] = {v.x, v.y, v.z, w.x, w.y, w.z};  // warm start from current velocities
-    const bool need_solve = J > 0 || any_contact;
+    // segment-uniform decisions are taken through votes throughout: the
+    // compiler then sees uniform control flow and drops the convergence
+    // checks it would otherwise put in front of every shuffle of the solve
+    const bool need_solve = __any_sync(mask, J > 0 || any_contact);
     if (!need_solve) {  // free-body fast path, solver.cpp:517-523
       u[0] = vfree.x; u[1] = vfree.y; u[2] = vfree.z;
       u[3] = wfree.x; u[4] = wfree.y; u[5] = wfree.z;
@@ -1045,7 +1048,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
           break;
         }
         const T bb = seg_sum<W>(dot6(rhs, rhs), mask);
-        if (bb == T(0)) {
+        if (__all_sync(mask, bb == T(0))) {
 #pragma unroll
           for (int k = 0; k < 6; ++k) u[k] = T(0);
           continue;
@@ -1323,7 +1326,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
         };
         int kk;
         if (L.any_diag || L.any_quirk) kk = pcr(std::true_type{}, std::integral_constant<int, 0>{});
-        else if (L.grounds == 2) kk = pcr(std::false_type{}, std::integral_constant<int, 2>{});
+        else if (__all_sync(mask, L.grounds == 2)) kk = pcr(std::false_type{}, std::integral_constant<int, 2>{});
         else kk = pcr(std::false_type{}, std::integral_constant<int, 0>{});
         // back to velocities: solve L^T u = xhat (reciprocal diagonal parked in R_SCAT)
 #pragma unroll
