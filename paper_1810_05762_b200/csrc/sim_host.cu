@@ -455,7 +455,7 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
   bool boxes_shape = false;
   for (int b = 0; b < s->B; ++b) boxes_shape = boxes_shape || model->bodies[b].shape == STP_BOX;
   s->cpb = boxes_shape || task->kind == STP_TASK_HFH_TERRAIN ? 8 : 2;
-  s->cap = s->B * s->cpb;
+  s->cap = s->B * (s->cpb > 2 ? s->cpb + stp::kSpillSlots : s->cpb);  // slots per body incl. overflow rows
   s->obs_dim = 11 + 3 * s->J + model->n_feet + (task->height_map ? 165 : 0);
   s->tsize = precision == STP_PRECISION_F64 ? 8 : 4;
   auto bail = [&](int) -> stp_sim* {
@@ -489,7 +489,7 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
       (rc = dalloc(s, &s->d_cdata, N * s->cap * stp::kCData * sizeof(double))) ||
       (rc = dalloc(s, &s->d_act, N * std::max(1, s->J) * 4)) || (rc = dalloc(s, &s->d_obs, N * s->obs_dim * 4)) ||
       (rc = dalloc(s, &s->d_rew, N * 4)) || (rc = dalloc(s, &s->d_done, N)) ||
-      (rc = dalloc(s, &s->d_scratch, N * 55 * s->W * ts)))
+      (rc = dalloc(s, &s->d_scratch, N * size_t(stp::kScratchRows) * s->W * ts)))
     return bail(rc);
   if (precision == STP_PRECISION_F64) {
     stp::DevModel<double> dm;
@@ -620,7 +620,7 @@ int stp_set_terrain(stp_sim* s, const stp_static_box* boxes, int32_t n) {
   if (n > 0 && s->cpb < 8) {
     // terrain contacts need more slots per body: grow the recorded list too
     s->cpb = 8;
-    s->cap = s->B * s->cpb;
+    s->cap = s->B * (s->cpb > 2 ? s->cpb + stp::kSpillSlots : s->cpb);  // slots per body incl. overflow rows
     const size_t N = size_t(s->n);
     for (void* p : {(void*)s->d_cbody, (void*)s->d_cdata}) {
       CK(cudaFree(p));

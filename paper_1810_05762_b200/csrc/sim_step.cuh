@@ -33,7 +33,8 @@ constexpr int R_CT = 86;    // 11 per contact slot: n(3) r(3) t1(3) d b
 constexpr int G_QH = 0;     // 13: quirk in the transformed system: d0, qa (6), qc (6)
 constexpr int G_HD = 13;    // 21: diagonal block, kept only when it is not positive definite
 constexpr int G_LC = 34;    // 21: Cholesky factor L of the own block (exact residual test, back-substitution)
-constexpr int kScratchRows = 55;
+constexpr int G_CT = 55;    // 11 per overflow contact slot (terrain instantiation, slots CPB.. CPB+7)
+static_assert(G_CT + 11 * kSpillSlots == kScratchRows, "scratch layout");
 template <int CPB>
 __host__ __device__ constexpr int smem_rows() {
   return R_CT + 11 * CPB;
@@ -59,6 +60,19 @@ struct Lane {
   __device__ __forceinline__ T& at(int row) const { return sm[row * 32 + lane]; }
   __device__ __forceinline__ T at_kid(int row, int k) const { return sm[row * 32 + base + k]; }
   __device__ __forceinline__ T& g(int row) const { return gs[row * W + b]; }
+
+  // contact slot k of this lane: 11 rows n(3) r(3) t1(3) d b, in shared memory
+  // for k < CPB, in the global overflow rows (G_CT) beyond (terrain only)
+  struct Slot {
+    T* p;
+    int s;
+    __device__ __forceinline__ T& operator[](int f) const { return p[f * s]; }
+  };
+  template <int CPB>
+  __device__ __forceinline__ Slot slot(int k) const {
+    if (k < CPB) return {sm + (R_CT + 11 * k) * 32 + lane, 32};
+    return {gs + (G_CT + 11 * (k - CPB)) * W + b, W};
+  }
 
   // out = sum over children of v (parent side of a child's contribution)
   template <int K>
@@ -360,6 +374,8 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
   const int par_src = par >= 0 ? par : b;
   const bool pdyn = par >= 0 && !M.is_static[par];
   const int J = M.nj;
+  // contact slots per body: CPB in shared memory (+ overflow rows for terrain)
+  constexpr int CT = CPB > 2 ? CPB + kSpillSlots : CPB;
 
   extern __shared__ unsigned char smem_raw[];
   Lane<T, W> L;
@@ -468,17 +484,17 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
     // ---------------- K1: contacts (detect_contacts, collide.cpp:270-299) -
     // slot k of this lane: rows R_CT + 11k: n(3) r(3) t1(3) d b; sep kept in d's row until rows are built
     auto add_contact = [&](v3<T> p, v3<T> n, T sep, int key = -1) {
-      if (nc < CPB) {
-        const int r0 = R_CT + 11 * nc;
+      if (nc < CT) {
+        const auto S = L.template slot<CPB>(nc);
         const v3<T> r = p - x;
-        L.at(r0 + 6) = T(key);
-        L.at(r0 + 0) = n.x;
-        L.at(r0 + 1) = n.y;
-        L.at(r0 + 2) = n.z;
-        L.at(r0 + 3) = r.x;
-        L.at(r0 + 4) = r.y;
-        L.at(r0 + 5) = r.z;
-        L.at(r0 + 10) = sep;
+        S[6] = T(key);
+        S[0] = n.x;
+        S[1] = n.y;
+        S[2] = n.z;
+        S[3] = r.x;
+        S[4] = r.y;
+        S[5] = r.z;
+        S[10] = sep;
         ++nc;
       } else {
         overflow = true;
@@ -642,15 +658,15 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
               }
             }
           // insertion sort of this lane's slots by key (plane contacts keep key < 0)
-          for (int s1 = 1; s1 < nc && s1 < CPB; ++s1) {
+          for (int s1 = 1; s1 < nc; ++s1) {
             for (int s2 = s1; s2 > 0; --s2) {
-              const int ra = R_CT + 11 * (s2 - 1), rb = R_CT + 11 * s2;
-              if (!(L.at(ra + 6) > L.at(rb + 6))) break;
+              const auto A = L.template slot<CPB>(s2 - 1), B = L.template slot<CPB>(s2);
+              if (!(A[6] > B[6])) break;
 #pragma unroll
               for (int f = 0; f < 11; ++f) {
-                const T tmp = L.at(ra + f);
-                L.at(ra + f) = L.at(rb + f);
-                L.at(rb + f) = tmp;
+                const T tmp = A[f];
+                A[f] = B[f];
+                B[f] = tmp;
               }
             }
           }
@@ -902,24 +918,28 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
 #pragma unroll
     for (int k = 0; k < 6; ++k) L.at(R_HEQ + 21 + k) = rhs_own[k];
     // contact rows (solver.cpp:176-210): normal weight + tangent basis
+    auto contact_row = [&](const typename Lane<T, W>::Slot& S) {
+      const v3<T> n{S[0], S[1], S[2]};
+      const v3<T> rr{S[3], S[4], S[5]};
+      const T sep = S[10];
+      const v3<T> rn = cross(rr, n);
+      T wsum = inv_m * dot(n, n);
+      wsum += quad(Iinv, rn);
+      const v3<T> ref = fabs(n.z) < T(0.9) ? v3<T>{0, 0, 1} : v3<T>{1, 0, 0};
+      const v3<T> t1 = vunit(cross(n, ref));
+      S[6] = t1.x;
+      S[7] = t1.y;
+      S[8] = t1.z;
+      S[9] = cf.kc * (wsum > T(1e-12) ? T(1) / wsum : T(0));
+      S[10] = uni_bias(sep, cf.beta, cf.dt);
+    };
 #pragma unroll
     for (int k = 0; k < CPB; ++k) {
-      if (k < nc) {
-        const int r0 = R_CT + 11 * k;
-        const v3<T> n{L.at(r0), L.at(r0 + 1), L.at(r0 + 2)};
-        const v3<T> rr{L.at(r0 + 3), L.at(r0 + 4), L.at(r0 + 5)};
-        const T sep = L.at(r0 + 10);
-        const v3<T> rn = cross(rr, n);
-        T wsum = inv_m * dot(n, n);
-        wsum += quad(Iinv, rn);
-        const v3<T> ref = fabs(n.z) < T(0.9) ? v3<T>{0, 0, 1} : v3<T>{1, 0, 0};
-        const v3<T> t1 = vunit(cross(n, ref));
-        L.at(r0 + 6) = t1.x;
-        L.at(r0 + 7) = t1.y;
-        L.at(r0 + 8) = t1.z;
-        L.at(r0 + 9) = cf.kc * (wsum > T(1e-12) ? T(1) / wsum : T(0));
-        L.at(r0 + 10) = uni_bias(sep, cf.beta, cf.dt);
-      }
+      if (k < nc) contact_row(L.template slot<CPB>(k));
+    }
+    if constexpr (CT > CPB) {
+#pragma unroll 1
+      for (int k = CPB; k < nc; ++k) contact_row(L.template slot<CPB>(k));
     }
     // the constant off-diagonal block must be finite (krylov.cpp:113)
     bool off_fin = true;
@@ -998,36 +1018,40 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
           rhs[5] += got[8];
         }
         // contacts: normal + smoothed Coulomb friction (:311-327)
+        auto contact_newton = [&](const typename Lane<T, W>::Slot& S) {
+          const v3<T> n{S[0], S[1], S[2]};
+          const v3<T> rr{S[3], S[4], S[5]};
+          const T cd = S[9], cb = S[10];
+          const v3<T> rn = cross(rr, n);
+          const T jn[6] = {n.x, n.y, n.z, rn.x, rn.y, rn.z};
+          const T pred = cd * (cb - dot6(jn, u));
+          if (pred > T(0)) {
+            const v3<T> ta{S[6], S[7], S[8]};
+            const v3<T> tb = cross(n, ta);
+            const v3<T> rta = cross(rr, ta), rtb = cross(rr, tb);
+            const T j1[6] = {ta.x, ta.y, ta.z, rta.x, rta.y, rta.z};
+            const T j2[6] = {tb.x, tb.y, tb.z, rtb.x, rtb.y, rtb.z};
+            const T vt1 = dot6(j1, u), vt2 = dot6(j2, u);
+            const T fw = fric_weight(pred, sqrt(vt1 * vt1 + vt2 * vt2), cf.epsf);
+            if (cd > T(0)) {
+              sym_add(H, jn, cd);
+              const T db = cd * cb;
 #pragma unroll
-        for (int k = 0; k < CPB; ++k) {
-          if (k < nc) {
-            const int r0 = R_CT + 11 * k;
-            const v3<T> n{L.at(r0), L.at(r0 + 1), L.at(r0 + 2)};
-            const v3<T> rr{L.at(r0 + 3), L.at(r0 + 4), L.at(r0 + 5)};
-            const T cd = L.at(r0 + 9), cb = L.at(r0 + 10);
-            const v3<T> rn = cross(rr, n);
-            const T jn[6] = {n.x, n.y, n.z, rn.x, rn.y, rn.z};
-            const T pred = cd * (cb - dot6(jn, u));
-            if (pred > T(0)) {
-              const v3<T> ta{L.at(r0 + 6), L.at(r0 + 7), L.at(r0 + 8)};
-              const v3<T> tb = cross(n, ta);
-              const v3<T> rta = cross(rr, ta), rtb = cross(rr, tb);
-              const T j1[6] = {ta.x, ta.y, ta.z, rta.x, rta.y, rta.z};
-              const T j2[6] = {tb.x, tb.y, tb.z, rtb.x, rtb.y, rtb.z};
-              const T vt1 = dot6(j1, u), vt2 = dot6(j2, u);
-              const T fw = fric_weight(pred, sqrt(vt1 * vt1 + vt2 * vt2), cf.epsf);
-              if (cd > T(0)) {
-                sym_add(H, jn, cd);
-                const T db = cd * cb;
-#pragma unroll
-                for (int r = 0; r < 6; ++r) rhs[r] += jn[r] * db;
-              }
-              if (fw > T(0)) {
-                sym_add(H, j1, fw);
-                sym_add(H, j2, fw);
-              }
+              for (int r = 0; r < 6; ++r) rhs[r] += jn[r] * db;
+            }
+            if (fw > T(0)) {
+              sym_add(H, j1, fw);
+              sym_add(H, j2, fw);
             }
           }
+        };
+#pragma unroll
+        for (int k = 0; k < CPB; ++k) {
+          if (k < nc) contact_newton(L.template slot<CPB>(k));
+        }
+        if constexpr (CT > CPB) {
+#pragma unroll 1
+          for (int k = CPB; k < nc; ++k) contact_newton(L.template slot<CPB>(k));
         }
 
         // ---------------- PCR (solve_krylov_inplace, krylov.cpp:106-174) --
@@ -1373,19 +1397,19 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
       off -= nc;  // exclusive prefix: contact list order = body order
       const int total = __shfl_sync(mask, off + nc, W - 1, W);
       if (b == 0) a.c_count[e] = total;
-#pragma unroll
-      for (int k = 0; k < CPB; ++k) {
-        if (k < nc && off + k < a.cap) {
-          const int r0 = R_CT + 11 * k;
-          const v3<T> n{L.at(r0), L.at(r0 + 1), L.at(r0 + 2)};
-          const v3<T> rr{L.at(r0 + 3), L.at(r0 + 4), L.at(r0 + 5)};
-          const T cd = L.at(r0 + 9), cb = L.at(r0 + 10);
+#pragma unroll 1
+      for (int k = 0; k < nc; ++k) {
+        if (off + k < a.cap) {
+          const auto S = L.template slot<CPB>(k);
+          const v3<T> n{S[0], S[1], S[2]};
+          const v3<T> rr{S[3], S[4], S[5]};
+          const T cd = S[9], cb = S[10];
           const v3<T> rn = cross(rr, n);
           const T jn[6] = {n.x, n.y, n.z, rn.x, rn.y, rn.z};
           const T pn = max(T(0), cd * (cb - dot6(jn, u)));
           v3<T> pt{0, 0, 0};
           if (pn > T(0)) {
-            const v3<T> ta{L.at(r0 + 6), L.at(r0 + 7), L.at(r0 + 8)};
+            const v3<T> ta{S[6], S[7], S[8]};
             const v3<T> tb = cross(n, ta);
             const v3<T> rta = cross(rr, ta), rtb = cross(rr, tb);
             const T j1[6] = {ta.x, ta.y, ta.z, rta.x, rta.y, rta.z};

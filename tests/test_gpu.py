@@ -277,6 +277,46 @@ def test_terrain_contacts_and_height_map(precision):
     assert (np.abs(oo[:, -165:] + oo[:, :1]) > 1e-3).any()  # some samples see a box
 
 
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_dense_terrain_contact_overflow_slots(precision):
+    """Dense terrain: bodies with more than the 8 shared-memory contact slots
+    continue in the global overflow rows; the ordered list (count, bodies,
+    normals) still equals the reference algorithm's uncapped one and no env
+    reports an overflow."""
+    n = 32
+    boxes = _terrain(n_boxes=900, seed=5)
+    g = VecEnv("hfh_terrain", n_envs=n, precision=precision, seed=13, terrain=boxes)
+    o = oracle.OracleEnv(g.model, g.task, g.cfg, n, seed=13, terrain=boxes)
+    tm = np.array([g.model.joints[j].max_torque for j in range(g.action_dim)])
+    most = 0
+    mism = 0
+    for t in range(12):
+        s = o.get_state()
+        if t == 0:
+            s[..., 2] += 0.3
+            o.set_state(s)
+        g.set_state(s)
+        tq = o.random_actions(t) * tm
+        o.physics_step(tq)
+        g.physics_step(tq)
+        co, cg = o.contact_arrays(g.contact_capacity), g.contact_arrays()
+        for e in range(n):
+            c = co["count"][e]
+            if c:
+                most = max(most, int(np.bincount(co["body_a"][e, :c]).max()))
+            same = c == cg["count"][e] and np.array_equal(co["body_a"][e, :c], cg["body_a"][e, :c])
+            if same and precision == "f64":
+                same = np.abs(co["normal"][e, :c] - cg["normal"][e, :c]).max(initial=0.0) <= 1e-9
+            if not same:
+                near = np.abs(co["separation"][e, :c] - g.cfg.contact_margin).min(initial=1.0)
+                if precision == "f64" or near > 1e-4:
+                    mism += 1
+    print(f"{precision}: most contacts on one body {most}")
+    assert most > 8  # the overflow rows were exercised
+    assert mism == 0
+    assert g.report()["overflow"].sum() == 0
+
+
 @pytest.mark.parametrize("n", [4096, 1000])
 def test_step_host_pipelined_matches_device_step(n):
     """stp_step_host runs env chunks on their own streams (copies overlap the
