@@ -454,7 +454,7 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
   s->W = s->B <= 8 ? 8 : (s->B <= 16 ? 16 : 32);
   bool boxes_shape = false;
   for (int b = 0; b < s->B; ++b) boxes_shape = boxes_shape || model->bodies[b].shape == STP_BOX;
-  s->cpb = boxes_shape || task->kind == STP_TASK_HFH_TERRAIN ? 8 : 2;
+  s->cpb = boxes_shape || task->kind == STP_TASK_HFH_TERRAIN ? 4 : 2;
   s->cap = s->B * (s->cpb > 2 ? s->cpb + stp::kSpillSlots : s->cpb);  // slots per body incl. overflow rows
   s->obs_dim = 11 + 3 * s->J + model->n_feet + (task->height_map ? 165 : 0);
   s->tsize = precision == STP_PRECISION_F64 ? 8 : 4;
@@ -617,9 +617,9 @@ int stp_set_terrain(stp_sim* s, const stp_static_box* boxes, int32_t n) {
     s->grid_y0 = y0;
     s->grid_inv = inv;
   }
-  if (n > 0 && s->cpb < 8) {
+  if (n > 0 && s->cpb < 4) {
     // terrain contacts need more slots per body: grow the recorded list too
-    s->cpb = 8;
+    s->cpb = 4;
     s->cap = s->B * (s->cpb > 2 ? s->cpb + stp::kSpillSlots : s->cpb);  // slots per body incl. overflow rows
     const size_t N = size_t(s->n);
     for (void* p : {(void*)s->d_cbody, (void*)s->d_cdata}) {

@@ -261,9 +261,22 @@ __device__ __forceinline__ double terrain_height_grid(const KArgs<T>& a, double 
 }
 
 // geometric height-map offsets (ratio 1.3 from 0.2 m)
+// 0.2 (1.3^a - 1) / 0.3 for a = 0..7, evaluated once on the host with libm
+// (the oracle's std::pow) and written as exact binary literals: no per-sample
+// double pow in the kernel.
 __device__ __forceinline__ double geo_offset(int k) {
   const int a = k < 0 ? -k : k;
-  const double d = 0.2 * (pow(1.3, double(a)) - 1.0) / 0.3;
+  double d;
+  switch (a) {
+    case 0: d = 0x0p+0; break;
+    case 1: d = 0x1.999999999999bp-3; break;
+    case 2: d = 0x1.d70a3d70a3d73p-2; break;
+    case 3: d = 0x1.989374bc6a7f1p-1; break;
+    case 4: d = 0x1.3cc63f141205ep+0; break;
+    case 5: d = 0x1.cf01b866e43adp+0; break;
+    case 6: d = 0x1.468deb0fadf31p+1; break;
+    default: d = 0x1.c21ee4c795559p+1; break;
+  }
   return k < 0 ? -d : d;
 }
 

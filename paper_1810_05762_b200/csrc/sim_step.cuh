@@ -33,7 +33,7 @@ constexpr int R_CT = 86;    // 11 per contact slot: n(3) r(3) t1(3) d b
 constexpr int G_QH = 0;     // 13: quirk in the transformed system: d0, qa (6), qc (6)
 constexpr int G_HD = 13;    // 21: diagonal block, kept only when it is not positive definite
 constexpr int G_LC = 34;    // 21: Cholesky factor L of the own block (exact residual test, back-substitution)
-constexpr int G_CT = 55;    // 11 per overflow contact slot (terrain instantiation, slots CPB.. CPB+7)
+constexpr int G_CT = 55;    // 11 per overflow contact slot (terrain instantiation, slots CPB.. CPB+11)
 static_assert(G_CT + 11 * kSpillSlots == kScratchRows, "scratch layout");
 template <int CPB>
 __host__ __device__ constexpr int smem_rows() {
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
           if (s0 < margin) add_contact(p0 - up * rad, up, s0, -2);
           const T s1 = p1.z - rad;
           if (s1 < margin) add_contact(p1 - up * rad, up, s1, -1);
-        } else if constexpr (CPB > 2) {  // dynamic boxes: 8 corners (host picks CPB = 8)
+        } else if constexpr (CPB > 2) {  // dynamic boxes: 8 corners (host picks the CPB = 4 + overflow instantiation)
           for (int cx = -1; cx <= 1; cx += 2)
             for (int cy = -1; cy <= 1; cy += 2)
               for (int cz = -1; cz <= 1; cz += 2) {
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
         }
       }
       // static terrain boxes (collide.cpp:287-298), in box-index order
-      // (terrain handles always run the CPB = 8 instantiation)
+      // (terrain handles always run the CPB = 4 + overflow instantiation)
       if constexpr (CPB > 2) if (a.n_boxes > 0 && shp != STP_BOX) {
         const double ox = a.origin[2 * e], oy = a.origin[2 * e + 1];
         const v3<T> lo{min(p0.x, p1.x) - rad, min(p0.y, p1.y) - rad, min(p0.z, p1.z) - rad};
@@ -1678,14 +1678,14 @@ template <class T>
 cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s) {
   if (lanes == 32) {
     if (cpb <= 2) return launch_one<T, 32, 2>(a, s);
-    return launch_one<T, 32, 8>(a, s);
+    return launch_one<T, 32, 4>(a, s);
   }
   if (lanes == 16) {
     if (cpb <= 2) return launch_one<T, 16, 2>(a, s);
-    return launch_one<T, 16, 8>(a, s);
+    return launch_one<T, 16, 4>(a, s);
   }
   if (cpb <= 2) return launch_one<T, 8, 2>(a, s);
-  return launch_one<T, 8, 8>(a, s);
+  return launch_one<T, 8, 4>(a, s);
 }
 
 }  // namespace stp

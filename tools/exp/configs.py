@@ -34,11 +34,12 @@ def run(task, n, boxes=None, steps=30):
     env.close()
 
 
-run("ant", 64)
-run("ant", 4096)
-run("humanoid", 1024)
-run("humanoid", 4096)
-run("hfh", 4096)
+if __name__ == "__main__":
+  run("ant", 64)
+  run("ant", 4096)
+  run("humanoid", 1024)
+  run("humanoid", 4096)
+  run("hfh", 4096)
 # HFH env grid: 64 columns x 2 m -> 4096 envs span ~128 m x 128 m
-run("hfh_terrain", 4096, terrain(2048, 131.0))
-run("hfh_terrain", 4096, terrain(8192, 131.0))
+  run("hfh_terrain", 4096, terrain(2048, 131.0))
+  run("hfh_terrain", 4096, terrain(8192, 131.0))
