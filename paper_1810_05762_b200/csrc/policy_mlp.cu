@@ -9,7 +9,10 @@
 //   -> last layer: mean (+ log_std, counter-based Gaussian sample, log-prob)
 // for the policy net, then the same chain for the value net.  Weights (packed
 // bf16, K-major 8x16B core-matrix layout) are staged into smem with TMA bulk
-// copies (cp.async.bulk) completing on an mbarrier.
+// copies (cp.async.bulk) completing on an mbarrier; nets whose weights do not
+// fit next to the operands (e.g. the 241-wide terrain observation) stream each
+// layer's weights in contiguous K-block chunks through one buffer, every chunk
+// accumulating into the same TMEM accumulator.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -28,6 +31,7 @@ struct MlpDims {
   int k[4];  // padded input width of layer l (multiple of 16)
   int n[4];  // padded output width of layer l (multiple of 16)
   int out;   // real output width of the last layer
+  int kb_chunk[4];  // streaming mode: 8-wide K blocks per weight chunk (even)
 };
 
 struct NetPtrs {
@@ -130,27 +134,26 @@ __device__ __forceinline__ void st_chunk(__nv_bfloat16* buf, int kc, int row, co
 }
 
 struct Smem {
-  uint64_t bar_w;    // weights landed
-  uint64_t bar_mma;  // layer accumulator ready
+  uint64_t bar_w;      // weights landed
+  uint64_t bar_mma;    // layer accumulator ready
+  uint64_t bar_chunk;  // streaming mode: a chunk's MMAs done (weight buffer free)
   uint32_t tmem;
 };
 
 // One 4-layer net over the CTA's 128 rows; A operand of layer 0 already in abuf0.
 // Returns with the final accumulator (n[3] columns) in TMEM.
 __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4], __nv_bfloat16* abuf0,
-                        __nv_bfloat16* abuf1, Smem* sh, uint32_t& wphase, uint32_t& mphase, int tid) {
+                        __nv_bfloat16* abuf1, Smem* sh, uint32_t& wphase, uint32_t& mphase, int tid,
+                        bool stream) {
   const int warp = tid >> 5;
   const int row = (warp & 3) * 32 + (tid & 31);  // TMEM lane = tile row
   const int half = warp >> 2;                    // column half of the epilogue
-  // stage the 4 weight blobs (one TMA bulk copy each, one barrier)
-  if (tid == 0) {
-    uint32_t bytes = 0;
-    for (int l = 0; l < 4; ++l) bytes += uint32_t(D.k[l]) * D.n[l] * 2;
-    mbar_expect_tx(&sh->bar_w, bytes);
-    for (int l = 0; l < 4; ++l) bulk_g2s(wsm[l], P.w[l], uint32_t(D.k[l]) * D.n[l] * 2, &sh->bar_w);
+  // resident mode: the 4 weight blobs were issued by the caller
+  if (!stream) {
+    mbar_wait(&sh->bar_w, wphase);
+    wphase ^= 1;
   }
-  mbar_wait(&sh->bar_w, wphase);
-  wphase ^= 1;
+  uint32_t cphase = 0;  // streaming mode, issuing thread only
   __nv_bfloat16* a_in = abuf0;
   __nv_bfloat16* a_out = abuf1;
   for (int l = 0; l < 4; ++l) {
@@ -159,12 +162,37 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
     if (tid == 0) {
       tc_after_sync();
       const uint32_t idesc = umma_idesc(kM, D.n[l]);
-      const uint32_t a0 = smem_u32(a_in), b0 = smem_u32(wsm[l]);
-      for (int ks = 0; ks < D.k[l] / 16; ++ks) {
-        // K step of 16 = two 8-element core-matrix columns
-        const uint64_t da = umma_desc(a0 + uint32_t(ks) * 2 * kM * 16, kM * 16, 128);
-        const uint64_t db = umma_desc(b0 + uint32_t(ks) * 2 * D.n[l] * 16, uint32_t(D.n[l]) * 16, 128);
-        mma_bf16(sh->tmem, da, db, idesc, ks > 0);
+      const uint32_t a0 = smem_u32(a_in), b0 = smem_u32(wsm[stream ? 0 : l]);
+      if (!stream) {
+        for (int ks = 0; ks < D.k[l] / 16; ++ks) {
+          // K step of 16 = two 8-element core-matrix columns
+          const uint64_t da = umma_desc(a0 + uint32_t(ks) * 2 * kM * 16, kM * 16, 128);
+          const uint64_t db = umma_desc(b0 + uint32_t(ks) * 2 * D.n[l] * 16, uint32_t(D.n[l]) * 16, 128);
+          mma_bf16(sh->tmem, da, db, idesc, ks > 0);
+        }
+      } else {
+        // K blocks [kb0, kb0 + nb) of the packed [k/8][n][8] weight are one
+        // contiguous range: stage it, accumulate its MMAs, free the buffer
+        const int kbt = D.k[l] / 8, kbc = D.kb_chunk[l];
+        for (int kb0 = 0; kb0 < kbt; kb0 += kbc) {
+          const int nb = min(kbc, kbt - kb0);
+          const uint32_t bytes = uint32_t(nb) * 8 * D.n[l] * 2;
+          mbar_expect_tx(&sh->bar_w, bytes);
+          bulk_g2s(wsm[0], P.w[l] + size_t(kb0) * 8 * D.n[l], bytes, &sh->bar_w);
+          mbar_wait(&sh->bar_w, wphase);
+          wphase ^= 1;
+          for (int ks = 0; ks < nb / 2; ++ks) {
+            const int kg = kb0 / 2 + ks;  // global K step of 16
+            const uint64_t da = umma_desc(a0 + uint32_t(kg) * 2 * kM * 16, kM * 16, 128);
+            const uint64_t db = umma_desc(b0 + uint32_t(ks) * 2 * D.n[l] * 16, uint32_t(D.n[l]) * 16, 128);
+            mma_bf16(sh->tmem, da, db, idesc, kg > 0);
+          }
+          if (kb0 + nb < kbt) {
+            umma_commit(&sh->bar_chunk);
+            mbar_wait(&sh->bar_chunk, cphase);
+            cphase ^= 1;
+          }
+        }
       }
       umma_commit(&sh->bar_mma);
     }
@@ -198,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const float* __restrict__ stdv, MlpDims Dpi, NetPtrs Ppi, MlpDims Dv, NetPtrs Pv,
                  const float* __restrict__ log_std, uint64_t seed, uint64_t step, long long env_offset,
                  float* __restrict__ mu_out, float* __restrict__ act_out, float* __restrict__ logp_out,
-                 float* __restrict__ v_out, int a0_elems, int a1_elems) {
+                 float* __restrict__ v_out, int a0_elems, int a1_elems, int wbuf_elems) {
   extern __shared__ __align__(1024) unsigned char smem[];
   Smem* sh = reinterpret_cast<Smem*>(smem);
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(smem + 1024);
@@ -217,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     mbar_init(&sh->bar_w, 1);
     mbar_init(&sh->bar_mma, 1);
+    mbar_init(&sh->bar_chunk, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {  // TMEM: 256 columns (max layer width)
@@ -227,30 +256,62 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_after_sync();
 
-  // whitened, clipped observation row -> bf16 operand (RunningStat);
-  // the two thread halves split the K chunks
-  for (int kc = warp >> 2; kc < D.k[0] / 8; kc += 2) {
-    float x8[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int c = kc * 8 + i;
-      float x = 0.f;
-      if (row < n_envs && c < obs_dim) {
-        x = (obs[size_t(row) * obs_dim + c] - mean[c]) * (1.f / stdv[c]);
-        x = fminf(fmaxf(x, -10.f), 10.f);
-      }
-      x8[i] = x;
-    }
-    st_chunk(abuf0, kc, lrow, x8);
-  }
   __nv_bfloat16* wsm[4];
   int off = 0;
   for (int l = 0; l < 4; ++l) {
     wsm[l] = wbase + off;
     off += D.k[l] * D.n[l];
   }
+  // stage the 4 weight blobs first (one TMA bulk copy each, one barrier) so
+  // the copies overlap the observation prologue (resident mode)
+  const bool stream = wbuf_elems > 0;
+  if (tid == 0 && !stream) {
+    uint32_t bytes = 0;
+    for (int l = 0; l < 4; ++l) bytes += uint32_t(D.k[l]) * D.n[l] * 2;
+    mbar_expect_tx(&sh->bar_w, bytes);
+    for (int l = 0; l < 4; ++l) bulk_g2s(wsm[l], P.w[l], uint32_t(D.k[l]) * D.n[l] * 2, &sh->bar_w);
+  }
+  // whitened, clipped observation rows -> bf16 operand (RunningStat,
+  // SPEC.md:446-454).  The tile's rows are one contiguous block of global
+  // memory: it is read with coalesced float4 loads into the (still unused)
+  // layer-1 operand buffer, in row passes that fit it, then each (row, 8-column
+  // chunk) is whitened and written as one 16-byte operand chunk.
+  {
+    float* stage = reinterpret_cast<float*>(abuf1);
+    const int tile0 = blockIdx.x * kM;
+    const int rows = min(kM, n_envs - tile0);
+    const int pass_rows = min(kM, (a1_elems * 2) / (obs_dim * 4));
+    const int kchunks = D.k[0] / 8;
+    for (int p0 = 0; p0 < kM; p0 += pass_rows) {
+      const int pr = max(0, min(pass_rows, rows - p0));
+      const int nf = pr * obs_dim;
+      const float* src = obs + (size_t(tile0) + p0) * obs_dim;
+      const int nf4 = (reinterpret_cast<uintptr_t>(src) & 15) == 0 ? nf / 4 : 0;  // float4 path when aligned
+      for (int i = tid; i < nf4; i += kThreads)
+        reinterpret_cast<float4*>(stage)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
+      for (int i = nf4 * 4 + tid; i < nf; i += kThreads) stage[i] = __ldg(src + i);
+      __syncthreads();
+      const int prow = min(pass_rows, kM - p0);
+      for (int u = tid; u < prow * kchunks; u += kThreads) {
+        const int r = u % prow, kc = u / prow;
+        float x8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = kc * 8 + i;
+          float x = 0.f;
+          if (r < pr && c < obs_dim) {
+            x = (stage[r * obs_dim + c] - __ldg(mean + c)) * (1.f / __ldg(stdv + c));
+            x = fminf(fmaxf(x, -10.f), 10.f);
+          }
+          x8[i] = x;
+        }
+        st_chunk(abuf0, kc, p0 + r, x8);
+      }
+      __syncthreads();
+    }
+  }
   uint32_t wphase = 0, mphase = 0;
-  run_net(D, P, wsm, abuf0, abuf1, sh, wphase, mphase, tid);
+  run_net(D, P, wsm, abuf0, abuf1, sh, wphase, mphase, tid, stream);
   const uint32_t tbase = sh->tmem + (uint32_t((warp & 3) * 32) << 16);
   if (warp < 4) {  // last layer: 32 (policy) / 16 (value) columns, one warp per TMEM lane group
     if (!value_net) {
@@ -348,8 +409,25 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
     c1 = mx(c1, mx(Dv.k[1], Dv.k[3]));
   }
   const int a0 = kM * c0, a1 = kM * c1;
-  const size_t smem = 1024 + size_t(a0 + a1 + wmax) * 2;
-  if (smem > 227 * 1024) return stp::fail(STP_EINVAL, "stp_policy_forward: network too large for shared memory");
+  const size_t kSmemMax = 227 * 1024;
+  const size_t base = 1024 + size_t(a0 + a1) * 2;
+  size_t smem = base + size_t(wmax) * 2;
+  int wbuf = 0;  // 0: all weights resident
+  for (MlpDims* D : {&Dpi, &Dv})
+    for (int l = 0; l < 4; ++l) D->kb_chunk[l] = D->k[l] / 8;
+  if (smem > kSmemMax) {
+    // stream: one weight buffer filling the rest of shared memory
+    wbuf = int((kSmemMax - base) / 2) / 128 * 128;
+    for (MlpDims* D : {&Dpi, &Dv}) {
+      if (D == &Dv && !value_out) continue;
+      for (int l = 0; l < 4; ++l) {
+        D->kb_chunk[l] = (wbuf / (8 * D->n[l])) & ~1;
+        if (D->kb_chunk[l] < 2)
+          return stp::fail(STP_EINVAL, "stp_policy_forward: network too large for shared memory");
+      }
+    }
+    smem = base + size_t(wbuf) * 2;
+  }
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(k_policy_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -359,7 +437,7 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
   const dim3 grid((n_envs + kM - 1) / kM, value_out ? 2 : 1);
   k_policy_mlp<<<grid, kThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
       obs, n_envs, obs_dim, obs_mean, obs_std, Dpi, Ppi, Dv, Pv, log_std, seed, step, env_offset, mean_out,
-      action_out, logp_out, value_out, a0, a1);
+      action_out, logp_out, value_out, a0, a1, wbuf);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_policy_mlp: ") + cudaGetErrorString(e));
   return STP_OK;

@@ -11,7 +11,7 @@ from paper_1810_05762_b200.policy import HIDDEN, ActorCritic, PolicyKernel, Runn
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name,obs_dim,act_dim,n", [("humanoid", 76, 21, 4096), ("ant", 39, 8, 300),
+@pytest.mark.parametrize("name,obs_dim,act_dim,n", [("humanoid", 76, 21, 4096), ("ant", 39, 8, 300), ("hfh", 241, 21, 1000),
                                                     ("humanoid", 76, 21, 77)])
 def test_policy_kernel_matches_torch_fp32(name, obs_dim, act_dim, n):
     torch.manual_seed(0)
