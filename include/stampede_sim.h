@@ -237,6 +237,16 @@ int stp_set_external_loads(stp_sim* sim, const double* loads);
 int stp_get_contacts(stp_sim* sim, int32_t* count, int32_t* body_a, int32_t* body_b,
                      double* point, double* normal, double* separation,
                      double* normal_impulse, double* tangential_impulse);
+/* Inter-agent contacts of the current state: the pairs
+ * detect_contacts (collide.cpp:300-343) appends when
+ * Scene::inter_agent_collisions is set — dynamic sphere/capsule bodies of
+ * different envs whose AABBs overlap within the margin, one segment-segment
+ * contact each (:219-266), in (body_a, body_b) order.  Body indices are global
+ * within the sim (env * B + body).  count = total pairs; at most capacity
+ * entries are written; any array may be NULL.  Detection only: the step does
+ * not yet solve contact-merged islands. */
+int stp_detect_inter_agent(stp_sim* sim, int32_t capacity, int32_t* count, int32_t* body_a, int32_t* body_b,
+                           double* point, double* normal, double* separation);
 /* StepReport (types.hpp:115-120) of the last physics step, per env:
  * newton iterations, krylov iterations, failed (rolled back) flag,
  * contact overflow flag (more contacts than slots; should stay 0). */

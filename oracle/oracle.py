@@ -64,6 +64,9 @@ def _lib(kind: str) -> C.CDLL:
     L.orc_step.argtypes = [P, P, P, P, P]
     L.orc_random_actions.argtypes = [P, P, C.c_uint64]
     L.orc_get_contacts.argtypes = [P, C.c_int32] + [P] * 8
+    if hasattr(L, "orc_ref_detect"):  # reference builds only
+        L.orc_ref_detect.argtypes = [P, C.c_int32] + [P] * 5
+        L.orc_ref_detect.restype = C.c_int32
     L.orc_get_report.argtypes = [P, P, P, P]
     L.orc_get_task_state.argtypes = [P, P, P, P]
     L.orc_set_task_state.argtypes = [P, P, P, P]
@@ -178,6 +181,19 @@ class OracleEnv:
                                 _p(out["point"]), _p(out["normal"]), _p(out["separation"]),
                                 _p(out["normal_impulse"]), _p(out["tangential_impulse"]))
         return out
+
+    def ref_detect_contacts(self, capacity: int = 1 << 16):
+        """The compiled reference's detect_contacts with inter_agent_collisions
+        on, for the current state: every contact (global body indices), the
+        reference's order.  Reference builds only."""
+        if not hasattr(self.L, "orc_ref_detect"):
+            raise RuntimeError("ref_detect_contacts needs the compiled reference (kind='reference')")
+        out = dict(body_a=np.zeros(capacity, np.int32), body_b=np.zeros(capacity, np.int32),
+                   point=np.zeros((capacity, 3)), normal=np.zeros((capacity, 3)), separation=np.zeros(capacity))
+        n = self.L.orc_ref_detect(self.h, capacity, _p(out["body_a"]), _p(out["body_b"]), _p(out["point"]),
+                                  _p(out["normal"]), _p(out["separation"]))
+        k = min(n, capacity)
+        return {key: v[:k] for key, v in out.items()}
 
     def report(self):
         N = self.n_envs

@@ -194,3 +194,35 @@ extern "C" int orc_ref_first_system(void* h, int e, const double* torques, doubl
   std::copy(sys.rhs.begin(), sys.rhs.end(), rhs);
   return int(contacts.size());
 }
+
+// Parity hook for inter-agent contacts: the reference's detect_contacts
+// (collide.cpp:270-346) with Scene::inter_agent_collisions = true on the
+// world's current state.  Global body indices (env * B + body), the
+// reference's list order; returns the total count (entries beyond capacity
+// are not written).
+extern "C" int orc_ref_detect(void* h, int capacity, int32_t* body_a, int32_t* body_b, double* point,
+                              double* normal, double* separation) {
+  auto* w = reinterpret_cast<orc::World*>(h);
+  orc::ReferencePhysics rp;
+  rp.build(*w);
+  rp.scene.inter_agent_collisions = true;
+  const int NB = w->n * w->nb();
+  for (int i = 0; i < NB; ++i) {
+    const double* s = w->state.data() + size_t(i) * STP_STATE_STRIDE;
+    stampede::physics::RigidBodyState& rs = rp.scene.states[i];
+    rs.position = {s[0], s[1], s[2]};
+    rs.orientation = {s[3], s[4], s[5], s[6]};
+    rs.linear_velocity = {s[7], s[8], s[9]};
+    rs.angular_velocity = {s[10], s[11], s[12]};
+  }
+  const auto cs = stampede::physics::detect_contacts(rp.scene, w->cfg.contact_margin);
+  const int n = int(cs.size());
+  for (int i = 0; i < n && i < capacity; ++i) {
+    body_a[i] = cs[i].body_a;
+    body_b[i] = cs[i].body_b;
+    point[3 * i] = cs[i].point.x; point[3 * i + 1] = cs[i].point.y; point[3 * i + 2] = cs[i].point.z;
+    normal[3 * i] = cs[i].normal.x; normal[3 * i + 1] = cs[i].normal.y; normal[3 * i + 2] = cs[i].normal.z;
+    separation[i] = cs[i].separation;
+  }
+  return n;
+}

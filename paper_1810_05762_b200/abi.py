@@ -162,6 +162,7 @@ SIGNATURES = [
     ("stp_get_state", _I, [_P, _P]),
     ("stp_set_external_loads", _I, [_P, _P]),
     ("stp_get_contacts", _I, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("stp_detect_inter_agent", _I, [_P, _I32, _P, _P, _P, _P, _P, _P]),
     ("stp_get_report", _I, [_P, _P, _P, _P, _P]),
     ("stp_get_task_state", _I, [_P, _P, _P, _P]),
     ("stp_set_task_state", _I, [_P, _P, _P, _P]),

@@ -22,7 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 EXTRA = os.environ.get("STP_NVCC_EXTRA", "").split()
 FLAGS = EXTRA + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
-SOURCES = ["sim_step_f32.cu", "sim_step_f64.cu", "sim_host.cu", "sim_aux.cu", "models.cpp", "policy_mlp.cu"]
+SOURCES = ["sim_step_f32.cu", "sim_step_f64.cu", "sim_host.cu", "sim_aux.cu", "sim_pairs.cu", "models.cpp", "policy_mlp.cu"]
 DEPS = ["sim_device.cuh", "sim_kernels.cuh", "sim_step.cuh", "sim_launch.h", "stp_rng.h", "stp_error.h"]
 
 

@@ -69,6 +69,7 @@ struct stp_sim {
   static constexpr int kChunks = STP_HOST_CHUNKS;
   cudaStream_t cs[kChunks] = {};
   cudaEvent_t ev_in = nullptr, ev_out[kChunks] = {};
+  stp::PairScratch* pairs = nullptr;  // inter-agent detection scratch (created on first use)
   std::vector<void*> allocations;
 };
 
@@ -527,6 +528,7 @@ void stp_destroy(stp_sim* s) {
     if (s->ev_out[c]) cudaEventDestroy(s->ev_out[c]);
   }
   if (s->ev_in) cudaEventDestroy(s->ev_in);
+  stp::pair_scratch_free(s->pairs);
   for (void* p : s->allocations) cudaFree(p);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -637,6 +639,28 @@ int32_t stp_num_envs(const stp_sim* s) { return s ? s->n : 0; }
 int32_t stp_obs_dim(const stp_sim* s) { return s ? s->obs_dim : 0; }
 int32_t stp_action_dim(const stp_sim* s) { return s ? s->J : 0; }
 int32_t stp_contact_capacity(const stp_sim* s) { return s ? s->cap : 0; }
+
+int stp_detect_inter_agent(stp_sim* s, int32_t capacity, int32_t* count, int32_t* body_a, int32_t* body_b,
+                           double* point, double* normal, double* separation) {
+  if (!s || !count || capacity < 0) return fail(STP_EINVAL, "stp_detect_inter_agent: bad arguments");
+  bool overflow = false;
+  int n = 0;
+  cudaError_t e;
+  if (s->precision == STP_PRECISION_F64)
+    e = stp::detect_pairs<double>(s->pairs, reinterpret_cast<const stp::DevModel<double>*>(s->d_model), s->B,
+                                  reinterpret_cast<const double*>(s->d_state), s->d_origin, s->n, s->W,
+                                  s->cfg.contact_margin, capacity, &n, body_a, body_b, point, normal, separation,
+                                  &overflow, s->stream);
+  else
+    e = stp::detect_pairs<float>(s->pairs, reinterpret_cast<const stp::DevModel<float>*>(s->d_model), s->B,
+                                 reinterpret_cast<const float*>(s->d_state), s->d_origin, s->n, s->W,
+                                 s->cfg.contact_margin, capacity, &n, body_a, body_b, point, normal, separation,
+                                 &overflow, s->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stp_detect_inter_agent");
+  if (overflow) return fail(STP_EINVAL, "stp_detect_inter_agent: candidate buffer overflow");
+  *count = n;
+  return STP_OK;
+}
 void* stp_stream(const stp_sim* s) { return s ? reinterpret_cast<void*>(s->stream) : nullptr; }
 
 int stp_reset(stp_sim* s, const uint8_t* mask, float* obs, void* stream) {

@@ -14,4 +14,13 @@ constexpr int kScratchRows = 55 + 11 * kSpillSlots;
 // (2: plane only; 4 + kSpillSlots overflow rows: terrain boxes, dynamic boxes).
 template <class T>
 cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s);
+
+// Inter-agent contact detection (sim_pairs.cu): the reference's dynamic-pair
+// contacts of every env of a sim, global body indices, reference order.
+struct PairScratch;
+void pair_scratch_free(PairScratch* p);
+template <class T>
+cudaError_t detect_pairs(PairScratch*& scratch, const DevModel<T>* model, int B, const T* state, const double* origin,
+                         int n, int W, double margin, int cap_out, int* count, int32_t* body_a, int32_t* body_b,
+                         double* point, double* normal, double* separation, bool* overflow, cudaStream_t st);
 }  // namespace stp

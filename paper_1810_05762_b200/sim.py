@@ -209,6 +209,20 @@ class VecEnv:
                "get_contacts")
         return out
 
+    def detect_inter_agent(self, capacity: int | None = None):
+        """Inter-agent contacts of the current state (row A7, detect_contacts
+        with inter_agent_collisions, collide.cpp:300-343): global body indices
+        env * B + body, the reference's (a, b) order."""
+        cap = capacity if capacity is not None else 4 * self.n_envs * self.n_bodies
+        out = dict(body_a=np.zeros(cap, np.int32), body_b=np.zeros(cap, np.int32), point=np.zeros((cap, 3)),
+                   normal=np.zeros((cap, 3)), separation=np.zeros(cap))
+        n = np.zeros(1, np.int32)
+        _raise(self.lib.stp_detect_inter_agent(self._h, cap, _ptr(n), _ptr(out["body_a"]), _ptr(out["body_b"]),
+                                               _ptr(out["point"]), _ptr(out["normal"]), _ptr(out["separation"])),
+               "detect_inter_agent")
+        k = min(int(n[0]), cap)
+        return {key: v[:k] for key, v in out.items()}
+
     def contacts(self, env: int) -> list[Contact]:
         a = self.contact_arrays()
         n = min(int(a["count"][env]), self.contact_capacity)

@@ -96,3 +96,21 @@ def test_f32_restatement_envelope():
     dx, dv = np.concatenate(dx), np.concatenate(dv)
     assert np.percentile(dx, 99) <= 1e-4 and dx.max() <= 5e-3
     assert np.median(dv) <= 2e-3 and np.percentile(dv, 99) <= 1e-1
+
+
+@pytest.mark.skipif(not oracle.available("reference"), reason="compiled reference not built")
+def test_reference_inter_agent_hook_kat():
+    """orc_ref_detect (the checker of the GPU inter-agent detection) reproduces
+    test_physics.cpp:137-149 on the compiled reference: two single-sphere
+    agents 0.6 m apart -> one inter-agent contact, separation -0.4."""
+    import scenes as S
+    cfg = abi.default_step_config()
+    cfg.contact_margin = 0.0
+    sc = S.sphere_scene(5.0)
+    o = oracle.OracleEnv(sc.build(), S.quiet_task(), cfg, 2, kind="reference")
+    st = np.stack([sc.state(), sc.state()])
+    st[1, 0, 0] += 0.6
+    o.set_state(st)
+    c = o.ref_detect_contacts()
+    assert list(zip(c["body_a"].tolist(), c["body_b"].tolist())) == [(0, 1)]
+    assert abs(c["separation"][0] + 0.4) <= 1e-12
