@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define STP_ABI_VERSION 1
+#define STP_ABI_VERSION 2
 #define STP_MAX_BODIES 32
 #define STP_MAX_JOINTS 31
 #define STP_MAX_FEET 4
@@ -154,6 +154,9 @@ typedef struct stp_task {
   double reset_noise;     /* +-0.05 uniform on every initial DoF */
   int32_t auto_reset;     /* reset done envs inside stp_step */
   int32_t height_map;     /* append the 15x11 height map (HFH terrain) */
+  int32_t inter_agent_collisions; /* Scene::inter_agent_collisions (scene.hpp), set for the
+                                     HFH tasks by reset: contacts between
+                                     agents merge their envs into one island */
 } stp_task;
 
 typedef struct stp_sim stp_sim;

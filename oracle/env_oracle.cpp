@@ -291,9 +291,90 @@ struct Restated {
   }
 };
 
+// closest points between segments (collide.cpp:219-249, Ericson)
+void seg_closest(const V<double>& p1, const V<double>& q1, const V<double>& p2, const V<double>& q2,
+                 V<double>& c1, V<double>& c2) {
+  const V<double> d1 = q1 - p1, d2 = q2 - p2, r = p1 - p2;
+  const double a = d1.dot(d1), e = d2.dot(d2), f = d2.dot(r);
+  auto cl = [](double v) { return std::min(std::max(v, 0.0), 1.0); };
+  double s = 0, t = 0;
+  if (a <= 1e-12 && e <= 1e-12) {
+  } else if (a <= 1e-12) {
+    t = cl(f / e);
+  } else {
+    const double c = d1.dot(r);
+    if (e <= 1e-12) {
+      s = cl(-c / a);
+    } else {
+      const double b = d1.dot(d2), den = a * e - b * b;
+      if (den > 1e-12) s = cl((b * f - c * e) / den);
+      t = (b * s + f) / e;
+      if (t < 0) {
+        t = 0;
+        s = cl(-c / a);
+      } else if (t > 1) {
+        t = 1;
+        s = cl((b - c) / a);
+      }
+    }
+  }
+  c1 = p1 + d1 * s;
+  c2 = p2 + d2 * t;
+}
+
+// The restatement solves every env as its own island.  With
+// Scene::inter_agent_collisions on (HFH) that is the reference's
+// behaviour only while no two agents touch (collide.cpp:300-343 finds no
+// pair): check exactly that, and fail loudly otherwise (contact-merged
+// islands are checked against the compiled reference instead).
+void require_no_inter_agent_contacts(const World& w) {
+  Model<double> m;
+  m.load(w.model);
+  const double margin = w.cfg.contact_margin;
+  const int B = w.nb();
+  std::vector<Shape<double>> sh(size_t(w.n) * B);
+  std::vector<char> ok(size_t(w.n) * B);
+  std::vector<V<double>> lo(w.n, V<double>{1e300, 1e300, 1e300}), hi(w.n, V<double>{-1e300, -1e300, -1e300});
+  for (int e = 0; e < w.n; ++e)
+    for (int b = 0; b < B; ++b) {
+      const double* s = w.state.data() + (size_t(e) * B + b) * STP_STATE_STRIDE;
+      Body<double> st;
+      st.x = {s[0], s[1], s[2]};
+      st.q = {s[3], s[4], s[5], s[6]};
+      const size_t i = size_t(e) * B + b;
+      sh[i] = world_shape(m, b, st);
+      ok[i] = !m.is_static[b] && m.shape[b] != STP_BOX;
+      if (ok[i]) {
+        lo[e] = {std::min(lo[e].x, sh[i].lo.x), std::min(lo[e].y, sh[i].lo.y), std::min(lo[e].z, sh[i].lo.z)};
+        hi[e] = {std::max(hi[e].x, sh[i].hi.x), std::max(hi[e].y, sh[i].hi.y), std::max(hi[e].z, sh[i].hi.z)};
+      }
+    }
+  auto over = [&](const V<double>& al, const V<double>& ah, const V<double>& bl, const V<double>& bh) {
+    return al.x <= bh.x + margin && bl.x <= ah.x + margin && al.y <= bh.y + margin && bl.y <= ah.y + margin &&
+           al.z <= bh.z + margin && bl.z <= ah.z + margin;  // aabb_overlap, collide.cpp:80-84
+  };
+  for (int e1 = 0; e1 < w.n; ++e1)
+    for (int e2 = e1 + 1; e2 < w.n; ++e2) {
+      if (!over(lo[e1], hi[e1], lo[e2], hi[e2])) continue;
+      for (int a = 0; a < B; ++a)
+        for (int b = 0; b < B; ++b) {
+          const Shape<double>& A = sh[size_t(e1) * B + a];
+          const Shape<double>& Bs = sh[size_t(e2) * B + b];
+          if (!ok[size_t(e1) * B + a] || !ok[size_t(e2) * B + b] || !over(A.lo, A.hi, Bs.lo, Bs.hi)) continue;
+          V<double> ca, cb;
+          seg_closest(A.p0, A.p1, Bs.p0, Bs.p1, ca, cb);
+          const V<double> d = ca - cb;
+          if (d.norm() - A.r - Bs.r < margin)
+            throw std::runtime_error("restated physics: agents " + std::to_string(e1) + " and " + std::to_string(e2) +
+                                     " touch; contact-merged islands are only in the compiled reference backend");
+        }
+    }
+}
+
 struct RestatedPhysics : PhysicsBackend {
   const char* name() const override { return "restatement"; }
   void step(World& w, const double* torques) override {
+    if (w.task.inter_agent_collisions) require_no_inter_agent_contacts(w);
     const int nt = std::max(1, std::min(w.nthreads, w.n));
     auto body = [&](int e0, int e1) {
       if (w.precision == 0) Restated<float>::run(w, torques, e0, e1);

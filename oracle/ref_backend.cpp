@@ -35,7 +35,7 @@ struct ReferencePhysics : PhysicsBackend {
     scene = ph::Scene{};
     scene.has_ground_plane = w.cfg.has_ground_plane != 0;
     scene.gravity = {w.cfg.gravity[0], w.cfg.gravity[1], w.cfg.gravity[2]};
-    scene.inter_agent_collisions = false;
+    scene.inter_agent_collisions = w.task.inter_agent_collisions != 0;  // HFH
     for (int e = 0; e < w.n; ++e) {
       for (int b = 0; b < B; ++b) {
         const stp_body& d = m.bodies[b];
@@ -123,7 +123,9 @@ struct ReferencePhysics : PhysicsBackend {
       const int e = sc.geom.body_a / B;
       ContactRec r{};
       r.a = sc.geom.body_a - e * B;
-      r.b = sc.geom.body_b < 0 ? -1 : sc.geom.body_b - e * B;
+      // static -1; a body of another agent (inter-agent contact, listed with
+      // body_a's env) as its global index env * B + body (always >= B)
+      r.b = sc.geom.body_b < 0 ? -1 : (sc.geom.body_b / B == e ? sc.geom.body_b - e * B : sc.geom.body_b);
       r.p[0] = sc.geom.point.x; r.p[1] = sc.geom.point.y; r.p[2] = sc.geom.point.z;
       r.n[0] = sc.geom.normal.x; r.n[1] = sc.geom.normal.y; r.n[2] = sc.geom.normal.z;
       r.sep = sc.geom.separation;

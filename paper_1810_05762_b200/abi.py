@@ -122,6 +122,7 @@ class Task(C.Structure):
         ("reset_noise", C.c_double),
         ("auto_reset", C.c_int32),
         ("height_map", C.c_int32),
+        ("inter_agent_collisions", C.c_int32),
     ]
 
 

@@ -314,6 +314,7 @@ int stp_default_task(int32_t kind, stp_task* t) {
     t->target_refresh = 200;
     t->spacing = 2.0;
     t->height_map = kind == STP_TASK_HFH_TERRAIN;
+    t->inter_agent_collisions = kind == STP_TASK_HFH || kind == STP_TASK_HFH_TERRAIN;
   } else {
     t->fall_grace = 0;
     t->target_refresh = 0;         // fixed target 1000 m ahead

@@ -353,33 +353,45 @@ stp::KArgs<T> make_args(stp_sim* s, int mode) {
   return a;
 }
 
+template <class T>
+int launch_t(stp_sim* s, int mode, const float* torques, const float* actions, float* obs, float* reward,
+             uint8_t* done, const uint8_t* mask, cudaStream_t st, int e_begin, int e_end) {
+  auto a = make_args<T>(s, mode);
+  a.e_begin = e_begin;
+  if (e_end >= 0) a.n = e_end;
+  a.torques = torques;
+  a.actions = actions;
+  a.obs = obs;
+  a.reward = reward;
+  a.done = done;
+  a.reset_mask = mask;
+  if (mode != 2 && s->task.inter_agent_collisions && s->n > 1) {
+    // Scene::inter_agent_collisions (HFH): contacts between
+    // agents of the pre-step state (collide.cpp:300-343) merge envs into
+    // islands solved together (solver.cpp:458-502); all on the device
+    stp::IslandView v{};
+    cudaError_t e = stp::prepare_islands<T>(s->pairs, reinterpret_cast<const stp::DevModel<T>*>(s->d_model), s->B,
+                                            reinterpret_cast<const T*>(s->d_state), s->d_origin, s->n, s->W,
+                                            s->cfg.contact_margin, &v, st);
+    if (e != cudaSuccess) return cuda_fail(e, "inter-agent island preparation");
+    a.merged = v.merged;
+    a.isl_members = v.isl_members;
+    a.isl_count = v.isl_count;
+    a.isl_err = v.err;
+    a.xslots = v.xslots;
+    a.xcount = v.xcount;
+  }
+  const cudaError_t e = stp::launch_env_step<T>(a, s->W, s->cpb, st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_env_step launch");
+  return STP_OK;
+}
+
 int launch(stp_sim* s, int mode, const float* torques, const float* actions, float* obs, float* reward,
            uint8_t* done, const uint8_t* mask, cudaStream_t st, int e_begin = 0, int e_end = -1) {
-  cudaError_t e;
-  if (s->precision == STP_PRECISION_F64) {
-    auto a = make_args<double>(s, mode);
-    a.e_begin = e_begin;
-    if (e_end >= 0) a.n = e_end;
-    a.torques = torques;
-    a.actions = actions;
-    a.obs = obs;
-    a.reward = reward;
-    a.done = done;
-    a.reset_mask = mask;
-    e = stp::launch_env_step<double>(a, s->W, s->cpb, st);
-  } else {
-    auto a = make_args<float>(s, mode);
-    a.e_begin = e_begin;
-    if (e_end >= 0) a.n = e_end;
-    a.torques = torques;
-    a.actions = actions;
-    a.obs = obs;
-    a.reward = reward;
-    a.done = done;
-    a.reset_mask = mask;
-    e = stp::launch_env_step<float>(a, s->W, s->cpb, st);
-  }
-  if (e != cudaSuccess) return cuda_fail(e, "k_env_step launch");
+  const int rc = s->precision == STP_PRECISION_F64
+                     ? launch_t<double>(s, mode, torques, actions, obs, reward, done, mask, st, e_begin, e_end)
+                     : launch_t<float>(s, mode, torques, actions, obs, reward, done, mask, st, e_begin, e_end);
+  if (rc) return rc;
   if (mode != 2) s->loads_pending = false;
   return STP_OK;
 }
@@ -684,7 +696,10 @@ int stp_step_host(stp_sim* s, const float* actions, float* obs, float* reward, u
   const size_t N = size_t(s->n);
   // up to 4 chunks of >= 1024 envs (measured on B200 at 4096 envs: 4 chunks
   // 0.234 ms, 8 chunks 0.243 ms, one launch 0.259 ms per call)
-  const int C = int(std::min<size_t>(stp_sim::kChunks, std::max<size_t>(1, N / kMinChunk)));
+  // (envs coupled by inter-agent contacts are stepped as one launch)
+  const int C = s->task.inter_agent_collisions
+                    ? 1
+                    : int(std::min<size_t>(stp_sim::kChunks, std::max<size_t>(1, N / kMinChunk)));
   if (C == 1) {
     CK(cudaMemcpyAsync(s->d_act, actions, N * s->J * sizeof(float), cudaMemcpyHostToDevice, s->stream));
     int rc = launch(s, 1, nullptr, s->d_act, obs ? s->d_obs : nullptr, reward ? s->d_rew : nullptr,

@@ -24,6 +24,21 @@ namespace stp {
 
 constexpr int kCData = 11;  // recorded contact: point3 normal3 sep pn pt3 (double)
 
+// One inter-agent contact seen from one of its bodies (collide.cpp:251-266,
+// rows solver.cpp:176-210): the reference's row Jacobians are
+// j_own = role * (n, r_own x n), j_partner = -role * (n, r_partner x n)
+// (role +1: this body is body_a, -1: body_b), likewise for the tangents.
+struct XSlot {
+  long long key;  // a * (n * B) + b: the contact's place in the reference's (a, b) order
+  int partner;    // global body index (env * B + body) of the other body
+  int role;       // +1 body_a, -1 body_b
+  double r_own[3], r_part[3];  // contact point minus each body's position (pre-step)
+  double normal[3];            // from body_b to body_a
+  double sep;
+};
+constexpr int kXSlots = 4;      // cross contacts per body
+constexpr int kIslandMax = 8;   // envs per merged island (one warp each)
+
 template <class T>
 struct KArgs {
   const DevModel<T>* model;
@@ -66,6 +81,14 @@ struct KArgs {
   const int* cell_start;  // [nx*ny + 1]
   const int* cell_list;   // box indices, ascending within a cell
   const int4* box_cells;  // per box: first/last cell (x0, y0, x1, y1)
+  // inter-agent contacts (Scene::inter_agent_collisions): envs
+  // linked by one are stepped together by the island launch (sim_pairs.cu)
+  const uint8_t* merged;      // [n] 1: env belongs to a contact-merged island
+  const int* isl_members;     // [n / 2][kIslandMax] member envs (unordered; -1 unused)
+  const int* isl_count;       // number of merged islands
+  const XSlot* xslots;        // [n * B][kXSlots] cross contacts of each body
+  const int* xcount;          // [n * B]
+  const int* isl_err;         // preparation overflow bits (see IslandView)
 };
 
 enum { C_FRAME = 0, C_FLAG = 1, C_FALL = 2, C_NEXTP = 3, C_EPISODE = 4, C_FLAGDRAW = 5, C_PERTDRAW = 6 };

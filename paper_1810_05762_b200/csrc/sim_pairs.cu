@@ -7,14 +7,15 @@
 // each (closest_segment_segment :219-249, collide_dynamic_pair :251-266).  The
 // grid is only a broadphase: any overlapping pair shares a cell, so the pair
 // set is exactly "different agents, overlapping AABBs".  Here:
-//   K_a  per env: world shapes of its bodies in double (env origin + local
-//        pose, world_shape :38-78) and the env's AABB (union);
-//   sort envs by AABB x-min (cub radix sort), then
-//   K_b  sweep: each env scans the envs after it in x order while their x-min
-//        is within reach and keeps the pairs whose env AABBs overlap;
+//   K_a  one warp per env: world shapes of its bodies in double (env origin +
+//        local pose, world_shape :38-78), the env's AABB, and the env filed in
+//        a hashed 2-D grid by its AABB centre;
+//   K_b  per env: the grid cells within reach -> env pairs whose AABBs
+//        overlap within the margin;
 //   K_c  one warp per candidate env pair: all body pairs, the reference's AABB
-//        test and narrow phase, emitted with key (a, b);
-//   sort contacts by key (cub) -> the reference's order.
+//        test and narrow phase.
+// The detection entry sorts the contacts by (a, b) (cub) for its output; the
+// step path writes them into per-body slots (sorted there) and forms islands.
 // Body indices are global within the sim: env * B + body.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
@@ -30,20 +31,44 @@ namespace {
 
 struct WShape {  // world shape of one body (double), collide.cpp:27-36
   double p0[3], p1[3], lo[3], hi[3];
+  double x[3];  // body position (row lever arms, solver.cpp:180-181)
   double r;
   int ok;  // dynamic sphere / capsule (boxes never pair, :255)
 };
 
+__device__ __forceinline__ bool box_overlap(const double* a, const double* b, double m) {
+  // a, b: lo[3], hi[3]; the reference's aabb_overlap with margin m
+  return a[0] <= b[3] + m && b[0] <= a[3] + m && a[1] <= b[4] + m && b[1] <= a[4] + m && a[2] <= b[5] + m &&
+         b[2] <= a[5] + m;
+}
+
+// Broadphase over envs on a hashed 2-D grid (cell kCell m): one warp per env
+// forms its bodies' world shapes (lane = body) and the env AABB by warp
+// min / max, and files the env under the cell of its AABB centre; the query
+// visits the cells within reach (from the largest env extent of the step) and
+// keeps the pairs whose env AABBs overlap within the margin.  Envs that do
+// not fit their bin go to an overflow list every query also scans, so the
+// candidate set is always complete.
+constexpr double kCell = 3.0;
+constexpr int kBinCap = 8;
+
+__device__ __forceinline__ int cell_of(double v) { return int(floor(v / kCell)); }
+__device__ __forceinline__ unsigned cell_hash(int cx, int cy, unsigned hmask) {
+  return (unsigned(cx) * 73856093u ^ unsigned(cy) * 19349663u) & hmask;
+}
+
 template <class T>
-__global__ void k_world_shapes(const DevModel<T>* __restrict__ Mp, const T* __restrict__ state,
-                               const double* __restrict__ origin, int n, int W, double margin, WShape* __restrict__ ws,
-                               double* __restrict__ env_box, float* __restrict__ key, int* __restrict__ idx) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_shapes_warp(const DevModel<T>* __restrict__ Mp, const T* __restrict__ state,
+                              const double* __restrict__ origin, int n, int W, WShape* __restrict__ ws,
+                              double* __restrict__ env_box, int2* __restrict__ env_cell, int* __restrict__ bin_count,
+                              int* __restrict__ bins, unsigned hmask, int* __restrict__ ovf, int* __restrict__ n_ovf,
+                              int* __restrict__ max_ext_bits) {
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, b = threadIdx.x & 31;
   if (e >= n) return;
   const DevModel<T>& M = *Mp;
   const int B = M.nb;
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int b = 0; b < B; ++b) {
+  if (b < B) {
     WShape s{};
     const size_t sb = size_t(e) * kStateFields * W + b;
     auto st = [&](int f) { return double(state[sb + size_t(f) * W]); };
@@ -62,6 +87,9 @@ __global__ void k_world_shapes(const DevModel<T>* __restrict__ Mp, const T* __re
     }
     s.ok = !M.is_static[b] && M.shape[b] != STP_BOX;
     s.r = r;
+    s.x[0] = x.x;
+    s.x[1] = x.y;
+    s.x[2] = x.z;
     const double a0[3] = {p0.x, p0.y, p0.z}, a1[3] = {p1.x, p1.y, p1.z};
     for (int k = 0; k < 3; ++k) {
       s.p0[k] = a0[k];
@@ -69,46 +97,71 @@ __global__ void k_world_shapes(const DevModel<T>* __restrict__ Mp, const T* __re
       s.lo[k] = fmin(a0[k], a1[k]) - r;
       s.hi[k] = fmax(a0[k], a1[k]) + r;
       if (s.ok) {
-        lo[k] = fmin(lo[k], s.lo[k]);
-        hi[k] = fmax(hi[k], s.hi[k]);
+        lo[k] = s.lo[k];
+        hi[k] = s.hi[k];
       }
     }
     ws[size_t(e) * B + b] = s;
   }
-  for (int k = 0; k < 3; ++k) {
-    env_box[6 * e + k] = lo[k];
-    env_box[6 * e + 3 + k] = hi[k];
+  for (int off = 16; off > 0; off >>= 1)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], off));
+      hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], off));
+    }
+  if (b == 0) {
+    for (int k = 0; k < 3; ++k) {
+      env_box[6 * e + k] = lo[k];
+      env_box[6 * e + 3 + k] = hi[k];
+    }
+    if (!(lo[0] <= hi[0])) {  // no dynamic sphere / capsule: never pairs
+      env_cell[e] = make_int2(INT_MIN, INT_MIN);
+      return;
+    }
+    const int cx = cell_of(0.5 * (lo[0] + hi[0])), cy = cell_of(0.5 * (lo[1] + hi[1]));
+    env_cell[e] = make_int2(cx, cy);
+    const float ext = float(fmax(hi[0] - lo[0], hi[1] - lo[1]));
+    atomicMax(max_ext_bits, __float_as_int(__fmul_ru(ext, 1.0f)));  // positive floats order as ints
+    const unsigned h = cell_hash(cx, cy, hmask);
+    const int slot = atomicAdd(&bin_count[h], 1);
+    if (slot < kBinCap) bins[h * kBinCap + slot] = e;
+    else ovf[atomicAdd(n_ovf, 1)] = e;
   }
-  // sort key: x-min rounded down to float (a conservative lower bound)
-  float kx = __double2float_rd(lo[0] - margin);
-  if (!(lo[0] <= hi[0])) kx = INFINITY;  // no dynamic sphere/capsule body
-  key[e] = kx;
-  idx[e] = e;
 }
 
-__device__ __forceinline__ bool box_overlap(const double* a, const double* b, double m) {
-  // a, b: lo[3], hi[3]; the reference's aabb_overlap with margin m
-  return a[0] <= b[3] + m && b[0] <= a[3] + m && a[1] <= b[4] + m && b[1] <= a[4] + m && a[2] <= b[5] + m &&
-         b[2] <= a[5] + m;
-}
-
-__global__ void k_env_pairs(int n, const float* __restrict__ skey, const int* __restrict__ sidx,
-                            const double* __restrict__ env_box, double margin, int2* __restrict__ pairs, int cap,
+__global__ void k_env_query(int n, const double* __restrict__ env_box, const int2* __restrict__ env_cell,
+                            const int* __restrict__ bin_count, const int* __restrict__ bins, unsigned hmask,
+                            const int* __restrict__ ovf, const int* __restrict__ n_ovf,
+                            const int* __restrict__ max_ext_bits, double margin, int2* __restrict__ pairs, int cap,
                             int* __restrict__ n_pairs) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const int i = sidx[p];
+  // one warp per env; lanes over (cell, bin slot) candidates
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int2 ci = env_cell[i];
+  if (ci.x == INT_MIN) return;
   const double* bi = env_box + 6 * i;
-  if (!(bi[0] <= bi[3])) return;
-  const double reach = bi[3] + 2.0 * margin;  // x-min of a partner is <= hi.x + margin (key carries -margin)
-  for (int q = p + 1; q < n; ++q) {
-    if (double(skey[q]) > reach) break;
-    const int j = sidx[q];
+  // centres of overlapping envs differ by <= (ext_i + ext_max) / 2 + margin
+  const double ext_i = fmax(bi[3] - bi[0], bi[4] - bi[1]);
+  const double reach = 0.5 * (ext_i + double(__int_as_float(*max_ext_bits))) + margin;
+  const int rc = int(floor(reach / kCell)) + 1;  // |x_i - x_j| <= R  =>  |cell_i - cell_j| <= floor(R / C) + 1
+  const int side = 2 * rc + 1;
+  auto test = [&](int j) {
+    if (j <= i) return;
     if (box_overlap(bi, env_box + 6 * j, margin)) {
       const int slot = atomicAdd(n_pairs, 1);
-      if (slot < cap) pairs[slot] = make_int2(min(i, j), max(i, j));
+      if (slot < cap) pairs[slot] = make_int2(i, j);
     }
+  };
+  for (int u = lane; u < side * side * kBinCap; u += 32) {
+    const int c = u / kBinCap, k = u % kBinCap;
+    const int cx = ci.x + c % side - rc, cy = ci.y + c / side - rc;
+    const unsigned h = cell_hash(cx, cy, hmask);
+    if (k >= min(bin_count[h], kBinCap)) continue;
+    const int j = bins[h * kBinCap + k];
+    const int2 cj = env_cell[j];
+    if (cj.x == cx && cj.y == cy) test(j);  // hash collisions: each env once, in its own cell
   }
+  const int no = *n_ovf;
+  for (int k = lane; k < no; k += 32) test(ovf[k]);
 }
 
 // closest points between segments p1q1 and p2q2 (Ericson; collide.cpp:219-249)
@@ -198,6 +251,131 @@ __global__ void k_narrow(const int2* __restrict__ pairs, const int* __restrict__
   }
 }
 
+// Step path: the same narrow phase, written straight into each body's cross
+// contact slots (both sides) plus the env edge of every contact; persistent
+// warps loop over the device-counted candidate pairs (no host round trip).
+__global__ void k_narrow_slots(const int2* __restrict__ pairs, const int* __restrict__ n_pairs_p, int pair_cap,
+                               int B, long long NB, const WShape* __restrict__ ws, double margin,
+                               XSlot* __restrict__ xslots, int* __restrict__ xcount, int2* __restrict__ edges,
+                               int edge_cap, int* __restrict__ n_edges, int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int np = min(*n_pairs_p, pair_cap);
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < np; w += nwarps) {
+    const int2 pr = pairs[w];
+    for (int u = lane; u < B * B; u += 32) {
+      const int ba = u / B, bb = u % B;
+      const WShape& A = ws[size_t(pr.x) * B + ba];
+      const WShape& Bs = ws[size_t(pr.y) * B + bb];
+      if (!A.ok || !Bs.ok) continue;
+      const double la[6] = {A.lo[0], A.lo[1], A.lo[2], A.hi[0], A.hi[1], A.hi[2]};
+      const double lb[6] = {Bs.lo[0], Bs.lo[1], Bs.lo[2], Bs.hi[0], Bs.hi[1], Bs.hi[2]};
+      if (!box_overlap(la, lb, margin)) continue;
+      double ca[3], cb[3];
+      seg_seg(A.p0, A.p1, Bs.p0, Bs.p1, ca, cb);
+      const double dl[3] = {ca[0] - cb[0], ca[1] - cb[1], ca[2] - cb[2]};
+      const double dist = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      double nrm[3] = {0.0, 0.0, 1.0};
+      if (dist > 1e-9) {
+        for (int k = 0; k < 3; ++k) nrm[k] = dl[k] / dist;
+      }
+      const double sep = dist - A.r - Bs.r;
+      if (!(sep < margin)) continue;
+      const long long ga = (long long)pr.x * B + ba, gb = (long long)pr.y * B + bb;
+      const double off = Bs.r + 0.5 * (dist - A.r - Bs.r);
+      double pt[3], xa[3], xb[3];
+      for (int k = 0; k < 3; ++k) {
+        pt[k] = cb[k] + nrm[k] * off;
+        xa[k] = A.x[k];
+        xb[k] = Bs.x[k];
+      }
+      for (int side = 0; side < 2; ++side) {
+        const long long me = side == 0 ? ga : gb;
+        const int slot = atomicAdd(&xcount[me], 1);
+        if (slot >= kXSlots) {
+          atomicOr(err, 1);
+          continue;
+        }
+        XSlot x;
+        x.key = ga * NB + gb;
+        x.partner = int(side == 0 ? gb : ga);
+        x.role = side == 0 ? 1 : -1;
+        for (int k = 0; k < 3; ++k) {
+          x.r_own[k] = pt[k] - (side == 0 ? xa[k] : xb[k]);
+          x.r_part[k] = pt[k] - (side == 0 ? xb[k] : xa[k]);
+          x.normal[k] = nrm[k];
+        }
+        x.sep = sep;
+        xslots[me * kXSlots + slot] = x;
+      }
+      const int ei = atomicAdd(n_edges, 1);
+      if (ei < edge_cap) edges[ei] = pr;
+      else atomicOr(err, 4);
+    }
+  }
+}
+
+// Islands of envs (solver.cpp:458-482 restricted to what couples envs): label
+// propagation over the contact edges, then island lists.  One CTA.
+__global__ void k_islands(int n, const int2* __restrict__ edges, const int* __restrict__ n_edges_p, int edge_cap,
+                          int* __restrict__ label, uint8_t* __restrict__ merged, int* __restrict__ isl_of,
+                          int* __restrict__ isl_size, int* __restrict__ isl_members, int* __restrict__ isl_count,
+                          int* __restrict__ err) {
+  __shared__ int changed;
+  const int ne = min(*n_edges_p, edge_cap);
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    label[e] = e;
+    merged[e] = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+    merged[edges[i].x] = 1;
+    merged[edges[i].y] = 1;
+  }
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) changed = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+      const int a = edges[i].x, b = edges[i].y;
+      const int la = label[a], lb = label[b];
+      if (la != lb) {
+        const int m = min(la, lb);
+        atomicMin(&label[a], m);
+        atomicMin(&label[b], m);
+        atomicMin(&label[max(la, lb)], m);
+        changed = 1;
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {  // pointer jumping
+      const int l = label[e], ll = label[l];
+      if (ll < l) {
+        atomicMin(&label[e], ll);
+        changed = 1;
+      }
+    }
+    __syncthreads();
+    if (!changed) break;
+  }
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    if (merged[e] && label[e] == e) {
+      const int i = atomicAdd(isl_count, 1);
+      isl_of[e] = i;
+      isl_size[i] = 0;
+      for (int k = 0; k < kIslandMax; ++k) isl_members[i * kIslandMax + k] = -1;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    if (!merged[e]) continue;
+    const int i = isl_of[label[e]];
+    const int pos = atomicAdd(&isl_size[i], 1);
+    if (pos < kIslandMax) isl_members[i * kIslandMax + pos] = e;
+    else atomicOr(err, 2);
+  }
+}
+
 __global__ void k_keys(const PairContact* __restrict__ c, const int* __restrict__ n_p, int cap,
                        unsigned long long* __restrict__ keys, int* __restrict__ idx) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -214,23 +392,54 @@ struct PairScratch {
   size_t n_cap = 0, pair_cap = 0, c_cap = 0, tmp_bytes = 0;
   WShape* ws = nullptr;
   double* env_box = nullptr;
-  float *key = nullptr, *skey = nullptr;
-  int *idx = nullptr, *sidx = nullptr;
   int2* pairs = nullptr;
   int* counters = nullptr;  // [0] env pairs, [1] contacts
   PairContact* cont = nullptr;
   unsigned long long *ckey = nullptr, *sckey = nullptr;
   int *cidx = nullptr, *scidx = nullptr;
   void* tmp = nullptr;
+  // hashed env grid
+  unsigned hmask = 0;
+  int2* env_cell = nullptr;
+  int *bin_count = nullptr, *bins = nullptr, *ovf = nullptr, *gcnt = nullptr;  // gcnt: [0] overflow, [1] max extent
+  // step path (prepare_islands)
+  size_t isl_n = 0;
+  XSlot* xslots = nullptr;
+  int* xcount = nullptr;
+  int2* edges = nullptr;
+  int* icnt = nullptr;  // [0] edges, [1] islands, [2] error bits
+  int *label = nullptr, *isl_of = nullptr, *isl_size = nullptr, *isl_members = nullptr;
+  uint8_t* merged = nullptr;
 };
 
 void pair_scratch_free(PairScratch* p) {
   if (!p) return;
-  for (void* q : {(void*)p->ws, (void*)p->env_box, (void*)p->key, (void*)p->skey, (void*)p->idx, (void*)p->sidx,
-                  (void*)p->pairs, (void*)p->counters, (void*)p->cont, (void*)p->ckey, (void*)p->sckey,
-                  (void*)p->cidx, (void*)p->scidx, p->tmp})
+  for (void* q : {(void*)p->ws, (void*)p->env_box, (void*)p->pairs, (void*)p->counters, (void*)p->cont, (void*)p->ckey, (void*)p->sckey,
+                  (void*)p->cidx, (void*)p->scidx, p->tmp, (void*)p->xslots, (void*)p->xcount, (void*)p->edges,
+                  (void*)p->icnt, (void*)p->label, (void*)p->isl_of, (void*)p->isl_size, (void*)p->isl_members,
+                  (void*)p->merged, (void*)p->env_cell, (void*)p->bin_count, (void*)p->bins, (void*)p->ovf,
+                  (void*)p->gcnt})
     if (q) cudaFree(q);
   delete p;
+}
+
+// candidate env pairs (i < j, env AABBs overlapping within the margin) of the
+// current state into P->pairs / P->counters[0]; world shapes into P->ws
+template <class T>
+static cudaError_t broadphase(PairScratch* P, const DevModel<T>* model, const T* state, const double* origin, int n,
+                              int W, double margin, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(P->bin_count, 0, sizeof(int) * (P->hmask + 1), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(P->gcnt, 0, sizeof(int) * 2, st);
+  if (e != cudaSuccess) return e;
+  k_shapes_warp<T><<<(n * 32 + 127) / 128, 128, 0, st>>>(model, state, origin, n, W, P->ws, P->env_box, P->env_cell,
+                                                         P->bin_count, P->bins, P->hmask, P->ovf, P->gcnt,
+                                                         P->gcnt + 1);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_env_query<<<(n * 32 + 127) / 128, 128, 0, st>>>(n, P->env_box, P->env_cell, P->bin_count, P->bins, P->hmask, P->ovf,
+                                               P->gcnt, P->gcnt + 1, margin, P->pairs, int(P->pair_cap),
+                                               P->counters);
+  return cudaGetLastError();
 }
 
 template <class T>
@@ -254,10 +463,6 @@ cudaError_t detect_pairs(PairScratch*& P, const DevModel<T>* model, int B, const
     P->c_cap = c_cap;
     STP_CK(cudaMalloc(&P->ws, sizeof(WShape) * size_t(n) * B));
     STP_CK(cudaMalloc(&P->env_box, sizeof(double) * 6 * n));
-    STP_CK(cudaMalloc(&P->key, sizeof(float) * n));
-    STP_CK(cudaMalloc(&P->skey, sizeof(float) * n));
-    STP_CK(cudaMalloc(&P->idx, sizeof(int) * n));
-    STP_CK(cudaMalloc(&P->sidx, sizeof(int) * n));
     STP_CK(cudaMalloc(&P->pairs, sizeof(int2) * pair_cap));
     STP_CK(cudaMalloc(&P->counters, sizeof(int) * 2));
     STP_CK(cudaMalloc(&P->cont, sizeof(PairContact) * c_cap));
@@ -265,21 +470,21 @@ cudaError_t detect_pairs(PairScratch*& P, const DevModel<T>* model, int B, const
     STP_CK(cudaMalloc(&P->sckey, sizeof(unsigned long long) * c_cap));
     STP_CK(cudaMalloc(&P->cidx, sizeof(int) * c_cap));
     STP_CK(cudaMalloc(&P->scidx, sizeof(int) * c_cap));
-    size_t t1 = 0, t2 = 0;
-    STP_CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, P->key, P->skey, P->idx, P->sidx, n));
+    size_t t2 = 0;
     STP_CK(cub::DeviceRadixSort::SortPairs(nullptr, t2, P->ckey, P->sckey, P->cidx, P->scidx, int(c_cap)));
-    P->tmp_bytes = t1 > t2 ? t1 : t2;
+    P->tmp_bytes = t2;
     STP_CK(cudaMalloc(&P->tmp, P->tmp_bytes));
+    unsigned H = 1024;
+    while (H < 2u * unsigned(n)) H <<= 1;
+    P->hmask = H - 1;
+    STP_CK(cudaMalloc(&P->env_cell, sizeof(int2) * n));
+    STP_CK(cudaMalloc(&P->bin_count, sizeof(int) * H));
+    STP_CK(cudaMalloc(&P->bins, sizeof(int) * H * kBinCap));
+    STP_CK(cudaMalloc(&P->ovf, sizeof(int) * n));
+    STP_CK(cudaMalloc(&P->gcnt, sizeof(int) * 2));
   }
   STP_CK(cudaMemsetAsync(P->counters, 0, sizeof(int) * 2, st));
-  k_world_shapes<T><<<(n + 127) / 128, 128, 0, st>>>(model, state, origin, n, W, margin, P->ws, P->env_box, P->key,
-                                                     P->idx);
-  STP_CK(cudaGetLastError());
-  size_t tb = P->tmp_bytes;
-  STP_CK(cub::DeviceRadixSort::SortPairs(P->tmp, tb, P->key, P->skey, P->idx, P->sidx, n, 0, 32, st));
-  k_env_pairs<<<(n + 127) / 128, 128, 0, st>>>(n, P->skey, P->sidx, P->env_box, margin, P->pairs, int(pair_cap),
-                                               P->counters);
-  STP_CK(cudaGetLastError());
+  STP_CK(broadphase<T>(P, model, state, origin, n, W, margin, st));
   int h_cnt[2] = {0, 0};
   STP_CK(cudaMemcpyAsync(h_cnt, P->counters, sizeof(int), cudaMemcpyDeviceToHost, st));
   STP_CK(cudaStreamSynchronize(st));
@@ -298,7 +503,7 @@ cudaError_t detect_pairs(PairScratch*& P, const DevModel<T>* model, int B, const
   if (nc == 0) return cudaSuccess;
   k_keys<<<(nc + 127) / 128, 128, 0, st>>>(P->cont, P->counters + 1, int(c_cap), P->ckey, P->cidx);
   STP_CK(cudaGetLastError());
-  tb = P->tmp_bytes;
+  size_t tb = P->tmp_bytes;
   STP_CK(cub::DeviceRadixSort::SortPairs(P->tmp, tb, P->ckey, P->sckey, P->cidx, P->scidx, nc, 0, 64, st));
   // gather to the host in key order
   std::vector<PairContact> hc(nc);
@@ -320,6 +525,67 @@ cudaError_t detect_pairs(PairScratch*& P, const DevModel<T>* model, int B, const
   return cudaSuccess;
 #undef STP_CK
 }
+
+// Device-only preparation of the step's inter-agent coupling: cross contact
+// slots per body, env islands and the merged flags (no host round trip).
+template <class T>
+cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, const T* state, const double* origin,
+                            int n, int W, double margin, IslandView* view, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+#define STP_CK(x)                   \
+  do {                              \
+    e = (x);                        \
+    if (e != cudaSuccess) return e; \
+  } while (0)
+  if (!P) P = new PairScratch();
+  const size_t pair_cap = size_t(n) * 32 + 64;
+  if (P->n_cap < size_t(n) || P->pair_cap < pair_cap) {
+    // (re)build the detection scratch through the detection entry's allocator
+    int cnt = 0;
+    bool ov = false;
+    STP_CK(detect_pairs<T>(P, model, B, state, origin, n, W, margin, 0, &cnt, nullptr, nullptr, nullptr, nullptr,
+                           nullptr, &ov, st));
+  }
+  if (P->isl_n < size_t(n)) {
+    for (void* q : {(void*)P->xslots, (void*)P->xcount, (void*)P->edges, (void*)P->icnt, (void*)P->label,
+                    (void*)P->isl_of, (void*)P->isl_size, (void*)P->isl_members, (void*)P->merged})
+      if (q) cudaFree(q);
+    P->isl_n = n;
+    STP_CK(cudaMalloc(&P->xslots, sizeof(XSlot) * size_t(n) * B * kXSlots));
+    STP_CK(cudaMalloc(&P->xcount, sizeof(int) * size_t(n) * B));
+    STP_CK(cudaMalloc(&P->edges, sizeof(int2) * size_t(n) * B * kXSlots));
+    STP_CK(cudaMalloc(&P->icnt, sizeof(int) * 3));
+    STP_CK(cudaMalloc(&P->label, sizeof(int) * n));
+    STP_CK(cudaMalloc(&P->isl_of, sizeof(int) * n));
+    STP_CK(cudaMalloc(&P->isl_size, sizeof(int) * (n / 2 + 1)));
+    STP_CK(cudaMalloc(&P->isl_members, sizeof(int) * (n / 2 + 1) * kIslandMax));
+    STP_CK(cudaMalloc(&P->merged, n));
+  }
+  const int edge_cap = n * B * kXSlots;
+  STP_CK(cudaMemsetAsync(P->counters, 0, sizeof(int) * 2, st));
+  STP_CK(cudaMemsetAsync(P->icnt, 0, sizeof(int) * 3, st));
+  STP_CK(cudaMemsetAsync(P->xcount, 0, sizeof(int) * size_t(n) * B, st));
+  STP_CK(broadphase<T>(P, model, state, origin, n, W, margin, st));
+  k_narrow_slots<<<148 * 2, 256, 0, st>>>(P->pairs, P->counters, int(P->pair_cap), B, (long long)n * B, P->ws, margin,
+                                          P->xslots, P->xcount, P->edges, edge_cap, P->icnt, P->icnt + 2);
+  STP_CK(cudaGetLastError());
+  k_islands<<<1, 1024, 0, st>>>(n, P->edges, P->icnt, edge_cap, P->label, P->merged, P->isl_of, P->isl_size,
+                                P->isl_members, P->icnt + 1, P->icnt + 2);
+  STP_CK(cudaGetLastError());
+  view->merged = P->merged;
+  view->isl_members = P->isl_members;
+  view->isl_count = P->icnt + 1;
+  view->err = P->icnt + 2;
+  view->xslots = P->xslots;
+  view->xcount = P->xcount;
+  return cudaSuccess;
+#undef STP_CK
+}
+
+template cudaError_t prepare_islands<float>(PairScratch*&, const DevModel<float>*, int, const float*, const double*,
+                                            int, int, double, IslandView*, cudaStream_t);
+template cudaError_t prepare_islands<double>(PairScratch*&, const DevModel<double>*, int, const double*,
+                                             const double*, int, int, double, IslandView*, cudaStream_t);
 
 template cudaError_t detect_pairs<float>(PairScratch*&, const DevModel<float>*, int, const float*, const double*, int,
                                          int, double, int, int*, int32_t*, int32_t*, double*, double*, double*, bool*,

@@ -34,7 +34,12 @@ constexpr int G_QH = 0;     // 13: quirk in the transformed system: d0, qa (6), 
 constexpr int G_HD = 13;    // 21: diagonal block, kept only when it is not positive definite
 constexpr int G_LC = 34;    // 21: Cholesky factor L of the own block (exact residual test, back-substitution)
 constexpr int G_CT = 55;    // 11 per overflow contact slot (terrain instantiation, slots CPB.. CPB+11)
-static_assert(G_CT + 11 * kSpillSlots == kScratchRows, "scratch layout");
+// island mode, per cross-contact slot s at G_XS + kXSlotRows * s:
+//   0 partner warp, 1 partner lane, 2 role, 3 r_own, 6 r_part, 9 normal,
+//   12 tangent t1, 15 bias, 16 normal-row weight (kc m_eff), 17 active normal
+//   weight, 18 friction weight (this Newton iterate), 19.. Hh_x (36, row-major)
+constexpr int G_XS = G_CT + 11 * kSpillSlots;
+static_assert(G_XS + kXSlotRows * kXSlots == kScratchRows, "scratch layout");
 template <int CPB>
 __host__ __device__ constexpr int smem_rows() {
   return R_CT + 11 * CPB;
@@ -356,11 +361,50 @@ __device__ __forceinline__ void seg_sum2(T& a, T& b, unsigned mask) {
 #endif
 constexpr int kStepThreads = STP_TPB;  // threads per block (whole warps, one env segment each)
 
-template <class T, int W, int CPB>
-__global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1)) k_env_step(const KArgs<T> a) {
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int e = a.e_begin + tid / W;
-  if (e >= a.n) return;  // whole segments exit together
+// Island mode (ISL): one CTA per contact-merged island, warp w = the island's
+// w-th env in index order (the reference's slot order, solver.cpp:472-481).
+// Envs stay warp-local; what couples them — inter-agent contact rows, the
+// island-wide PCR reductions and exit tests, rollback — goes through shared
+// memory and a named barrier over the island's warps.
+template <class T>
+__host__ __device__ constexpr int island_cap() {
+  return sizeof(T) == 4 ? kIslandMax : kIslandMax / 2;
+}
+constexpr int kXch = 21;  // per-lane exchange entries (Mi is the largest)
+
+template <class T, int W, int CPB, bool ISL = false>
+__global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
+    k_env_step(const KArgs<T> a) {
+  int e;
+  int isl_m = 1, isl_w = 0;  // island size and this warp's place in it
+  if constexpr (ISL) {
+    static_assert(W == 32, "island mode: one env per warp");
+    if (blockIdx.x >= unsigned(*a.isl_count)) return;
+    const int* mem = a.isl_members + blockIdx.x * kIslandMax;
+    isl_m = 0;
+    for (int k = 0; k < kIslandMax; ++k) isl_m += mem[k] >= 0;
+    if (isl_m > island_cap<T>() || *a.isl_err) {
+      // island beyond this instantiation's capacity, or cross contacts were
+      // dropped in preparation: not stepped, flagged (stp_get_report overflow)
+      if (threadIdx.x == 0 && a.overflow_out)
+        for (int k = 0; k < kIslandMax; ++k)
+          if (mem[k] >= 0) a.overflow_out[mem[k]] = 1;
+      if (isl_m > island_cap<T>()) return;
+    }
+    isl_w = threadIdx.x >> 5;
+    if (isl_w >= isl_m) return;  // before the first island barrier
+    e = -1;
+    for (int k = 0; k < isl_m; ++k) {
+      int rank = 0;
+      for (int j = 0; j < isl_m; ++j) rank += mem[j] < mem[k];
+      if (rank == isl_w) e = mem[k];
+    }
+  } else {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    e = a.e_begin + tid / W;
+    if (e >= a.n) return;  // whole segments exit together
+    if (a.merged && a.merged[e]) return;  // stepped by the island launch
+  }
   const int lane = threadIdx.x & 31;
   const int b = lane % W;
   const int base = lane - b;
@@ -380,6 +424,62 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
   extern __shared__ unsigned char smem_raw[];
   Lane<T, W> L;
   L.sm = reinterpret_cast<T*>(smem_raw) + (threadIdx.x >> 5) * (smem_rows<CPB>() * 32);
+  // island exchange area (ISL): per-lane entries, reduction partials, votes
+  T* xch = reinterpret_cast<T*>(smem_raw) + (ISL ? island_cap<T>() : 0) * smem_rows<CPB>() * 32;
+  T* red = xch + (ISL ? island_cap<T>() * 32 * kXch : 0);
+  int* vote = reinterpret_cast<int*>(red + 4 * island_cap<T>());
+  auto isl_bar = [&]() {
+    if constexpr (ISL) asm volatile("bar.sync 1, %0;\n" ::"r"(32 * isl_m) : "memory");
+  };
+  // segment sums / votes over the whole island (the warp forms without ISL)
+  auto isl_sum = [&](T v) -> T {
+    v = seg_sum<W>(v, mask);
+    if constexpr (ISL) {
+      if (lane == 0) red[isl_w] = v;
+      isl_bar();
+      T s = T(0);
+      for (int k = 0; k < isl_m; ++k) s += red[k];
+      isl_bar();
+      v = s;
+    }
+    return v;
+  };
+  auto isl_sum4 = [&](T& v0, T& v1, T& v2, T& v3) {
+    seg_sum4<W>(v0, v1, v2, v3, mask);
+    if constexpr (ISL) {
+      if (lane == 0) {
+        red[4 * isl_w] = v0;
+        red[4 * isl_w + 1] = v1;
+        red[4 * isl_w + 2] = v2;
+        red[4 * isl_w + 3] = v3;
+      }
+      isl_bar();
+      T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
+      for (int k = 0; k < isl_m; ++k) {
+        s0 += red[4 * k];
+        s1 += red[4 * k + 1];
+        s2 += red[4 * k + 2];
+        s3 += red[4 * k + 3];
+      }
+      isl_bar();
+      v0 = s0;
+      v1 = s1;
+      v2 = s2;
+      v3 = s3;
+    }
+  };
+  auto isl_all = [&](bool p) -> bool {
+    bool r = __all_sync(mask, p);
+    if constexpr (ISL) {
+      if (lane == 0) vote[isl_w] = r ? 1 : 0;
+      isl_bar();
+      r = true;
+      for (int k = 0; k < isl_m; ++k) r = r && vote[k] != 0;
+      isl_bar();
+    }
+    return r;
+  };
+  auto isl_any = [&](bool p) -> bool { return !isl_all(!p); };
   L.gs = a.scratch + size_t(e) * kScratchRows * W;
   L.mask = mask;
   L.lane = lane;
@@ -941,20 +1041,91 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
 #pragma unroll 1
       for (int k = CPB; k < nc; ++k) contact_row(L.template slot<CPB>(k));
     }
+    // inter-agent contact rows (island mode; collide.cpp:251-266, rows
+    // solver.cpp:176-210): slots in the reference's contact order, lever arms,
+    // tangent basis, bias and the normal row's weight kc / (J M^-1 J^T) summed
+    // over body_a then body_b as effective_mass does (:69-80) — computed the
+    // same way on both sides so both agree on every activity decision.
+    int xc = 0;
+    if constexpr (ISL) {
+      const int gme = e * M.nb + b;
+      if (act) xc = min(a.xcount[gme], kXSlots);
+      int ord[kXSlots] = {0, 1, 2, 3};
+      for (int s1 = 1; s1 < xc; ++s1)
+        for (int s2 = s1; s2 > 0 && a.xslots[size_t(gme) * kXSlots + ord[s2 - 1]].key >
+                                        a.xslots[size_t(gme) * kXSlots + ord[s2]].key;
+             --s2) {
+          const int t = ord[s2];
+          ord[s2] = ord[s2 - 1];
+          ord[s2 - 1] = t;
+        }
+      const int* mem = a.isl_members + blockIdx.x * kIslandMax;
+      T* my = xch + (isl_w * 32 + lane) * kXch;
+      my[0] = inv_m;
+      my[1] = Iinv.xx;
+      my[2] = Iinv.yy;
+      my[3] = Iinv.zz;
+      my[4] = Iinv.xy;
+      my[5] = Iinv.xz;
+      my[6] = Iinv.yz;
+      isl_bar();
+      for (int s2 = 0; s2 < xc; ++s2) {
+        const XSlot& X = a.xslots[size_t(gme) * kXSlots + ord[s2]];
+        const int pe = X.partner / M.nb, pb = X.partner % M.nb;
+        int pw = 0;
+        for (int k = 0; k < isl_m; ++k) pw += mem[k] < pe;
+        const T* pp = xch + (pw * 32 + pb) * kXch;
+        const T pinv = pp[0];
+        const sym3<T> pI{pp[1], pp[2], pp[3], pp[4], pp[5], pp[6]};
+        const int G = G_XS + kXSlotRows * s2;
+        const v3<T> n{T(X.normal[0]), T(X.normal[1]), T(X.normal[2])};
+        const v3<T> ro{T(X.r_own[0]), T(X.r_own[1]), T(X.r_own[2])};
+        const v3<T> rp{T(X.r_part[0]), T(X.r_part[1]), T(X.r_part[2])};
+        const v3<T> ref = fabs(n.z) < T(0.9) ? v3<T>{0, 0, 1} : v3<T>{1, 0, 0};
+        const v3<T> t1 = vunit(cross(n, ref));
+        const bool own_a = X.role > 0;
+        const T ia = own_a ? inv_m : pinv, ib = own_a ? pinv : inv_m;
+        const sym3<T>& Ia = own_a ? Iinv : pI;
+        const sym3<T>& Ib = own_a ? pI : Iinv;
+        const v3<T> ra = own_a ? ro : rp, rb = own_a ? rp : ro;
+        T wsum = ia * dot(n, n);
+        wsum += quad(Ia, cross(ra, n));
+        wsum += ib * dot(n, n);
+        wsum += quad(Ib, cross(rb, n));  // jb = -(n, rb x n): the quadratic forms are equal
+        L.g(G + 0) = T(pw);
+        L.g(G + 1) = T(pb);
+        L.g(G + 2) = T(X.role);
+        L.g(G + 3) = ro.x;
+        L.g(G + 4) = ro.y;
+        L.g(G + 5) = ro.z;
+        L.g(G + 6) = rp.x;
+        L.g(G + 7) = rp.y;
+        L.g(G + 8) = rp.z;
+        L.g(G + 9) = n.x;
+        L.g(G + 10) = n.y;
+        L.g(G + 11) = n.z;
+        L.g(G + 12) = t1.x;
+        L.g(G + 13) = t1.y;
+        L.g(G + 14) = t1.z;
+        L.g(G + 15) = uni_bias(T(X.sep), cf.beta, cf.dt);
+        L.g(G + 16) = cf.kc * (wsum > T(1e-12) ? T(1) / wsum : T(0));
+      }
+      isl_bar();  // exchange area free again
+    }
     // the constant off-diagonal block must be finite (krylov.cpp:113)
     bool off_fin = true;
     if (L.has_off) {
 #pragma unroll
       for (int k = 0; k < 36; ++k) off_fin = off_fin && isfinite(L.at(R_HOFF + k));
     }
-    const bool off_ok = __all_sync(mask, off_fin);
+    const bool off_ok = isl_all(off_fin);
 
     // ---------------- Newton loop (solver.cpp:540-548) ---------------------
     T u[6] = {v.x, v.y, v.z, w.x, w.y, w.z};  // warm start from current velocities
     // segment-uniform decisions are taken through votes throughout: the
     // compiler then sees uniform control flow and drops the convergence
     // checks it would otherwise put in front of every shuffle of the solve
-    const bool need_solve = __any_sync(mask, J > 0 || any_contact);
+    const bool need_solve = isl_any(J > 0 || any_contact || xc > 0);
     if (!need_solve) {  // free-body fast path, solver.cpp:517-523
       u[0] = vfree.x; u[1] = vfree.y; u[2] = vfree.z;
       u[3] = wfree.x; u[4] = wfree.y; u[5] = wfree.z;
@@ -1053,6 +1224,69 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
 #pragma unroll 1
           for (int k = CPB; k < nc; ++k) contact_newton(L.template slot<CPB>(k));
         }
+        if constexpr (ISL) {
+          // inter-agent rows at the iterate: partners' velocities through the
+          // exchange area; rates in body_a, body_b order (assemble :304-327)
+          T* my = xch + (isl_w * 32 + lane) * kXch;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) my[k] = u[k];
+          isl_bar();
+          for (int s2 = 0; s2 < xc; ++s2) {
+            const int G = G_XS + kXSlotRows * s2;
+            const T* up = xch + (int(L.g(G)) * 32 + int(L.g(G + 1))) * kXch;
+            const T role = L.g(G + 2);
+            const v3<T> ro{L.g(G + 3), L.g(G + 4), L.g(G + 5)}, rp{L.g(G + 6), L.g(G + 7), L.g(G + 8)};
+            const v3<T> n{L.g(G + 9), L.g(G + 10), L.g(G + 11)}, t1{L.g(G + 12), L.g(G + 13), L.g(G + 14)};
+            const v3<T> t2 = cross(n, t1);
+            const T bias = L.g(G + 15), dn = L.g(G + 16);
+            auto rate = [&](const v3<T>& d) {  // J_a u_a + J_b u_b of the row along d
+              const v3<T> co = cross(ro, d) * role, cp = cross(rp, d) * (-role);
+              const v3<T> lo = d * role, lp = d * (-role);
+              const T jo[6] = {lo.x, lo.y, lo.z, co.x, co.y, co.z};
+              const T jp[6] = {lp.x, lp.y, lp.z, cp.x, cp.y, cp.z};
+              T upv[6];
+#pragma unroll
+              for (int k = 0; k < 6; ++k) upv[k] = up[k];
+              return role > T(0) ? dot6(jo, u) + dot6(jp, upv) : dot6(jp, upv) + dot6(jo, u);
+            };
+            const T pred = dn * (bias - rate(n));
+            T rn = T(0), rf = T(0);
+            if (pred > T(0)) {
+              const T vt1 = rate(t1), vt2 = rate(t2);
+              rf = fric_weight(pred, sqrt(vt1 * vt1 + vt2 * vt2), cf.epsf);
+              rn = dn;
+            }
+            auto jown = [&](const v3<T>& d, T (&j)[6]) {
+              const v3<T> c = cross(ro, d) * role;
+              j[0] = d.x * role;
+              j[1] = d.y * role;
+              j[2] = d.z * role;
+              j[3] = c.x;
+              j[4] = c.y;
+              j[5] = c.z;
+            };
+            if (rn > T(0)) {
+              T jn[6];
+              jown(n, jn);
+              sym_add(H, jn, rn);
+              const T db = rn * bias;
+#pragma unroll
+              for (int r = 0; r < 6; ++r) rhs[r] += jn[r] * db;
+            }
+            if (rf > T(0)) {
+              T j1[6], j2[6];
+              jown(t1, j1);
+              jown(t2, j2);
+              sym_add(H, j1, rf);
+              sym_add(H, j2, rf);
+            } else {
+              rf = T(0);
+            }
+            L.g(G + 17) = rn;
+            L.g(G + 18) = rf;
+          }
+          isl_bar();
+        }
 
         // ---------------- PCR (solve_krylov_inplace, krylov.cpp:106-174) --
         // Split block-Jacobi form.  With L_b L_b^T = H_bb (krylov.cpp:27-41),
@@ -1067,12 +1301,12 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
 #pragma unroll
         for (int k = 0; k < 6; ++k) fin = fin && isfinite(rhs[k]);
         ++newton_done;
-        if (!off_ok || !__all_sync(mask, fin)) {  // reference throws (krylov.cpp:113-114)
+        if (!off_ok || !isl_all(fin)) {  // reference throws (krylov.cpp:113-114)
           step_failed = true;
           break;
         }
-        const T bb = seg_sum<W>(dot6(rhs, rhs), mask);
-        if (__all_sync(mask, bb == T(0))) {
+        const T bb = isl_sum(dot6(rhs, rhs));
+        if (isl_all(bb == T(0))) {
 #pragma unroll
           for (int k = 0; k < 6; ++k) u[k] = T(0);
           continue;
@@ -1165,6 +1399,55 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
               L.g(G_QH + 7 + i) = qc;
             }
           }
+          if constexpr (ISL) {
+            // transformed coupling blocks of the inter-agent rows:
+            // Ahat(own, partner) = Mi_own H(own, partner) Mi_partner^T
+            //                    = sum_rows w (Mi_own j_own)(Mi_partner j_partner)^T
+            T* my = xch + (isl_w * 32 + lane) * kXch;
+#pragma unroll
+            for (int k = 0; k < 21; ++k) my[k] = Mi[k];
+            isl_bar();
+            for (int s2 = 0; s2 < xc; ++s2) {
+              const int G = G_XS + kXSlotRows * s2;
+              const T* mp = xch + (int(L.g(G)) * 32 + int(L.g(G + 1))) * kXch;
+              const T role = L.g(G + 2);
+              const v3<T> ro{L.g(G + 3), L.g(G + 4), L.g(G + 5)}, rp{L.g(G + 6), L.g(G + 7), L.g(G + 8)};
+              const v3<T> n{L.g(G + 9), L.g(G + 10), L.g(G + 11)}, t1{L.g(G + 12), L.g(G + 13), L.g(G + 14)};
+              const v3<T> t2 = cross(n, t1);
+              const T wrow[3] = {L.g(G + 17), L.g(G + 18), L.g(G + 18)};
+              const v3<T> dir[3] = {n, t1, t2};
+              T hx[36];
+#pragma unroll
+              for (int k = 0; k < 36; ++k) hx[k] = T(0);
+#pragma unroll
+              for (int r = 0; r < 3; ++r) {
+                if (!(wrow[r] > T(0))) continue;
+                const v3<T> d = dir[r];
+                const v3<T> co = cross(ro, d) * role, cp = cross(rp, d) * (-role);
+                const T jo[6] = {d.x * role, d.y * role, d.z * role, co.x, co.y, co.z};
+                const T jp[6] = {-d.x * role, -d.y * role, -d.z * role, cp.x, cp.y, cp.z};
+                T al[6], be[6];
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                  T sa = T(0), sb = T(0);
+#pragma unroll
+                  for (int k = 0; k <= i; ++k) {
+                    sa += Mi[tri(i, k)] * jo[k];
+                    sb += mp[tri(i, k)] * jp[k];
+                  }
+                  al[i] = wrow[r] * sa;
+                  be[i] = sb;
+                }
+#pragma unroll
+                for (int i = 0; i < 6; ++i)
+#pragma unroll
+                  for (int j = 0; j < 6; ++j) hx[i * 6 + j] += al[i] * be[j];
+              }
+#pragma unroll
+              for (int k = 0; k < 36; ++k) L.g(G + 19 + k) = hx[k];
+            }
+            isl_bar();
+          }
         }
         // Exit test of the reference, ||r|| > tol ||b|| (krylov.cpp:141, :154),
         // compared squared.  ||r|| = |L rhat| costs 27 FMA per lane, so each
@@ -1183,7 +1466,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
             for (int k = 0; k <= i; ++k) ri += L.g(G_LC + tri(i, k)) * rh[k];
             s0 += ri * ri;
           }
-          return seg_sum<W>(s0, mask);
+          return isl_sum(s0);
         };
         // The loop is instantiated three times so the common case runs without
         // the rare-term branches and with a compile-time gather schedule.  Exit
@@ -1192,7 +1475,30 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
         auto pcr = [&](auto rare_c, auto gr_c) -> int {
           constexpr bool RARE = decltype(rare_c)::value;
           constexpr int GR = decltype(gr_c)::value;
-          if constexpr (sizeof(T) == 4 && kPackedPCR) {
+          // y = Ahat v: the env's own blocks, plus in island mode the
+          // inter-agent coupling blocks against the partners' v (exchange area)
+          auto apply_x = [&](const T (&v)[6], T (&y)[6]) {
+            L.template apply_hat<RARE, GR>(v, y);
+            if constexpr (ISL) {
+              T* my = xch + (isl_w * 32 + lane) * kXch;
+#pragma unroll
+              for (int k = 0; k < 6; ++k) my[k] = v[k];
+              isl_bar();
+              for (int s2 = 0; s2 < xc; ++s2) {
+                const int G = G_XS + kXSlotRows * s2;
+                const T* vp = xch + (int(L.g(G)) * 32 + int(L.g(G + 1))) * kXch;
+#pragma unroll
+                for (int r = 0; r < 6; ++r) {
+                  T acc = T(0);
+#pragma unroll
+                  for (int c = 0; c < 6; ++c) acc += L.g(G + 19 + r * 6 + c) * vp[c];
+                  y[r] += acc;
+                }
+              }
+              isl_bar();
+            }
+          };
+          if constexpr (sizeof(T) == 4 && kPackedPCR && !ISL) {
             // fp32: the loop on packed pairs (see Lane::apply_hat_p)
             float2 Hp[18];
 #pragma unroll
@@ -1268,10 +1574,10 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
             return kk;
           } else {
           T rh[6], ar[6], ph[6], ap[6];
-          L.template apply_hat<RARE, GR>(xh, ar);
+          apply_x(xh, ar);
 #pragma unroll
           for (int k = 0; k < 6; ++k) rh[k] = dyn ? bh[k] - ar[k] : T(0);
-          L.template apply_hat<RARE, GR>(rh, ar);
+          apply_x(rh, ar);
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
             ph[k] = rh[k];
@@ -1285,10 +1591,15 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
           // (Ahat p' = Ahat r + beta Ahat p); ap itself is still updated
           // explicitly, only its norm is formed by the expansion.
           T denom = dot6(ar, ar);
-          seg_sum3<W>(zaz, lb, denom, mask);
+          if constexpr (ISL) {
+            T dummy = T(0);
+            isl_sum4(zaz, lb, denom, dummy);
+          } else {
+            seg_sum3<W>(zaz, lb, denom, mask);
+          }
           bool above = lb > tol2_safe || res_exact(rh) > tol2;
-          while (__all_sync(mask, kk < cf.kmax && above)) {
-            if (!__all_sync(mask, denom > T(0) && zaz > T(0))) break;  // breakdown (krylov.cpp:144)
+          while (isl_all(kk < cf.kmax && above)) {
+            if (!isl_all(denom > T(0) && zaz > T(0))) break;  // breakdown (krylov.cpp:144)
             const T alpha = fdiv(zaz, denom);
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
@@ -1299,12 +1610,12 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
             // at the iteration cap the exit is certain: the product, the norms
             // and the exit test of this point cannot change xhat
             if (kk >= cf.kmax) break;
-            L.template apply_hat<RARE, GR>(rh, ar);
+            apply_x(rh, ar);
             T zn = dot6(rh, ar), aa = dot6(ar, ar), ax = dot6(ar, ap);
             lb = lbw * dot6(rh, rh);
-            seg_sum4<W>(lb, zn, aa, ax, mask);
+            isl_sum4(lb, zn, aa, ax);
             above = lb > tol2_safe || res_exact(rh) > tol2;
-            if (!__all_sync(mask, above)) break;
+            if (!isl_all(above)) break;
             const T beta = fdiv(zn, zaz);
             zaz = zn;
             denom = aa + beta * (T(2) * ax + beta * denom);
@@ -1349,7 +1660,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
           }
         };
         int kk;
-        if (L.any_diag || L.any_quirk) kk = pcr(std::true_type{}, std::integral_constant<int, 0>{});
+        if (ISL || L.any_diag || L.any_quirk) kk = pcr(std::true_type{}, std::integral_constant<int, 0>{});
         else if (__all_sync(mask, L.grounds == 2)) kk = pcr(std::false_type{}, std::integral_constant<int, 2>{});
         else kk = pcr(std::false_type{}, std::integral_constant<int, 0>{});
         // back to velocities: solve L^T u = xhat (reciprocal diagonal parked in R_SCAT)
@@ -1364,7 +1675,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
         bool ufin = true;
 #pragma unroll
         for (int k = 0; k < 6; ++k) ufin = ufin && isfinite(u[k]);
-        if (!__all_sync(mask, ufin)) {  // never hand back a poisoned iterate (:168-172)
+        if (!isl_all(ufin)) {  // never hand back a poisoned iterate (:168-172)
 #pragma unroll
           for (int k = 0; k < 6; ++k) u[k] = T(0);
         }
@@ -1449,7 +1760,7 @@ __global__ void __launch_bounds__(kStepThreads, (sizeof(T) == 4 ? STP_MINB : 1))
       qn = qunit(qmul(qexp(wn * cf.dt), q));
     }
     const bool fin_state = vfinite(xn) && qfinite(qn) && vfinite(vn) && vfinite(wn);
-    step_failed = step_failed || !__all_sync(mask, fin_state);
+    step_failed = step_failed || !isl_all(fin_state);  // the whole island rolls back (:580-593)
     if (!step_failed) {
       x = xn;
       q = qn;
@@ -1674,8 +1985,31 @@ static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <class T, int W, int CPB>
+static cudaError_t launch_island(const KArgs<T>& a, cudaStream_t s) {
+  constexpr int cap = island_cap<T>();
+  const size_t smem = size_t(cap) * smem_rows<CPB>() * 32 * sizeof(T) + size_t(cap) * 32 * kXch * sizeof(T) +
+                      size_t(4 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t err = cudaFuncSetAttribute(k_env_step<T, W, CPB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(smem));
+    if (err != cudaSuccess) return err;
+    configured = true;
+  }
+  const int grid = (a.n - a.e_begin) / 2 > 0 ? (a.n - a.e_begin) / 2 : 1;  // at most n/2 merged islands
+  k_env_step<T, W, CPB, true><<<grid, 32 * cap, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <class T>
 cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s) {
+  if (a.merged) {  // inter-agent collisions: independent envs, then the merged islands
+    if (lanes != 32) return cudaErrorInvalidValue;
+    cudaError_t e = cpb <= 2 ? launch_one<T, 32, 2>(a, s) : launch_one<T, 32, 4>(a, s);
+    if (e != cudaSuccess) return e;
+    return cpb <= 2 ? launch_island<T, 32, 2>(a, s) : launch_island<T, 32, 4>(a, s);
+  }
   if (lanes == 32) {
     if (cpb <= 2) return launch_one<T, 32, 2>(a, s);
     return launch_one<T, 32, 4>(a, s);

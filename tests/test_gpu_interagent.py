@@ -116,3 +116,43 @@ def test_crowded_humanoids_match_reference(precision):
                 assert abs(d["separation"][i] - ref["separation"][jj]) <= 1e-5
     print(f"{precision}: {total} reference inter-agent contacts over 4 states, {flips} boundary flips")
     assert total > 50  # the crowd actually touches
+
+
+@pytest.mark.skipif(not oracle.available("reference"), reason="compiled reference (oracle/_ref) not built")
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_contact_merged_islands_match_reference(precision):
+    """HFH with inter-agent collisions: agents overlapping in
+    pairs and one triple form contact-merged islands that the island launch
+    solves as one system each (solver.cpp:458-502).  Teacher-forced one-step
+    states against the compiled reference: f64 |dx| <= 1e-7 m, rel|dv| <= 1e-4;
+    f32 the SURVEY §8(c) bounds (|dx| p99 <= 1e-4, max <= 5e-3)."""
+    n = 9
+    g = VecEnv("hfh", n_envs=n, precision=precision, seed=31)
+    assert g.task.inter_agent_collisions == 1
+    o = oracle.OracleEnv(g.model, g.task, g.cfg, n, seed=31, kind="reference")
+    st = o.get_state()
+    for e, dx in ((1, 1.7), (3, 1.7), (5, 1.7), (7, 1.7), (8, 3.4)):  # islands {0,1} {2,3} {4,5} {6,7,8}
+        st[e, :, 0] -= dx
+    o.set_state(st)
+    tm = np.array([g.model.joints[j].max_torque for j in range(g.action_dim)])
+    dxs, dvs = [], []
+    pairs = 0
+    for t in range(6):
+        s = o.get_state()
+        g.set_state(s)
+        pairs += g.detect_inter_agent()["body_a"].size
+        tq = o.random_actions(t) * tm
+        o.physics_step(tq)
+        g.physics_step(tq)
+        so, sg = o.get_state(), g.get_state()
+        dxs.append(np.abs(so[..., 0:3] - sg[..., 0:3]).max(axis=(1, 2)))
+        dvs.append(np.abs(so[..., 7:13] - sg[..., 7:13]).max(axis=(1, 2)) / np.maximum(1, np.abs(so[..., 7:13]).max(axis=(1, 2))))
+        assert g.report()["overflow"].sum() == 0
+    dx, dv = np.concatenate(dxs), np.concatenate(dvs)
+    print(f"{precision}: {pairs} inter-agent contacts over 6 states; |dx| max {dx.max():.2e} p99 "
+          f"{np.quantile(dx, 0.99):.2e}; rel|dv| max {dv.max():.2e}")
+    assert pairs > 6
+    if precision == "f64":
+        assert dx.max() <= 1e-7 and dv.max() <= 1e-4
+    else:
+        assert np.quantile(dx, 0.99) <= 1e-4 and dx.max() <= 5e-3

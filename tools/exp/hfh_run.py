@@ -1,0 +1,12 @@
+"""HFH (inter-agent collisions on) at 4096 envs: a few env steps (for ncu launch lists)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import torch
+from paper_1810_05762_b200.sim import VecEnv
+
+env = VecEnv("hfh", n_envs=4096, seed=3)
+env.reset()
+for s in range(12):
+    env.step(env.random_actions(s))
+torch.cuda.synchronize()
+print("ok")
