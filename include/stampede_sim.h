@@ -235,8 +235,10 @@ int stp_set_external_loads(stp_sim* sim, const double* loads);
 /* Ordered contact list of the last physics step per env (detect_contacts
  * order, collide.cpp:283-299) with the solved impulses (SolvedContact,
  * types.hpp:109-113).  count int32[N]; per slot (N*capacity): body_a,
- * body_b (-1 static), point[3], normal[3], separation, normal impulse,
- * tangential impulse[3].  Any output pointer may be NULL. */
+ * body_b (-1 static; an inter-agent contact is listed with body_a's env after
+ * its static contacts, body_b = the partner's global index env * B + body),
+ * point[3], normal[3], separation, normal impulse, tangential impulse[3].
+ * Any output pointer may be NULL. */
 int stp_get_contacts(stp_sim* sim, int32_t* count, int32_t* body_a, int32_t* body_b,
                      double* point, double* normal, double* separation,
                      double* normal_impulse, double* tangential_impulse);

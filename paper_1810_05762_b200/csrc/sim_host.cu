@@ -866,8 +866,8 @@ int stp_get_contacts(stp_sim* s, int32_t* count, int32_t* body_a, int32_t* body_
     for (int i = 0; i < m; ++i) {
       const size_t k = e * C + i;
       const double* d = data.data() + k * stp::kCData;
-      if (body_a) body_a[k] = body[k];
-      if (body_b) body_b[k] = -1;
+      if (body_a) body_a[k] = body[k] & 0xff;
+      if (body_b) body_b[k] = (body[k] >> 8) - 1;  // -1 static; inter-agent: partner's global index
       for (int c = 0; c < 3; ++c) {
         if (point) point[3 * k + c] = d[c];
         if (normal) normal[3 * k + c] = d[3 + c];

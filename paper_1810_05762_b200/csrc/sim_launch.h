@@ -10,9 +10,9 @@ namespace stp {
 // whose 4 first slots per body live in shared memory, then the island mode's
 // cross-contact slots).
 constexpr int kSpillSlots = 12;
-// island mode: per cross-contact slot 19 geometry / weight rows + the 36-entry
-// transformed coupling block (sim_step.cuh G_XS)
-constexpr int kXSlotRows = 19 + 36;
+// island mode: per cross-contact slot 19 geometry / weight rows, the 36-entry
+// transformed coupling block and the partner's global index (sim_step.cuh G_XS)
+constexpr int kXSlotRows = 19 + 36 + 1;
 constexpr int kScratchRows = 55 + 11 * kSpillSlots + kXSlotRows * kXSlots;
 // lanes = W (8/16/32 lanes per env), cpb = shared-memory contact slots per body
 // (2: plane only; 4 + kSpillSlots overflow rows: terrain boxes, dynamic boxes).

@@ -37,7 +37,8 @@ constexpr int G_CT = 55;    // 11 per overflow contact slot (terrain instantiati
 // island mode, per cross-contact slot s at G_XS + kXSlotRows * s:
 //   0 partner warp, 1 partner lane, 2 role, 3 r_own, 6 r_part, 9 normal,
 //   12 tangent t1, 15 bias, 16 normal-row weight (kc m_eff), 17 active normal
-//   weight, 18 friction weight (this Newton iterate), 19.. Hh_x (36, row-major)
+//   weight, 18 friction weight (this Newton iterate), 19.. Hh_x (36, row-major),
+//   55 partner's global body index
 constexpr int G_XS = G_CT + 11 * kSpillSlots;
 static_assert(G_XS + kXSlotRows * kXSlots == kScratchRows, "scratch layout");
 template <int CPB>
@@ -1109,6 +1110,7 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
         L.g(G + 14) = t1.z;
         L.g(G + 15) = uni_bias(T(X.sep), cf.beta, cf.dt);
         L.g(G + 16) = cf.kc * (wsum > T(1e-12) ? T(1) / wsum : T(0));
+        L.g(G + 55) = T(X.partner);
       }
       isl_bar();  // exchange area free again
     }
@@ -1730,7 +1732,7 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
             pt = ta * (-fw * vt1) + tb * (-fw * vt2);
           }
           const size_t slot = size_t(e) * a.cap + off + k;
-          a.c_body[slot] = b;
+          a.c_body[slot] = b;  // body_b = static (high bits 0, see below)
           double* cdp = a.c_data + slot * kCData;
           const v3<T> pw = x + rr;
           // separation: recovered from the bias row (unilateral_bias is invertible)
@@ -1748,7 +1750,72 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
           cdp[10] = double(pt.z);
         }
       }
-    }
+          if constexpr (ISL) {
+        // inter-agent contacts follow the env's static ones, in (a, b) order,
+        // listed with body_a's env; body_b = partner's global index, encoded
+        // in c_body above the low 8 bits (+1, 0 = static)
+        T* my = xch + (isl_w * 32 + lane) * kXch;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) my[k] = u[k];
+        isl_bar();
+        int na = 0;
+        for (int s2 = 0; s2 < xc; ++s2) na += L.g(G_XS + kXSlotRows * s2 + 2) > T(0);
+        int offx = na;
+#pragma unroll
+        for (int s2 = 1; s2 < W; s2 <<= 1) {
+          const int o = __shfl_up_sync(mask, offx, s2, W);
+          if (b >= s2) offx += o;
+        }
+        offx -= na;
+        const int totx = __shfl_sync(mask, offx + na, W - 1, W);
+        int q = 0;
+        for (int s2 = 0; s2 < xc; ++s2) {
+          const int G = G_XS + kXSlotRows * s2;
+          if (!(L.g(G + 2) > T(0))) continue;
+          const int idx = total + offx + q++;
+          if (idx >= a.cap) continue;
+          const T* up = xch + (int(L.g(G)) * 32 + int(L.g(G + 1))) * kXch;
+          const v3<T> ro{L.g(G + 3), L.g(G + 4), L.g(G + 5)}, rp{L.g(G + 6), L.g(G + 7), L.g(G + 8)};
+          const v3<T> n{L.g(G + 9), L.g(G + 10), L.g(G + 11)}, t1{L.g(G + 12), L.g(G + 13), L.g(G + 14)};
+          const v3<T> t2 = cross(n, t1);
+          const T cb = L.g(G + 15), dn = L.g(G + 16);
+          auto rate = [&](const v3<T>& d) {  // body_a (this lane) then body_b
+            const v3<T> ca = cross(ro, d), cp = cross(rp, d);
+            const T ja[6] = {d.x, d.y, d.z, ca.x, ca.y, ca.z};
+            const T jb[6] = {-d.x, -d.y, -d.z, -cp.x, -cp.y, -cp.z};
+            T upv[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) upv[k] = up[k];
+            return dot6(ja, u) + dot6(jb, upv);
+          };
+          const T pn = max(T(0), dn * (cb - rate(n)));
+          v3<T> pt{0, 0, 0};
+          if (pn > T(0)) {
+            const T vt1 = rate(t1), vt2 = rate(t2);
+            const T fw = fric_weight(pn, sqrt(vt1 * vt1 + vt2 * vt2), cf.epsf);
+            pt = t1 * (-fw * vt1) + t2 * (-fw * vt2);
+          }
+          const size_t slot = size_t(e) * a.cap + idx;
+          a.c_body[slot] = b | ((int(L.g(G + 55)) + 1) << 8);
+          double* cdp = a.c_data + slot * kCData;
+          const v3<T> pw = x + ro;
+          const T sep = cb > T(0) ? -cb * cf.dt / cf.beta : -cb * cf.dt;
+          cdp[0] = ox + double(pw.x);
+          cdp[1] = oy + double(pw.y);
+          cdp[2] = double(pw.z);
+          cdp[3] = double(n.x);
+          cdp[4] = double(n.y);
+          cdp[5] = double(n.z);
+          cdp[6] = double(sep);
+          cdp[7] = double(pn);
+          cdp[8] = double(pt.x);
+          cdp[9] = double(pt.y);
+          cdp[10] = double(pt.z);
+        }
+        if (b == 0) a.c_count[e] = total + totx;
+        isl_bar();
+      }
+}
 
     // ---------------- integrate + rollback (:562-569, :580-593) -----------
     v3<T> xn = x, vn = v, wn = w;

@@ -145,6 +145,17 @@ def test_contact_merged_islands_match_reference(precision):
         o.physics_step(tq)
         g.physics_step(tq)
         so, sg = o.get_state(), g.get_state()
+        if precision == "f64":  # the ordered contact lists, inter-agent contacts included
+            co, cg = o.contact_arrays(g.contact_capacity), g.contact_arrays()
+            np.testing.assert_array_equal(co["count"], cg["count"])
+            for e in range(n):
+                c = co["count"][e]
+                np.testing.assert_array_equal(co["body_a"][e, :c], cg["body_a"][e, :c])
+                np.testing.assert_array_equal(co["body_b"][e, :c], cg["body_b"][e, :c])
+                assert np.abs(co["point"][e, :c] - cg["point"][e, :c]).max(initial=0.0) <= 1e-7
+                assert np.abs(co["separation"][e, :c] - cg["separation"][e, :c]).max(initial=0.0) <= 1e-9
+                pn = co["normal_impulse"][e, :c]
+                assert np.abs(pn - cg["normal_impulse"][e, :c]).max(initial=0.0) <= 1e-5 * max(1.0, np.abs(pn).max(initial=0.0))
         dxs.append(np.abs(so[..., 0:3] - sg[..., 0:3]).max(axis=(1, 2)))
         dvs.append(np.abs(so[..., 7:13] - sg[..., 7:13]).max(axis=(1, 2)) / np.maximum(1, np.abs(so[..., 7:13]).max(axis=(1, 2))))
         assert g.report()["overflow"].sum() == 0
