@@ -242,6 +242,15 @@ int stp_set_external_loads(stp_sim* sim, const double* loads);
 int stp_get_contacts(stp_sim* sim, int32_t* count, int32_t* body_a, int32_t* body_b,
                      double* point, double* normal, double* separation,
                      double* normal_impulse, double* tangential_impulse);
+/* Scene snapshot "SSNP" v1 (Scene::save_snapshot / load_snapshot,
+ * scene.cpp:80-104): u32 magic 0x504e5353, u32 version 1, u64 body count, then
+ * per body (env-major = scene body order) 13 little-endian f64: position,
+ * orientation (w x y z), linear velocity, angular velocity.  Byte-compatible
+ * with the reference; load rejects a bad magic / version / body count with the
+ * reference's messages (STP_EINVAL). */
+int64_t stp_snapshot_size(const stp_sim* sim);
+int stp_save_snapshot(stp_sim* sim, uint8_t* buffer, int64_t capacity);
+int stp_load_snapshot(stp_sim* sim, const uint8_t* buffer, int64_t size);
 /* Inter-agent contacts of the current state: the pairs
  * detect_contacts (collide.cpp:300-343) appends when
  * Scene::inter_agent_collisions is set — dynamic sphere/capsule bodies of

@@ -396,6 +396,8 @@ struct RestatedPhysics : PhysicsBackend {
 
 }  // namespace
 
+int set_error(const std::string& message) { return err(message); }
+
 std::unique_ptr<PhysicsBackend> make_restated_backend() { return std::make_unique<RestatedPhysics>(); }
 
 }  // namespace orc

@@ -61,4 +61,7 @@ struct World {
 std::unique_ptr<PhysicsBackend> make_restated_backend();
 std::unique_ptr<PhysicsBackend> make_reference_backend();  // only in oracle/_ref
 
+// last-error setter for the C API (returns STP_EINVAL)
+int set_error(const std::string& message);
+
 }  // namespace orc

@@ -67,6 +67,10 @@ def _lib(kind: str) -> C.CDLL:
     if hasattr(L, "orc_ref_detect"):  # reference builds only
         L.orc_ref_detect.argtypes = [P, C.c_int32] + [P] * 5
         L.orc_ref_detect.restype = C.c_int32
+        L.orc_ref_save_snapshot.argtypes = [P, P, C.c_int64]
+        L.orc_ref_save_snapshot.restype = C.c_int64
+        L.orc_ref_load_snapshot.argtypes = [P, P, C.c_int64]
+        L.orc_ref_load_snapshot.restype = C.c_int32
     L.orc_get_report.argtypes = [P, P, P, P]
     L.orc_get_task_state.argtypes = [P, P, P, P]
     L.orc_set_task_state.argtypes = [P, P, P, P]
@@ -194,6 +198,18 @@ class OracleEnv:
                                   _p(out["normal"]), _p(out["separation"]))
         k = min(n, capacity)
         return {key: v[:k] for key, v in out.items()}
+
+    def ref_save_snapshot(self) -> bytes:
+        """Scene::save_snapshot of the compiled reference for the current state."""
+        n = self.L.orc_ref_save_snapshot(self.h, None, 0)
+        buf = np.zeros(n, np.uint8)
+        self.L.orc_ref_save_snapshot(self.h, _p(buf), n)
+        return buf.tobytes()
+
+    def ref_load_snapshot(self, data: bytes):
+        buf = np.frombuffer(data, np.uint8).copy()
+        if self.L.orc_ref_load_snapshot(self.h, _p(buf), buf.size) != 0:
+            raise RuntimeError(self.L.orc_last_error().decode())
 
     def report(self):
         N = self.n_envs

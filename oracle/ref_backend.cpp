@@ -6,6 +6,8 @@
 // on the reference util::ThreadPool (threading.hpp:32-126).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <sstream>
 #include <stdexcept>
 #include <vector>
 
@@ -227,4 +229,48 @@ extern "C" int orc_ref_detect(void* h, int capacity, int32_t* body_a, int32_t* b
     separation[i] = cs[i].separation;
   }
   return n;
+}
+
+// Snapshot hooks (Scene::save_snapshot / load_snapshot, scene.cpp:80-104) on a
+// reference scene built from the world: the checker of the GPU's SSNP bytes.
+extern "C" int64_t orc_ref_save_snapshot(void* h, uint8_t* buf, int64_t cap) {
+  auto* w = reinterpret_cast<orc::World*>(h);
+  orc::ReferencePhysics rp;
+  rp.build(*w);
+  const int NB = w->n * w->nb();
+  for (int i = 0; i < NB; ++i) {
+    const double* s = w->state.data() + size_t(i) * STP_STATE_STRIDE;
+    auto& rs = rp.scene.states[i];
+    rs.position = {s[0], s[1], s[2]};
+    rs.orientation = {s[3], s[4], s[5], s[6]};
+    rs.linear_velocity = {s[7], s[8], s[9]};
+    rs.angular_velocity = {s[10], s[11], s[12]};
+  }
+  std::stringstream ss;
+  rp.scene.save_snapshot(ss);
+  const std::string b = ss.str();
+  if (int64_t(b.size()) <= cap) std::memcpy(buf, b.data(), b.size());
+  return int64_t(b.size());
+}
+
+extern "C" int orc_ref_load_snapshot(void* h, const uint8_t* buf, int64_t size) {
+  auto* w = reinterpret_cast<orc::World*>(h);
+  orc::ReferencePhysics rp;
+  rp.build(*w);
+  std::stringstream ss(std::string(reinterpret_cast<const char*>(buf), size_t(size)));
+  try {
+    rp.scene.load_snapshot(ss);
+  } catch (const std::exception& ex) {
+    return orc::set_error(std::string(ex.what()));
+  }
+  const int NB = w->n * w->nb();
+  for (int i = 0; i < NB; ++i) {
+    double* s = w->state.data() + size_t(i) * STP_STATE_STRIDE;
+    const auto& rs = rp.scene.states[i];
+    s[0] = rs.position.x; s[1] = rs.position.y; s[2] = rs.position.z;
+    s[3] = rs.orientation.w; s[4] = rs.orientation.x; s[5] = rs.orientation.y; s[6] = rs.orientation.z;
+    s[7] = rs.linear_velocity.x; s[8] = rs.linear_velocity.y; s[9] = rs.linear_velocity.z;
+    s[10] = rs.angular_velocity.x; s[11] = rs.angular_velocity.y; s[12] = rs.angular_velocity.z;
+  }
+  return 0;
 }

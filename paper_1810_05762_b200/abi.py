@@ -164,6 +164,9 @@ SIGNATURES = [
     ("stp_set_external_loads", _I, [_P, _P]),
     ("stp_get_contacts", _I, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("stp_detect_inter_agent", _I, [_P, _I32, _P, _P, _P, _P, _P, _P]),
+    ("stp_snapshot_size", C.c_int64, [_P]),
+    ("stp_save_snapshot", _I, [_P, _P, C.c_int64]),
+    ("stp_load_snapshot", _I, [_P, _P, C.c_int64]),
     ("stp_get_report", _I, [_P, _P, _P, _P, _P]),
     ("stp_get_task_state", _I, [_P, _P, _P, _P]),
     ("stp_set_task_state", _I, [_P, _P, _P, _P]),

@@ -652,6 +652,42 @@ int32_t stp_obs_dim(const stp_sim* s) { return s ? s->obs_dim : 0; }
 int32_t stp_action_dim(const stp_sim* s) { return s ? s->J : 0; }
 int32_t stp_contact_capacity(const stp_sim* s) { return s ? s->cap : 0; }
 
+namespace {
+constexpr uint32_t kSnapshotMagic = 0x504e5353;  // "SSNP", scene.cpp:25-26
+constexpr uint32_t kSnapshotVersion = 1;
+}  // namespace
+
+int64_t stp_snapshot_size(const stp_sim* s) {
+  return s ? int64_t(16) + int64_t(s->n) * s->B * STP_STATE_STRIDE * 8 : 0;
+}
+
+int stp_save_snapshot(stp_sim* s, uint8_t* buf, int64_t capacity) {
+  if (!s || !buf) return fail(STP_EINVAL, "stp_save_snapshot: bad arguments");
+  const int64_t need = stp_snapshot_size(s);
+  if (capacity < need) return fail(STP_EINVAL, "stp_save_snapshot: buffer too small");
+  const uint64_t nb = uint64_t(s->n) * s->B;
+  std::memcpy(buf, &kSnapshotMagic, 4);
+  std::memcpy(buf + 4, &kSnapshotVersion, 4);
+  std::memcpy(buf + 8, &nb, 8);
+  return stp_get_state(s, reinterpret_cast<double*>(buf + 16));  // RigidBodyState order (types.hpp:28-32)
+}
+
+int stp_load_snapshot(stp_sim* s, const uint8_t* buf, int64_t size) {
+  if (!s || !buf || size < 16) return fail(STP_EINVAL, "stp_load_snapshot: bad arguments");
+  uint32_t magic, version;
+  uint64_t nb;
+  std::memcpy(&magic, buf, 4);
+  std::memcpy(&version, buf + 4, 4);
+  std::memcpy(&nb, buf + 8, 8);
+  if (magic != kSnapshotMagic) return fail(STP_EINVAL, "scene snapshot: bad magic");
+  if (version != kSnapshotVersion) return fail(STP_EINVAL, "scene snapshot: unsupported version");
+  if (nb != uint64_t(s->n) * s->B) return fail(STP_EINVAL, "scene snapshot: body count mismatch");
+  if (size < stp_snapshot_size(s)) return fail(STP_EINVAL, "scene snapshot: truncated");
+  std::vector<double> st(size_t(nb) * STP_STATE_STRIDE);
+  std::memcpy(st.data(), buf + 16, st.size() * 8);  // unaligned-safe
+  return stp_set_state(s, st.data());
+}
+
 int stp_detect_inter_agent(stp_sim* s, int32_t capacity, int32_t* count, int32_t* body_a, int32_t* body_b,
                            double* point, double* normal, double* separation) {
   if (!s || !count || capacity < 0) return fail(STP_EINVAL, "stp_detect_inter_agent: bad arguments");

@@ -209,6 +209,16 @@ class VecEnv:
                "get_contacts")
         return out
 
+    def save_snapshot(self) -> bytes:
+        """Scene snapshot "SSNP" v1 (scene.cpp:80-104), byte-compatible with the reference."""
+        buf = np.zeros(int(self.lib.stp_snapshot_size(self._h)), np.uint8)
+        _raise(self.lib.stp_save_snapshot(self._h, _ptr(buf), buf.size), "save_snapshot")
+        return buf.tobytes()
+
+    def load_snapshot(self, data: bytes):
+        buf = np.frombuffer(data, np.uint8).copy()
+        _raise(self.lib.stp_load_snapshot(self._h, _ptr(buf), buf.size), "load_snapshot")
+
     def detect_inter_agent(self, capacity: int | None = None):
         """Inter-agent contacts of the current state (row A7, detect_contacts
         with inter_agent_collisions, collide.cpp:300-343): global body indices

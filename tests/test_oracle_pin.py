@@ -114,3 +114,25 @@ def test_reference_inter_agent_hook_kat():
     c = o.ref_detect_contacts()
     assert list(zip(c["body_a"].tolist(), c["body_b"].tolist())) == [(0, 1)]
     assert abs(c["separation"][0] + 0.4) <= 1e-12
+
+
+@pytest.mark.skipif(not oracle.available("reference"), reason="compiled reference not built")
+def test_reference_snapshot_hooks_round_trip():
+    """orc_ref_save_snapshot / orc_ref_load_snapshot (the checkers of the GPU's
+    SSNP format) round-trip through the compiled reference's Scene and reject
+    a wrong body count with its message (scene.cpp:94-98)."""
+    import scenes as S
+    cfg = abi.default_step_config()
+    sc = S.sphere_scene(3.0)
+    o = oracle.OracleEnv(sc.build(), S.quiet_task(), cfg, 2, kind="reference")
+    st = np.stack([sc.state(), sc.state()])
+    st[1, 0, 2] = 7.0
+    o.set_state(st)
+    snap = o.ref_save_snapshot()
+    assert snap[:4] == b"SSNP" and len(snap) == 16 + 2 * 13 * 8
+    o2 = oracle.OracleEnv(sc.build(), S.quiet_task(), cfg, 2, kind="reference")
+    o2.ref_load_snapshot(snap)
+    np.testing.assert_array_equal(o2.get_state(), st)
+    o1 = oracle.OracleEnv(sc.build(), S.quiet_task(), cfg, 1, kind="reference")
+    with pytest.raises(RuntimeError, match="body count mismatch"):
+        o1.ref_load_snapshot(snap)
