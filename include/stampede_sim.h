@@ -171,6 +171,13 @@ int stp_builtin_model(const char* name, stp_model* out);
 /* Validation with the reference's rules, Scene::validate scene.cpp:36-68. */
 int stp_validate_model(const stp_model* model);
 int stp_default_task(int32_t kind, stp_task* out);
+/* load_model / serialize: the line-oriented
+ * articulation text format "stampede-model 1" (grammar in csrc/models.cpp and
+ * DESIGN.md §5).  Parse errors name the line and field (STP_EINVAL); the
+ * result is checked with stp_validate_model.  to_text writes at most
+ * capacity-1 bytes + NUL and reports the full length; load(to_text(m)) == m. */
+int stp_model_from_text(const char* text, stp_model* out);
+int stp_model_to_text(const stp_model* model, char* buffer, int32_t capacity, int32_t* length);
 /* generate_terrain, SPEC.md:206-214 (counter-based RNG: deterministic). */
 int stp_generate_terrain(const stp_terrain_spec* spec, stp_static_box* out, int32_t capacity);
 /* terrain_height, collide.cpp:348-359 (host, double; used by tests). */

@@ -141,6 +141,8 @@ SIGNATURES = [
     ("stp_default_step_config", None, [C.POINTER(StepConfig)]),
     ("stp_builtin_model", _I, [C.c_char_p, C.POINTER(Model)]),
     ("stp_validate_model", _I, [C.POINTER(Model)]),
+    ("stp_model_from_text", _I, [C.c_char_p, C.POINTER(Model)]),
+    ("stp_model_to_text", _I, [C.POINTER(Model), C.c_char_p, _I32, C.POINTER(_I32)]),
     ("stp_default_task", _I, [_I32, C.POINTER(Task)]),
     ("stp_generate_terrain", _I, [C.POINTER(TerrainSpec), C.POINTER(StaticBox), _I32]),
     ("stp_terrain_height", C.c_double, [C.POINTER(StaticBox), _I32, C.c_double, C.c_double]),
@@ -205,6 +207,25 @@ def last_error(lib=None) -> str:
 def check(rc: int, what: str = "", lib=None) -> None:
     if rc != STP_OK:
         raise RuntimeError(f"{what} failed (status {rc}): {last_error(lib)}")
+
+
+def model_from_text(text: str) -> Model:
+    """load_model: parse a "stampede-model 1" document."""
+    lib = load()
+    m = Model()
+    rc = lib.stp_model_from_text(text.encode(), C.byref(m))
+    if rc != STP_OK:
+        raise ValueError(last_error(lib))
+    return m
+
+
+def model_to_text(m: Model) -> str:
+    lib = load()
+    n = C.c_int32(0)
+    check(lib.stp_model_to_text(C.byref(m), None, 0, C.byref(n)), "stp_model_to_text")
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib.stp_model_to_text(C.byref(m), buf, n.value + 1, C.byref(n)), "stp_model_to_text")
+    return buf.value.decode()
 
 
 def builtin_model(name: str) -> Model:

@@ -13,7 +13,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <sstream>
 #include <string>
+#include <vector>
 
 #include "stampede_sim.h"
 #include "stp_error.h"
@@ -361,3 +364,265 @@ double stp_terrain_height(const stp_static_box* boxes, int32_t n, double x, doub
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Articulation text format "stampede-model 1":
+// line-oriented stanzas, '#' comments, numbers in %.17g so serialize -> load
+// is the identity on stp_model.
+//
+//   stampede-model 1
+//   name <text>            alive_bonus <x>        fall_height <x>
+//   body <name>            (fields, then 'end'):
+//     shape sphere|capsule|box   static 0|1   radius r   half_length h
+//     half_extents x y z   local_pos x y z   local_rot w x y z
+//     mass m   inertia ix iy iz   rest x y z qw qx qy qz vx vy vz wx wy wz
+//   end
+//   joint <name>           (fields, then 'end'):
+//     parent <body>   child <body>   anchor_parent x y z   anchor_child x y z
+//     axis_parent x y z   axis_child x y z   rest_relative w x y z   limit lo hi
+//   end
+//   actuator <joint> <tau_max>
+//   foot <body>
+//   root <body>
+// ---------------------------------------------------------------------------
+namespace {
+
+int parse_fail(int line, const std::string& what) {
+  return stp::fail(STP_EINVAL, "load_model: " + (line > 0 ? "line " + std::to_string(line) + ": " : std::string()) + what);
+}
+
+bool read_n(std::istringstream& ls, double* v, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!(ls >> v[i])) return false;
+  std::string extra;
+  return !(ls >> extra);
+}
+
+}  // namespace
+
+extern "C" int stp_model_from_text(const char* text, stp_model* out) {
+  if (!text || !out) return stp::fail(STP_EINVAL, "load_model: null argument");
+  stp_model m;
+  std::memset(&m, 0, sizeof(m));
+  std::map<std::string, int> body_id, joint_id;
+  std::vector<bool> has_tau;
+  bool header = false, has_root = false;
+  std::string root_name;
+  std::vector<std::pair<std::string, std::string>> joint_ends;  // parent, child names per joint
+  std::vector<int> joint_line;
+  enum { NONE, BODY, JOINT } open = NONE;
+  std::istringstream in(text);
+  std::string raw;
+  int line = 0;
+  while (std::getline(in, raw)) {
+    ++line;
+    const size_t hash = raw.find('#');
+    if (hash != std::string::npos) raw.resize(hash);
+    std::istringstream ls(raw);
+    std::string key;
+    if (!(ls >> key)) continue;
+    if (!header) {
+      int version = 0;
+      if (key != "stampede-model" || !(ls >> version)) return parse_fail(line, "expected 'stampede-model 1' header");
+      if (version != 1) return parse_fail(line, "unsupported model format version " + std::to_string(version));
+      header = true;
+      continue;
+    }
+    auto nums = [&](double* v, int n) {
+      return read_n(ls, v, n) ? STP_OK : parse_fail(line, "expected " + std::to_string(n) + " number(s) after '" + key + "'");
+    };
+    int rc = STP_OK;
+    if (open == BODY) {
+      stp_body& b = m.bodies[m.n_bodies - 1];
+      if (key == "end") open = NONE;
+      else if (key == "shape") {
+        std::string t;
+        ls >> t;
+        if (t == "sphere") b.shape = STP_SPHERE;
+        else if (t == "capsule") b.shape = STP_CAPSULE;
+        else if (t == "box") b.shape = STP_BOX;
+        else return parse_fail(line, "unknown shape '" + t + "'");
+      } else if (key == "static") {
+        double v;
+        rc = nums(&v, 1);
+        b.is_static = v != 0;
+      } else if (key == "radius") rc = nums(&b.radius, 1);
+      else if (key == "half_length") rc = nums(&b.half_length, 1);
+      else if (key == "half_extents") rc = nums(b.half_extents, 3);
+      else if (key == "local_pos") rc = nums(b.local_pos, 3);
+      else if (key == "local_rot") rc = nums(b.local_rot, 4);
+      else if (key == "mass") rc = nums(&b.mass, 1);
+      else if (key == "inertia") rc = nums(b.inertia_diag, 3);
+      else if (key == "rest") rc = nums(m.rest_state[m.n_bodies - 1], STP_STATE_STRIDE);
+      else return parse_fail(line, "unknown body field '" + key + "'");
+    } else if (open == JOINT) {
+      stp_joint& j = m.joints[m.n_joints - 1];
+      if (key == "end") open = NONE;
+      else if (key == "parent") ls >> joint_ends.back().first;
+      else if (key == "child") ls >> joint_ends.back().second;
+      else if (key == "anchor_parent") rc = nums(j.anchor_parent, 3);
+      else if (key == "anchor_child") rc = nums(j.anchor_child, 3);
+      else if (key == "axis_parent") rc = nums(j.axis_parent, 3);
+      else if (key == "axis_child") rc = nums(j.axis_child, 3);
+      else if (key == "rest_relative") rc = nums(j.rest_relative, 4);
+      else if (key == "limit") {
+        double v[2];
+        rc = nums(v, 2);
+        j.limit_lo = v[0];
+        j.limit_hi = v[1];
+      } else return parse_fail(line, "unknown joint field '" + key + "'");
+    } else if (key == "name") {
+      std::string nm;
+      std::getline(ls >> std::ws, nm);
+      std::strncpy(m.name, nm.c_str(), sizeof(m.name) - 1);
+    } else if (key == "alive_bonus") rc = nums(&m.alive_bonus, 1);
+    else if (key == "fall_height") rc = nums(&m.fall_height, 1);
+    else if (key == "body") {
+      std::string nm;
+      if (!(ls >> nm)) return parse_fail(line, "body without a name");
+      if (body_id.count(nm)) return parse_fail(line, "duplicate body '" + nm + "'");
+      if (m.n_bodies >= STP_MAX_BODIES) return parse_fail(line, "more than 32 bodies");
+      body_id[nm] = m.n_bodies;
+      stp_body& b = m.bodies[m.n_bodies++];
+      b.local_rot[0] = 1.0;
+      m.rest_state[m.n_bodies - 1][3] = 1.0;
+      open = BODY;
+    } else if (key == "joint") {
+      std::string nm;
+      if (!(ls >> nm)) return parse_fail(line, "joint without a name");
+      if (joint_id.count(nm)) return parse_fail(line, "duplicate joint '" + nm + "'");
+      if (m.n_joints >= STP_MAX_JOINTS) return parse_fail(line, "more than 31 joints");
+      joint_id[nm] = m.n_joints;
+      stp_joint& j = m.joints[m.n_joints++];
+      j.rest_relative[0] = 1.0;
+      joint_ends.emplace_back();
+      joint_line.push_back(line);
+      has_tau.push_back(false);
+      open = JOINT;
+    } else if (key == "actuator") {
+      std::string jn;
+      double tau;
+      if (!(ls >> jn >> tau)) return parse_fail(line, "expected 'actuator <joint> <tau_max>'");
+      auto it = joint_id.find(jn);
+      if (it == joint_id.end()) return parse_fail(line, "actuator of unknown joint '" + jn + "'");
+      m.joints[it->second].max_torque = tau;
+      has_tau[it->second] = true;
+    } else if (key == "foot") {
+      std::string bn;
+      ls >> bn;
+      auto it = body_id.find(bn);
+      if (it == body_id.end()) return parse_fail(line, "foot of unknown body '" + bn + "'");
+      if (m.n_feet >= STP_MAX_FEET) return parse_fail(line, "more than 4 feet");
+      m.feet[m.n_feet++] = it->second;
+    } else if (key == "root") {
+      if (!(ls >> root_name)) return parse_fail(line, "root without a body name");
+      has_root = true;
+    } else {
+      return parse_fail(line, "unknown keyword '" + key + "'");
+    }
+    if (rc != STP_OK) return rc;
+  }
+  if (!header) return parse_fail(0, "empty document (expected 'stampede-model 1')");
+  if (open != NONE) return parse_fail(line, "unterminated stanza (missing 'end')");
+  if (!has_root) return parse_fail(0, "missing field 'root'");
+  auto rb = body_id.find(root_name);
+  if (rb == body_id.end()) return parse_fail(0, "root names unknown body '" + root_name + "'");
+  m.root = rb->second;
+  for (int j = 0; j < m.n_joints; ++j) {
+    auto pa = body_id.find(joint_ends[j].first), ch = body_id.find(joint_ends[j].second);
+    if (pa == body_id.end() || ch == body_id.end())
+      return parse_fail(joint_line[j], "joint needs known 'parent' and 'child' bodies");
+    m.joints[j].parent = pa->second;
+    m.joints[j].child = ch->second;
+    if (!has_tau[j]) return parse_fail(joint_line[j], "joint without an 'actuator' (tau_max)");
+  }
+  // the joint graph must be a tree: each body has at most one parent and
+  // following parents from any body ends at a body without one (no cycle)
+  std::vector<int> parent(m.n_bodies, -1);
+  for (int j = 0; j < m.n_joints; ++j) {
+    const int c = m.joints[j].child;
+    if (parent[c] >= 0) return parse_fail(joint_line[j], "body has two parent joints");
+    parent[c] = m.joints[j].parent;
+  }
+  for (int b = 0; b < m.n_bodies; ++b) {
+    int x = b;
+    for (int steps = 0; x >= 0; ++steps) {
+      if (steps > m.n_bodies) return parse_fail(0, "cyclic joint graph");
+      x = parent[x];
+    }
+  }
+  for (int b = 0; b < m.n_bodies; ++b)
+    if (!m.bodies[b].is_static && !(m.bodies[b].mass > 0))
+      return parse_fail(0, "body " + std::to_string(b) + ": nonpositive mass");
+  const int rc = stp_validate_model(&m);
+  if (rc != STP_OK) return rc;
+  *out = m;
+  return STP_OK;
+}
+
+extern "C" int stp_model_to_text(const stp_model* m, char* buf, int32_t capacity, int32_t* length) {
+  if (!m) return stp::fail(STP_EINVAL, "serialize_model: null model");
+  std::string o;
+  char t[256];
+  auto num = [&](double v) {
+    std::snprintf(t, sizeof t, " %.17g", v);
+    o += t;
+  };
+  auto vec = [&](const char* k, const double* v, int n) {
+    o += "  ";
+    o += k;
+    for (int i = 0; i < n; ++i) num(v[i]);
+    o += "\n";
+  };
+  o += "stampede-model 1\n";
+  o += "name " + std::string(m->name, strnlen(m->name, sizeof(m->name))) + "\n";
+  o += "alive_bonus";
+  num(m->alive_bonus);
+  o += "\nfall_height";
+  num(m->fall_height);
+  o += "\n";
+  static const char* shapes[] = {"sphere", "capsule", "box"};
+  for (int b = 0; b < m->n_bodies; ++b) {
+    const stp_body& d = m->bodies[b];
+    o += "body b" + std::to_string(b) + "\n";
+    o += std::string("  shape ") + shapes[d.shape] + "\n";
+    o += "  static " + std::to_string(d.is_static) + "\n";
+    vec("radius", &d.radius, 1);
+    vec("half_length", &d.half_length, 1);
+    vec("half_extents", d.half_extents, 3);
+    vec("local_pos", d.local_pos, 3);
+    vec("local_rot", d.local_rot, 4);
+    vec("mass", &d.mass, 1);
+    vec("inertia", d.inertia_diag, 3);
+    vec("rest", m->rest_state[b], STP_STATE_STRIDE);
+    o += "end\n";
+  }
+  for (int j = 0; j < m->n_joints; ++j) {
+    const stp_joint& d = m->joints[j];
+    o += "joint j" + std::to_string(j) + "\n";
+    o += "  parent b" + std::to_string(d.parent) + "\n";
+    o += "  child b" + std::to_string(d.child) + "\n";
+    vec("anchor_parent", d.anchor_parent, 3);
+    vec("anchor_child", d.anchor_child, 3);
+    vec("axis_parent", d.axis_parent, 3);
+    vec("axis_child", d.axis_child, 3);
+    vec("rest_relative", d.rest_relative, 4);
+    const double lim[2] = {d.limit_lo, d.limit_hi};
+    vec("limit", lim, 2);
+    o += "end\n";
+  }
+  for (int j = 0; j < m->n_joints; ++j) {
+    o += "actuator j" + std::to_string(j);
+    num(m->joints[j].max_torque);
+    o += "\n";
+  }
+  for (int f = 0; f < m->n_feet; ++f) o += "foot b" + std::to_string(m->feet[f]) + "\n";
+  o += "root b" + std::to_string(m->root) + "\n";
+  if (length) *length = int32_t(o.size());
+  if (buf && capacity > 0) {
+    const size_t n = std::min<size_t>(o.size(), size_t(capacity) - 1);
+    std::memcpy(buf, o.data(), n);
+    buf[n] = '\0';
+  }
+  return STP_OK;
+}
