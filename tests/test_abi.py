@@ -97,3 +97,26 @@ def test_terrain_generation_deterministic_and_in_range():
         assert a[i].center[2] == a[i].half_extents[2]
     spec.count = 0
     assert lib.stp_generate_terrain(C.byref(spec), a, 500) == 0
+
+
+def test_terrain_generation_is_uniform():
+    """10^4 samples -> every dimension inside its declared range
+    and Kolmogorov-Smirnov vs uniform passes at alpha = 0.01 (dims, x, y, yaw)."""
+    from scipy import stats
+    lib = abi.load()
+    n = 10000
+    spec = abi.TerrainSpec(count=n, dim_lo=0.2, dim_hi=1.0, x_lo=-30, x_hi=70, y_lo=-5, y_hi=5, yaw_lo=0,
+                           yaw_hi=3.141592653589793, seed=2024)
+    out = (abi.StaticBox * n)()
+    assert lib.stp_generate_terrain(C.byref(spec), out, n) == n
+    cols = {
+        "dim_x": ([2 * out[i].half_extents[0] for i in range(n)], 0.2, 1.0),
+        "dim_y": ([2 * out[i].half_extents[1] for i in range(n)], 0.2, 1.0),
+        "dim_z": ([2 * out[i].half_extents[2] for i in range(n)], 0.2, 1.0),
+        "x": ([out[i].center[0] for i in range(n)], -30.0, 70.0),
+        "y": ([out[i].center[1] for i in range(n)], -5.0, 5.0),
+        "yaw": ([out[i].yaw for i in range(n)], 0.0, 3.141592653589793),
+    }
+    for name, (v, lo, hi) in cols.items():
+        assert lo <= min(v) and max(v) <= hi, name
+        assert stats.kstest(v, "uniform", args=(lo, hi - lo)).pvalue > 0.01, name
