@@ -15,7 +15,7 @@ rows = list(csv.reader(io.StringIO(raw)))
 h = rows[1]; R = rows[2:]
 ia = h.index("Instructions Executed"); ist = h.index("Warp Stall Sampling (All Samples)")
 txt = open('/tmp/spill.sass').read()
-KERNEL = sys.argv[sys.argv.index('--kernel') + 1] if '--kernel' in sys.argv else '_ZN3stp10k_env_stepIfLi32ELi2E'
+KERNEL = sys.argv[sys.argv.index('--kernel') + 1] if '--kernel' in sys.argv else '_ZN3stp10k_env_stepIfLi32ELi2ELb0E'
 fn = [p for p in re.split(r'//-+ \.text\.', txt) if p.startswith(KERNEL)][0]
 ins = []; cur = None
 for ln in fn.splitlines():
