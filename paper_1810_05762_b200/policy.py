@@ -84,8 +84,9 @@ class RunningStat:
 
     @property
     def std(self):
+        """max(std, 1e-6) of the count-based variance M2 / n (whiten)."""
         var = self.m2 / torch.clamp(self.n, min=1.0)
-        return torch.sqrt(var + 1e-8)
+        return torch.clamp(torch.sqrt(var), min=1e-6)
 
     def whiten(self, x):
         return torch.clamp((x - self.mean.to(x.dtype)) / self.std.to(x.dtype), -10.0, 10.0)

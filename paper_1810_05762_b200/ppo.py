@@ -11,7 +11,9 @@ observation RunningStat is merged across ranks once per iteration
 """
 from __future__ import annotations
 
+import copy
 import dataclasses
+import math
 
 import torch
 import torch.distributed as dist
@@ -89,20 +91,35 @@ class PPOLearner:
         self.opt = torch.optim.Adam(model.parameters(), lr=cfg.lr)
         broadcast_params(model)
 
-    def update(self, xw, actions, old_logp, adv, ret, generator: torch.Generator | None = None):
-        """Clipped-surrogate PPO epochs with KL-adaptive step size.
-        xw: whitened obs [B, O]; all tensors flat over (time, agents) of this rank."""
+    def update(self, xw, actions, old_logp=None, adv=None, ret=None, generator: torch.Generator | None = None):
+        """ppo_update on the whitened batch xw [B, O] of this
+        rank (time x agents flattened).  The old policy is snapshotted on the
+        same whitened batch before the first epoch (its log-probs, not the
+        rollout's, which were taken under the previous observation statistics);
+        clipped-surrogate + value epochs over shuffled minibatches with every
+        gradient averaged across ranks; then KL(old || new) of the diagonal
+        Gaussians, averaged over states and ranks, adapts the learning rate
+        once (adapt_learning_rate, :468-475).  A non-finite loss restores the
+        snapshot, halves the learning rate and reports `aborted`."""
         cfg = self.cfg
+        del old_logp  # re-derived from the snapshot below
         adv = global_normalize(adv)
         B = xw.shape[0]
+        with torch.no_grad():
+            mu_old = self.model.pi(xw)
+            ls_old = self.model.log_std.detach().clone()
+            old_logp = gaussian_logp(actions, mu_old, ls_old)
+            snapshot = [p.detach().clone() for p in self.model.parameters()]
+            opt_state = copy.deepcopy(self.opt.state_dict())
         # Table 4: frames per iteration / minibatch size per agent = minibatches per epoch
         n_mb = max(1, cfg.frames_per_iter // max(1, cfg.minibatch_per_agent))
         mb = max(1, B // n_mb)
-        stats = {}
+        lr = self.opt.param_groups[0]["lr"]
+        loss = torch.zeros((), device=xw.device)
         for epoch in range(cfg.epochs):
             perm = torch.randperm(B, generator=generator, device="cpu").to(xw.device)
-            for s in range(0, B, mb):
-                idx = perm[s:s + mb]
+            for s0 in range(0, B, mb):
+                idx = perm[s0:s0 + mb]
                 logp = self.model.log_prob(xw[idx], actions[idx])
                 ratio = torch.exp(logp - old_logp[idx])
                 a = adv[idx]
@@ -110,24 +127,52 @@ class PPOLearner:
                 v = self.model.v(xw[idx]).squeeze(-1)
                 vf = ((v - ret[idx]) ** 2).mean()
                 loss = pg + cfg.vf_coef * vf
+                ok = torch.isfinite(loss).to(torch.float32)
+                if _dist():
+                    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                if ok.item() < 1.0:  # abort: restore the snapshot, halve the learning rate
+                    with torch.no_grad():
+                        for p_, s_ in zip(self.model.parameters(), snapshot):
+                            p_.copy_(s_)
+                    self.opt.load_state_dict(opt_state)
+                    lr = max(lr / 2.0, 1e-6)
+                    for g in self.opt.param_groups:
+                        g["lr"] = lr
+                    return {"kl": 0.0, "lr": lr, "loss": float("nan"), "aborted": True}
                 self.opt.zero_grad(set_to_none=False)
                 loss.backward()
                 allreduce_mean_grads(self.model)
                 self.opt.step()
-            with torch.no_grad():  # KL-adaptive learning rate
-                kl = (old_logp - self.model.log_prob(xw, actions)).mean()
-                if _dist():
-                    dist.all_reduce(kl, op=dist.ReduceOp.SUM)
-                    kl /= dist.get_world_size()
-                lr = self.opt.param_groups[0]["lr"]
-                if kl > 2.0 * cfg.desired_kl:
-                    lr = max(lr / 1.5, 1e-6)
-                elif kl < 0.5 * cfg.desired_kl:
-                    lr = min(lr * 1.5, 1e-2)
-                for g in self.opt.param_groups:
-                    g["lr"] = lr
-                stats = {"kl": float(kl), "lr": lr, "loss": float(loss)}
-        return stats
+        with torch.no_grad():
+            kl = gaussian_kl(mu_old, ls_old, self.model.pi(xw), self.model.log_std).mean()
+            if _dist():
+                dist.all_reduce(kl, op=dist.ReduceOp.SUM)
+                kl /= dist.get_world_size()
+            lr = adapt_learning_rate(lr, float(kl), cfg.desired_kl)
+            for g in self.opt.param_groups:
+                g["lr"] = lr
+        return {"kl": float(kl), "lr": lr, "loss": float(loss), "aborted": False}
+
+
+def adapt_learning_rate(lr: float, measured_kl: float, desired_kl: float) -> float:
+    """adapt_learning_rate: /1.5 above 2x the target KL, x1.5
+    below half of it, clamped to [1e-6, 1e-2]."""
+    if measured_kl > 2.0 * desired_kl:
+        lr = lr / 1.5
+    elif measured_kl < 0.5 * desired_kl:
+        lr = lr * 1.5
+    return min(max(lr, 1e-6), 1e-2)
+
+
+def gaussian_logp(actions, mu, log_std):
+    """log N(actions; mu, exp(log_std)^2) summed over action dims."""
+    return (-0.5 * ((actions - mu) / torch.exp(log_std)) ** 2 - log_std - 0.5 * math.log(2 * math.pi)).sum(-1)
+
+
+def gaussian_kl(mu0, ls0, mu1, ls1):
+    """KL(N0 || N1) of diagonal Gaussians per state (kl_diag_gaussian)."""
+    v0, v1 = torch.exp(2 * ls0), torch.exp(2 * ls1)
+    return (ls1 - ls0 + (v0 + (mu0 - mu1) ** 2) / (2 * v1) - 0.5).sum(-1)
 
 
 def rollout(env, kernel, obs_stat: RunningStat, frames: int, seed: int, step0: int, env_offset: int = 0):

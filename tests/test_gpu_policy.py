@@ -37,3 +37,16 @@ def test_policy_kernel_matches_torch_fp32(name, obs_dim, act_dim, n):
     lp_ref = model.log_prob(xw, act).detach()
     # log-prob of the sample under the kernel's own mean
     assert (logp - lp_ref).abs().max() <= 0.05 + 0.05 * lp_ref.abs().max()
+
+
+def test_train_loop_runs(capsys):
+    """Config C5 on one GPU (paper_1810_05762_b200.train): rollout on the fused
+    step kernel + tcgen05 policy forward, GAE, whitening, PPO update; every
+    iteration finite, not aborted, KL >= 0."""
+    import json
+    from paper_1810_05762_b200 import train
+    train.main(["--iters", "2", "--envs", "256", "--epochs", "2", "--frames", "8"])
+    rows = [json.loads(l) for l in capsys.readouterr().out.splitlines() if l.startswith("{")]
+    assert len(rows) == 2
+    for r in rows:
+        assert not r["aborted"] and r["kl"] >= 0 and np.isfinite(r["loss"]) and np.isfinite(r["mean_reward"])

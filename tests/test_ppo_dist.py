@@ -81,8 +81,12 @@ def test_gloo_two_rank_ppo_update_matches_union():
     xw, act, old, adv, ret = _data()
     # the union minibatch gradient = mean of the two shard gradients (equal sizes)
     cfg = learner.cfg
-    from paper_1810_05762_b200.ppo import global_normalize
+    from paper_1810_05762_b200.ppo import gaussian_kl, gaussian_logp, global_normalize
     advn = global_normalize(adv)
+    del old  # ppo_update snapshots the old policy on the whitened batch
+    with torch.no_grad():
+        mu_old, ls_old = model.pi(xw), model.log_std.detach().clone()
+        old = gaussian_logp(act, mu_old, ls_old)
     for epoch in range(cfg.epochs):
         grads = None
         for r in range(2):
@@ -99,12 +103,9 @@ def test_gloo_two_rank_ppo_update_matches_union():
         for p, g in zip(model.parameters(), grads):
             p.grad.copy_(g / 2)
         learner.opt.step()
-        with torch.no_grad():
-            kl = (old - model.log_prob(xw, act)).mean()
-            lr = learner.opt.param_groups[0]["lr"]
-            lr = max(lr / 1.5, 1e-6) if kl > 2 * cfg.desired_kl else (min(lr * 1.5, 1e-2) if kl < 0.5 * cfg.desired_kl else lr)
-            for gp in learner.opt.param_groups:
-                gp["lr"] = lr
+    with torch.no_grad():  # one learning-rate adaptation after the update (:468-475)
+        kl = gaussian_kl(mu_old, ls_old, model.pi(xw), model.log_std).mean()
+        assert kl >= 0
     flat = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).numpy()
     np.testing.assert_allclose(params[0], flat, rtol=1e-5, atol=1e-6)
     # RunningStat merge == statistics of the concatenated stream
@@ -130,3 +131,28 @@ def test_gae_matches_recursion():
             delta = r[t, n] + 0.99 * nv * nt - v[t, n]
             a = delta + 0.99 * 0.95 * nt * a
             assert abs(float(adv[t, n]) - float(a)) < 1e-5
+
+
+def test_adapt_learning_rate_spec_examples():
+    """SPEC.md:471-474 with desired KL 0.01."""
+    from paper_1810_05762_b200.ppo import adapt_learning_rate
+    assert abs(adapt_learning_rate(3e-4, 0.05, 0.01) - 3e-4 / 1.5) < 1e-15
+    assert abs(adapt_learning_rate(3e-4, 0.001, 0.01) - 3e-4 * 1.5) < 1e-15
+    assert adapt_learning_rate(3e-4, 0.01, 0.01) == 3e-4
+    assert adapt_learning_rate(1e-2, 0.0, 0.01) == 1e-2 and adapt_learning_rate(1e-6, 9.0, 0.01) == 1e-6
+
+
+def test_zero_advantages_leave_the_policy_unchanged_and_kl_nonnegative():
+    """zero advantages -> the policy loss term has zero
+    gradient (only the value net moves); the reported KL is >= 0."""
+    torch.manual_seed(3)
+    model = ActorCritic(O, A, hidden=(16, 16, 8))
+    learner = PPOLearner(model, _cfg())
+    xw, act, old, adv, ret = _data()
+    pi0 = [p.detach().clone() for p in model.pi.parameters()] + [model.log_std.detach().clone()]
+    v0 = [p.detach().clone() for p in model.v.parameters()]
+    st = learner.update(xw, act, old, torch.zeros_like(adv), ret)
+    assert st["kl"] >= 0.0 and not st["aborted"]
+    for p, q in zip(list(model.pi.parameters()) + [model.log_std], pi0):
+        assert torch.equal(p.detach(), q)
+    assert any(not torch.equal(p.detach(), q) for p, q in zip(model.v.parameters(), v0))
