@@ -151,7 +151,7 @@ class PPOLearner:
             lr = adapt_learning_rate(lr, float(kl), cfg.desired_kl)
             for g in self.opt.param_groups:
                 g["lr"] = lr
-        return {"kl": float(kl), "lr": lr, "loss": float(loss), "aborted": False}
+        return {"kl": float(kl), "lr": lr, "loss": float(loss.detach()), "aborted": False}
 
 
 def adapt_learning_rate(lr: float, measured_kl: float, desired_kl: float) -> float:
