@@ -268,6 +268,48 @@ def run_ours(args, world, rank, local):
     except Exception as ex:
         rollout = {"error": repr(ex)}
 
+    # ---- config C5: PPO iterations (rollout of 32 frames + 20-epoch update with
+    # the per-minibatch gradient allreduce), host-timed after one warm-up
+    # iteration; informational (the metric above is the env step)
+    ppo = None
+    try:
+        from paper_1810_05762_b200.ppo import PPOConfig, PPOLearner, gae
+        from paper_1810_05762_b200.ppo import rollout as ppo_rollout
+        torch.manual_seed(0)
+        pmodel = ActorCritic(env.obs_dim, env.action_dim, HIDDEN[TASK]).to(dev)
+        pcfg = PPOConfig()
+        learner = PPOLearner(pmodel, pcfg)
+        pkern = PolicyKernel(pmodel, dev)
+        pst = RunningStat(env.obs_dim, device=dev)
+        env.last_obs = env.reset()
+        pst.push(env.last_obs)
+        times = []
+        for it in range(3):
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            data, last_val = ppo_rollout(env, pkern, pst, pcfg.frames_per_iter, SEED, 1000 + it * pcfg.frames_per_iter,
+                                         env_offset=rank * N_ENVS)
+            loc = RunningStat(env.obs_dim, device=dev)
+            loc.push(data["obs"].reshape(-1, env.obs_dim))
+            if world > 1:
+                pst.merge_allreduce(loc)
+            else:
+                pst._merge(loc.n, loc.mean, loc.m2)
+            adv, ret = gae(data["rew"], data["val"], data["done"], last_val, pcfg.gamma, pcfg.lam)
+            stats = learner.update(pst.whiten(data["obs"].reshape(-1, env.obs_dim)),
+                                   data["act"].reshape(-1, env.action_dim), None, adv.reshape(-1), ret.reshape(-1))
+            pkern.refresh()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        it_s = statistics.median(times[1:])
+        frames = pcfg.frames_per_iter * N_ENVS * world
+        ppo = {"iteration_s": it_s, "frames_per_iteration": frames, "env_steps_per_s_with_update": frames / it_s,
+               "epochs": pcfg.epochs, "kl": stats["kl"], "aborted": stats["aborted"], "clock": "host, median of 2"}
+    except Exception as ex:
+        ppo = {"error": repr(ex)}
+
     # ---- e2e through the reference-facing C-ABI call with pinned host buffers:
     # each step's actions sit in their own pinned buffer (as a policy writing
     # into host memory would leave them), and stp_step_host is called with raw
@@ -331,7 +373,7 @@ def run_ours(args, world, rank, local):
                            "l2": "flushed between timed steps (256 MiB write)", "auto_reset": True},
                 "e2e": {"value": e2e_value, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "path": "stp_step_host (pinned host buffers)"},
-                "gpu_launches": K, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "rollout": rollout,
+                "gpu_launches": K, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "rollout": rollout, "ppo": ppo,
                 "wall_s_timed_region": wall, "failed_envs_last_step": failed}
         print(json.dumps(line), flush=True)
     env.close()
