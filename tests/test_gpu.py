@@ -341,3 +341,30 @@ def test_step_host_pipelined_matches_device_step(n):
         np.testing.assert_array_equal(rd.cpu().numpy(), rh)
         np.testing.assert_array_equal(dd.cpu().numpy(), dh)
     np.testing.assert_array_equal(a.get_state(), b.get_state())
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_divergent_env_is_rolled_back_and_flagged(precision):
+    """solver.cpp:580-593 / SPEC.md:274: a non-finite step restores the env's
+    pre-step state and reports it failed (env_step: done, reward 0); the
+    other envs step normally.  (The reference throws on a non-finite system,
+    krylov.cpp:113-114; here the env is rolled back.)"""
+    import torch
+    task = abi.default_task(abi.TASK_HUMANOID)
+    task.auto_reset = 0
+    g = VecEnv(model=abi.builtin_model("humanoid"), task_config=task, step_config=abi.default_step_config(),
+               n_envs=4, precision=precision, seed=3)
+    g.reset()
+    s0 = g.get_state()
+    loads = np.zeros((4, g.n_bodies, 6))
+    loads[1, g.model.root, 0] = np.inf
+    g.set_external_loads(loads)
+    obs, rew, done = g.step(torch.zeros((4, g.action_dim), device="cuda"))
+    torch.cuda.synchronize()
+    rep = g.report()
+    s1 = g.get_state()
+    assert rep["failed"][1] == 1 and rep["failed"][[0, 2, 3]].sum() == 0
+    np.testing.assert_array_equal(s1[1], s0[1])
+    assert not np.array_equal(s1[0], s0[0])
+    d, r = done.cpu().numpy(), rew.cpu().numpy()
+    assert d[1] == 1 and r[1] == 0.0 and d[[0, 2, 3]].sum() == 0
