@@ -705,40 +705,45 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
             nrm = {cs * ln.x - sn * ln.y, sn * ln.x + cs * ln.y, ln.z};
             return -best;
           };
-          v3<T> nrm, surf;
-          if (shp == STP_SPHERE) {
-            const T d = point_box(p0, nrm, surf);
-            if (d - rad < margin) add_contact(surf, nrm, d - rad, 4 * i);
-          } else {
-            // collide_capsule_obb, collide.cpp:183-214
-            const v3<T> seg = p1 - p0;
+          // one point_box call site per phase (code size: this runs inside the
+          // step kernel, whose instruction working set is its bottleneck on
+          // terrain): sphere = 1 query at p0 (collide_sphere_obb :175-181);
+          // capsule (collide_capsule_obb :183-214) = 32-step ternary search on
+          // t, then the mid point and the two end points in that order
+          const v3<T> seg = p1 - p0;
+          T tmid = T(0);
+          if (shp != STP_SPHERE) {
             T lo_t = 0, hi_t = 1;
+#pragma unroll 1
             for (int it = 0; it < 32; ++it) {
               const T m1 = lo_t + (hi_t - lo_t) / T(3), m2 = hi_t - (hi_t - lo_t) / T(3);
-              v3<T> n1, s1;
-              const T d1 = point_box(p0 + seg * m1, n1, s1);
-              const T d2 = point_box(p0 + seg * m2, n1, s1);
-              if (d1 <= d2) hi_t = m2;
+              T dq[2];
+#pragma unroll 1
+              for (int q = 0; q < 2; ++q) {
+                v3<T> n1, s1;
+                dq[q] = point_box(p0 + seg * (q == 0 ? m1 : m2), n1, s1);
+              }
+              if (dq[0] <= dq[1]) hi_t = m2;
               else lo_t = m1;
             }
-            const T tmid = T(0.5) * (lo_t + hi_t);
-            bool mid_added = false;
-            {
-              const T d = point_box(p0 + seg * tmid, nrm, surf);
-              if (d - rad < margin) {
-                add_contact(surf, nrm, d - rad, 4 * i);
-                mid_added = true;
-              }
-            }
-            for (int te = 0; te < 2; ++te) {
-              const T tt = T(te);
-              if (mid_added && fabs(tt - tmid) < T(0.05)) continue;
-              const T d = point_box(p0 + seg * tt, nrm, surf);
-              if (d - rad < margin) add_contact(surf, nrm, d - rad, 4 * i + 1 + te);
+            tmid = T(0.5) * (lo_t + hi_t);
+          }
+          bool mid_added = false;
+          const int nq = shp == STP_SPHERE ? 1 : 3;
+#pragma unroll 1
+          for (int q = 0; q < nq; ++q) {
+            const T tt = q == 0 ? tmid : T(q - 1);  // mid (sphere: p0), then t = 0, 1
+            if (q > 0 && mid_added && fabs(tt - tmid) < T(0.05)) continue;
+            v3<T> nrm, surf;
+            const T d = point_box(q == 0 && shp == STP_SPHERE ? p0 : p0 + seg * tt, nrm, surf);
+            if (d - rad < margin) {
+              add_contact(surf, nrm, d - rad, 4 * i + q);
+              if (q == 0) mid_added = true;
             }
           }
         };
-        if (a.grid_nx > 0) {
+        {
+          // (stp_set_terrain builds the grid whenever there are boxes)
           // uniform-grid broadphase over the boxes' loose footprints; each box is
           // visited once (in the first shared cell) and the slots are re-sorted
           // by (box index, mid/end) afterwards: the reference's all-boxes loop
@@ -774,8 +779,6 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
               }
             }
           }
-        } else {
-          for (int i = 0; i < a.n_boxes; ++i) test_box(i);
         }
       }
     }
