@@ -1040,13 +1040,14 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
       S[9] = cf.kc * (wsum > T(1e-12) ? T(1) / wsum : T(0));
       S[10] = uni_bias(sep, cf.beta, cf.dt);
     };
-#pragma unroll
-    for (int k = 0; k < CPB; ++k) {
-      if (k < nc) contact_row(L.template slot<CPB>(k));
-    }
-    if constexpr (CT > CPB) {
+    if constexpr (CT > CPB) {  // terrain: one call site (instruction working set)
 #pragma unroll 1
-      for (int k = CPB; k < nc; ++k) contact_row(L.template slot<CPB>(k));
+      for (int k = 0; k < nc; ++k) contact_row(L.template slot<CPB>(k));
+    } else {
+#pragma unroll
+      for (int k = 0; k < CPB; ++k) {
+        if (k < nc) contact_row(L.template slot<CPB>(k));
+      }
     }
     // inter-agent contact rows (island mode; collide.cpp:251-266, rows
     // solver.cpp:176-210): slots in the reference's contact order, lever arms,
@@ -1224,13 +1225,14 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
             }
           }
         };
-#pragma unroll
-        for (int k = 0; k < CPB; ++k) {
-          if (k < nc) contact_newton(L.template slot<CPB>(k));
-        }
-        if constexpr (CT > CPB) {
+        if constexpr (CT > CPB) {  // terrain: one call site (instruction working set)
 #pragma unroll 1
-          for (int k = CPB; k < nc; ++k) contact_newton(L.template slot<CPB>(k));
+          for (int k = 0; k < nc; ++k) contact_newton(L.template slot<CPB>(k));
+        } else {
+#pragma unroll
+          for (int k = 0; k < CPB; ++k) {
+            if (k < nc) contact_newton(L.template slot<CPB>(k));
+          }
         }
         if constexpr (ISL) {
           // inter-agent rows at the iterate: partners' velocities through the
