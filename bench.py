@@ -182,7 +182,7 @@ def run_reference(args, world, rank):
     r = cpu_reference_rate(N_ENVS, max(1, args.steps), max(0, args.warmup), threads, budget_s=90.0)
     line = {"metric": "env-steps/sec (Humanoid, 4096 envs/GPU)", "value": r["value"], "unit": "env-steps/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": 1e3 * N_ENVS / r["value"] if r["value"] else None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": "humanoid_run_flat_4096envs_random_actions", "envs_per_gpu": N_ENVS,
                        "task": TASK, "parallelism": "cpu-threads"},
