@@ -62,7 +62,7 @@ __global__ void k_shapes_warp(const DevModel<T>* __restrict__ Mp, const T* __res
                               const double* __restrict__ origin, int n, int W, WShape* __restrict__ ws,
                               double* __restrict__ env_box, int2* __restrict__ env_cell, int* __restrict__ bin_count,
                               int* __restrict__ bins, unsigned hmask, int* __restrict__ ovf, int* __restrict__ n_ovf,
-                              int* __restrict__ max_ext_bits) {
+                              int* __restrict__ max_ext_bits, int* __restrict__ xcount) {
   const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, b = threadIdx.x & 31;
   if (e >= n) return;
   const DevModel<T>& M = *Mp;
@@ -70,21 +70,25 @@ __global__ void k_shapes_warp(const DevModel<T>* __restrict__ Mp, const T* __res
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
   if (b < B) {
     WShape s{};
+    if (xcount) xcount[size_t(e) * B + b] = 0;  // this step's cross-contact slots (step path)
     const size_t sb = size_t(e) * kStateFields * W + b;
-    auto st = [&](int f) { return double(state[sb + size_t(f) * W]); };
-    const v3<double> x{st(0) + origin[2 * e], st(1) + origin[2 * e + 1], st(2)};
-    const qt<double> q{st(3), st(4), st(5), st(6)};
-    const qt<double> lr{double(M.lrot[0][b]), double(M.lrot[1][b]), double(M.lrot[2][b]), double(M.lrot[3][b])};
-    const v3<double> lp{double(M.lpos[0][b]), double(M.lpos[1][b]), double(M.lpos[2][b])};
-    const qt<double> rot = qmul(q, lr);
-    const v3<double> pos = x + qrot(q, lp);
+    auto st = [&](int f) { return state[sb + size_t(f) * W]; };
+    // rotations in the handle's precision (world_shape, collide.cpp:38-78),
+    // the env origin added in double
+    const v3<T> xr{st(0), st(1), st(2)};
+    const qt<T> q{st(3), st(4), st(5), st(6)};
+    const qt<T> lr{M.lrot[0][b], M.lrot[1][b], M.lrot[2][b], M.lrot[3][b]};
+    const v3<T> lp{M.lpos[0][b], M.lpos[1][b], M.lpos[2][b]};
+    const qt<T> rot = qmul(q, lr);
+    const v3<T> off = qrot(q, lp);
+    v3<T> ax{T(0), T(0), T(0)};
+    if (M.shape[b] == STP_CAPSULE) ax = qrot(rot, v3<T>{T(0), T(0), M.half_len[b]});
+    const double ox = origin[2 * e], oy = origin[2 * e + 1];
+    const v3<double> x{ox + double(xr.x), oy + double(xr.y), double(xr.z)};
+    const v3<double> pos{x.x + double(off.x), x.y + double(off.y), x.z + double(off.z)};
     const double r = double(M.radius[b]);
-    v3<double> p0 = pos, p1 = pos;
-    if (M.shape[b] == STP_CAPSULE) {
-      const v3<double> ax = qrot(rot, v3<double>{0.0, 0.0, double(M.half_len[b])});
-      p0 = pos - ax;
-      p1 = pos + ax;
-    }
+    const v3<double> p0{pos.x - double(ax.x), pos.y - double(ax.y), pos.z - double(ax.z)};
+    const v3<double> p1{pos.x + double(ax.x), pos.y + double(ax.y), pos.z + double(ax.z)};
     s.ok = !M.is_static[b] && M.shape[b] != STP_BOX;
     s.r = r;
     s.x[0] = x.x;
@@ -427,13 +431,13 @@ void pair_scratch_free(PairScratch* p) {
 // current state into P->pairs / P->counters[0]; world shapes into P->ws
 template <class T>
 static cudaError_t broadphase(PairScratch* P, const DevModel<T>* model, const T* state, const double* origin, int n,
-                              int W, double margin, cudaStream_t st) {
+                              int W, double margin, cudaStream_t st, int* xcount = nullptr) {
   cudaError_t e = cudaMemsetAsync(P->bin_count, 0, sizeof(int) * (P->hmask + 1), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(P->gcnt, 0, sizeof(int) * 2, st);
   if (e != cudaSuccess) return e;
   k_shapes_warp<T><<<(n * 32 + 127) / 128, 128, 0, st>>>(model, state, origin, n, W, P->ws, P->env_box, P->env_cell,
                                                          P->bin_count, P->bins, P->hmask, P->ovf, P->gcnt,
-                                                         P->gcnt + 1);
+                                                         P->gcnt + 1, xcount);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_env_query<<<(n * 32 + 127) / 128, 128, 0, st>>>(n, P->env_box, P->env_cell, P->bin_count, P->bins, P->hmask, P->ovf,
@@ -564,8 +568,7 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
   const int edge_cap = n * B * kXSlots;
   STP_CK(cudaMemsetAsync(P->counters, 0, sizeof(int) * 2, st));
   STP_CK(cudaMemsetAsync(P->icnt, 0, sizeof(int) * 3, st));
-  STP_CK(cudaMemsetAsync(P->xcount, 0, sizeof(int) * size_t(n) * B, st));
-  STP_CK(broadphase<T>(P, model, state, origin, n, W, margin, st));
+  STP_CK(broadphase<T>(P, model, state, origin, n, W, margin, st, P->xcount));
   k_narrow_slots<<<148 * 2, 256, 0, st>>>(P->pairs, P->counters, int(P->pair_cap), B, (long long)n * B, P->ws, margin,
                                           P->xslots, P->xcount, P->edges, edge_cap, P->icnt, P->icnt + 2);
   STP_CK(cudaGetLastError());
