@@ -250,20 +250,35 @@ def run_ours(args, world, rank, local):
             _, a, _, _ = kern.forward(obs, m_, s_, seed=SEED, step=s)
             env.step(a.clamp(-1, 1), obs, rew, done)
         torch.cuda.synchronize()
-        r0, r1, p0 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        r0, r1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
         r0.record()
         for s in range(K):
             _, a, _, _ = kern.forward(obs, m_, s_, seed=SEED, step=3 + s)
             env.step(a.clamp(-1, 1), obs, rew, done)
         r1.record()
-        for s in range(K):
-            kern.forward(obs, m_, s_, seed=SEED, step=3 + s)
-        p0.record()
         torch.cuda.synchronize()
         roll_ms = r0.elapsed_time(r1) / K
-        pol_ms = r1.elapsed_time(p0) / K
+        # K4 alone: one CUDA graph of K forwards, so the device time is not
+        # bounded by the host's per-call Python / ctypes overhead
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(dev)
+        cs.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g, stream=cs):
+                for s in range(K):
+                    kern.forward(obs, m_, s_, seed=SEED, step=3 + s)
+        torch.cuda.current_stream(dev).wait_stream(cs)
+        g.replay()
+        torch.cuda.synchronize()
+        q0, q1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+        q0.record()
+        g.replay()
+        q1.record()
+        torch.cuda.synchronize()
+        pol_ms = q0.elapsed_time(q1) / K
         rollout = {"env_steps_per_s": N_ENVS / (roll_ms / 1e3), "ms_per_step": roll_ms,
-                   "policy_forward_ms": pol_ms, "policy": f"tcgen05 SELU MLP pi+V {HIDDEN[TASK]} bf16",
+                   "policy_forward_ms": pol_ms, "policy_forward_timing": "CUDA graph of K forwards, device",
+                   "policy": f"tcgen05 SELU MLP pi+V {HIDDEN[TASK]} bf16",
                    "l2": "not flushed"}
     except Exception as ex:
         rollout = {"error": repr(ex)}

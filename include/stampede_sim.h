@@ -289,7 +289,8 @@ int stp_set_task_state(stp_sim* sim, const double* target, const int32_t* counte
  * dims_* = {in, h1, h2, h3, out} (widths <= 256); w_*[l] = packed bf16
  * weights of layer l, K-major core-matrix layout [ceil16(in)/8][ceil16(out)][8]
  * (paper_1810_05762_b200/policy.py pack_linear); b_*[l] = fp32 bias padded to
- * ceil16(out).  All pointers are device pointers; asynchronous on `stream`.
+ * ceil16(out); weights and biases 16-byte aligned.  All pointers are device
+ * pointers; asynchronous on `stream`.
  * action_out / logp_out / value_out may be NULL. */
 int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_dim, const float* obs_mean,
                        const float* obs_std, const int32_t* dims_pi, const void* const* w_pi,

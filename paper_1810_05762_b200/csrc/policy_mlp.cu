@@ -24,7 +24,7 @@
 namespace {
 
 constexpr int kM = 128;        // rows (envs) per CTA = UMMA M
-constexpr int kThreads = 256;  // 8 warps: warps w and w+4 share TMEM lanes 32(w%4).. by column halves
+constexpr int kThreads = 512;  // 16 warps: warps w, w+4, w+8, w+12 share TMEM lanes 32(w%4).. (16-column chunks round-robin)
 constexpr float kSeluL = 1.0507009873554805f, kSeluA = 1.6732632423543772f;
 
 struct MlpDims {
@@ -123,9 +123,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 
 // SELU with the fast exponential: the result is rounded to bf16 for the next
 // layer anyway (8 significant bits), so __expf's ~2 ulp fp32 error is invisible.
-__device__ __forceinline__ float selu(float x) { return x > 0.f ? kSeluL * x : kSeluL * kSeluA * (__expf(x) - 1.f); }
+// Branch-free: the exponential of min(x, 0) is computed for every lane and
+// selected, so a warp never splits on the sign.
+// __expf(y) is ex2.approx(y * log2 e); the flush-to-zero form skips the
+// denormal-range fixups, which only differ for y < -87 where SELU's negative
+// branch rounds to -lambda*alpha either way.
+__device__ __forceinline__ float selu(float x) {
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fminf(x, 0.f) * 1.4426950408889634f));
+  const float neg = kSeluL * kSeluA * (e - 1.f);
+  return x > 0.f ? kSeluL * x : neg;
+}
 
 // Write 8 bf16 (16 B) of row `row`, K-chunk `kc` into a [k/8][128][8] operand.
+__device__ __forceinline__ int quarter_of(int warp) { return warp >> 2; }
+
 __device__ __forceinline__ void st_chunk(__nv_bfloat16* buf, int kc, int row, const float* x8) {
   __nv_bfloat162 p[4];
 #pragma unroll
@@ -133,12 +145,33 @@ __device__ __forceinline__ void st_chunk(__nv_bfloat16* buf, int kc, int row, co
   *reinterpret_cast<uint4*>(buf + (size_t(kc) * kM + row) * 8) = *reinterpret_cast<uint4*>(p);
 }
 
+// Experiment-only phase timestamps (tools/exp/k4_phases.py builds with
+// -DSTP_K4_PHASES): thread 0 of each CTA records %globaltimer at phase ends.
+#ifdef STP_K4_PHASES
+constexpr int kPhases = 16;
+__device__ unsigned long long g_k4_phase[512 * kPhases];
+__device__ __forceinline__ void phase(int i) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_k4_phase[(blockIdx.y * gridDim.x + blockIdx.x) * kPhases + i] = t;
+  }
+}
+#else
+__device__ __forceinline__ void phase(int) {}
+#endif
+
 struct Smem {
+  uint64_t bar_obs;    // observation tile landed (TMA path)
   uint64_t bar_w;      // weights landed
   uint64_t bar_mma;    // layer accumulator ready
   uint64_t bar_chunk;  // streaming mode: a chunk's MMAs done (weight buffer free)
   uint32_t tmem;
+  float wmean[256];  // whitening: per-column mean and 1 / std of the observation
+  float winv[256];
 };
+constexpr int kHeader = 3072;  // Smem, rounded to the operand alignment
+static_assert(sizeof(Smem) <= kHeader, "Smem header");
 
 // One 4-layer net over the CTA's 128 rows; A operand of layer 0 already in abuf0.
 // Returns with the final accumulator (n[3] columns) in TMEM.
@@ -147,12 +180,13 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
                         bool stream) {
   const int warp = tid >> 5;
   const int row = (warp & 3) * 32 + (tid & 31);  // TMEM lane = tile row
-  const int half = warp >> 2;                    // column half of the epilogue
+  const int quarter = quarter_of(warp);          // epilogue chunk phase (0..3)
   // resident mode: the 4 weight blobs were issued by the caller
   if (!stream) {
     mbar_wait(&sh->bar_w, wphase);
     wphase ^= 1;
   }
+  phase(3);
   uint32_t cphase = 0;  // streaming mode, issuing thread only
   __nv_bfloat16* a_in = abuf0;
   __nv_bfloat16* a_out = abuf1;
@@ -199,21 +233,33 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
     mbar_wait(&sh->bar_mma, mphase);
     mphase ^= 1;
     tc_after_sync();
+    phase(4 + 2 * l);
     if (l == 3) break;
-    // epilogue: bias + SELU -> bf16 -> next operand (this thread's row and column half)
+    // epilogue: bias + SELU -> bf16 -> next operand (this thread's row, every
+    // 4th 16-column chunk)
     const uint32_t tbase = sh->tmem + (uint32_t((warp & 3) * 32) << 16);
-    const int ncols = D.n[l];
-    const int c_lo = ncols >= 32 ? half * (ncols / 2) : 0;
-    const int c_hi = ncols >= 32 ? c_lo + ncols / 2 : (half == 0 ? ncols : 0);
-    for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
-      float v[16];
-      tmem_ld16(tbase + uint32_t(c0), v);
+    const int nch = D.n[l] / 16;
+    for (int j = quarter; j < nch; j += 4) {
+      // bias loads first: their latency overlaps the TMEM load's
+      const float4* b4 = reinterpret_cast<const float4*>(P.bias[l] + 16 * j);
+      float4 bq[4];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = selu(v[i] + P.bias[l][c0 + i]);
-      st_chunk(a_out, c0 / 8, row, v);
-      st_chunk(a_out, c0 / 8 + 1, row, v + 8);
+      for (int q = 0; q < 4; ++q) bq[q] = __ldg(b4 + q);
+      float v[16];
+      tmem_ld16(tbase + uint32_t(16 * j), v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 b = bq[q];
+        v[4 * q] = selu(v[4 * q] + b.x);
+        v[4 * q + 1] = selu(v[4 * q + 1] + b.y);
+        v[4 * q + 2] = selu(v[4 * q + 2] + b.z);
+        v[4 * q + 3] = selu(v[4 * q + 3] + b.w);
+      }
+      st_chunk(a_out, 2 * j, row, v);
+      st_chunk(a_out, 2 * j + 1, row, v + 8);
     }
     tc_before_sync();
+    phase(5 + 2 * l);
     __nv_bfloat16* t = a_in;
     a_in = a_out;
     a_out = t;
@@ -223,13 +269,16 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
 // K4 kernel: blockIdx.x = 128-env tile, blockIdx.y = net (0 policy, 1 value).
 __global__ void __launch_bounds__(kThreads, 1)
     k_policy_mlp(const float* __restrict__ obs, int n_envs, int obs_dim, const float* __restrict__ mean,
-                 const float* __restrict__ stdv, MlpDims Dpi, NetPtrs Ppi, MlpDims Dv, NetPtrs Pv,
+                 const float* __restrict__ stdv, const __grid_constant__ MlpDims Dpi,
+                 const __grid_constant__ NetPtrs Ppi, const __grid_constant__ MlpDims Dv,
+                 const __grid_constant__ NetPtrs Pv,
                  const float* __restrict__ log_std, uint64_t seed, uint64_t step, long long env_offset,
                  float* __restrict__ mu_out, float* __restrict__ act_out, float* __restrict__ logp_out,
                  float* __restrict__ v_out, int a0_elems, int a1_elems, int wbuf_elems) {
   extern __shared__ __align__(1024) unsigned char smem[];
   Smem* sh = reinterpret_cast<Smem*>(smem);
-  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(smem + 1024);
+  phase(0);
+  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(smem + kHeader);
   // operand ping-pong: abuf0 holds layer 0/2 inputs, abuf1 layer 1/3 inputs
   __nv_bfloat16* abuf0 = base;
   __nv_bfloat16* abuf1 = base + a0_elems;
@@ -242,55 +291,75 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lrow = (warp & 3) * 32 + (tid & 31);  // TMEM lane / tile row of this thread
   const int row = blockIdx.x * kM + lrow;
 
-  if (tid == 0) {
-    mbar_init(&sh->bar_w, 1);
-    mbar_init(&sh->bar_mma, 1);
-    mbar_init(&sh->bar_chunk, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 0) {  // TMEM: 256 columns (max layer width)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&sh->tmem)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  tc_before_sync();
-  __syncthreads();
-  tc_after_sync();
-
   __nv_bfloat16* wsm[4];
   int off = 0;
   for (int l = 0; l < 4; ++l) {
     wsm[l] = wbase + off;
     off += D.k[l] * D.n[l];
   }
-  // stage the 4 weight blobs first (one TMA bulk copy each, one barrier) so
-  // the copies overlap the observation prologue (resident mode)
-  const bool stream = wbuf_elems > 0;
-  if (tid == 0 && !stream) {
-    uint32_t bytes = 0;
-    for (int l = 0; l < 4; ++l) bytes += uint32_t(D.k[l]) * D.n[l] * 2;
-    mbar_expect_tx(&sh->bar_w, bytes);
-    for (int l = 0; l < 4; ++l) bulk_g2s(wsm[l], P.w[l], uint32_t(D.k[l]) * D.n[l] * 2, &sh->bar_w);
-  }
   // whitened, clipped observation rows -> bf16 operand (RunningStat,
   // SPEC.md:446-454).  The tile's rows are one contiguous block of global
-  // memory: it is read with coalesced float4 loads into the (still unused)
-  // layer-1 operand buffer, in row passes that fit it, then each (row, 8-column
-  // chunk) is whitened and written as one 16-byte operand chunk.
+  // memory staged into the (still unused) layer-1 operand buffer: by one TMA
+  // bulk copy when its size and address allow (issued first, then the 4 weight
+  // blobs, all completing on mbarriers while the CTA waits for the first),
+  // else by coalesced loads in row passes that fit the buffer.  Each
+  // (row, 8-column chunk) is then whitened and written as one 16-byte chunk.
+  float* stage = reinterpret_cast<float*>(abuf1);
+  const int tile0 = blockIdx.x * kM;
+  const int rows = min(kM, n_envs - tile0);
+  const float* src = obs + size_t(tile0) * obs_dim;
+  const uint32_t tile_bytes = uint32_t(rows) * uint32_t(obs_dim) * 4u;
+  const bool tma_obs = (tile_bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                       tile_bytes <= uint32_t(a1_elems) * 2u;
+  const bool stream = wbuf_elems > 0;
+  if (tid == 0) {
+    mbar_init(&sh->bar_obs, 1);
+    mbar_init(&sh->bar_w, 1);
+    mbar_init(&sh->bar_mma, 1);
+    mbar_init(&sh->bar_chunk, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    if (tma_obs) {
+      mbar_expect_tx(&sh->bar_obs, tile_bytes);
+      bulk_g2s(stage, src, tile_bytes, &sh->bar_obs);
+    }
+    if (!stream) {
+      uint32_t bytes = 0;
+      for (int l = 0; l < 4; ++l) bytes += uint32_t(D.k[l]) * D.n[l] * 2;
+      mbar_expect_tx(&sh->bar_w, bytes);
+      for (int l = 0; l < 4; ++l) bulk_g2s(wsm[l], P.w[l], uint32_t(D.k[l]) * D.n[l] * 2, &sh->bar_w);
+    }
+  }
+  if (warp == 0) {  // TMEM: 256 columns (max layer width)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&sh->tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  for (int c = tid; c < obs_dim; c += kThreads) {
+    sh->wmean[c] = __ldg(mean + c);
+    sh->winv[c] = 1.f / __ldg(stdv + c);
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  phase(1);
+
   {
-    float* stage = reinterpret_cast<float*>(abuf1);
-    const int tile0 = blockIdx.x * kM;
-    const int rows = min(kM, n_envs - tile0);
-    const int pass_rows = min(kM, (a1_elems * 2) / (obs_dim * 4));
+    const int pass_rows = tma_obs ? kM : min(kM, (a1_elems * 2) / (obs_dim * 4));
     const int kchunks = D.k[0] / 8;
+    if (tma_obs) mbar_wait(&sh->bar_obs, 0);
+    phase(11);
     for (int p0 = 0; p0 < kM; p0 += pass_rows) {
       const int pr = max(0, min(pass_rows, rows - p0));
-      const int nf = pr * obs_dim;
-      const float* src = obs + (size_t(tile0) + p0) * obs_dim;
-      const int nf4 = (reinterpret_cast<uintptr_t>(src) & 15) == 0 ? nf / 4 : 0;  // float4 path when aligned
-      for (int i = tid; i < nf4; i += kThreads)
-        reinterpret_cast<float4*>(stage)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
-      for (int i = nf4 * 4 + tid; i < nf; i += kThreads) stage[i] = __ldg(src + i);
-      __syncthreads();
+      if (!tma_obs) {
+        const int nf = pr * obs_dim;
+        const float* s0 = src + size_t(p0) * obs_dim;
+        const int nf4 = (reinterpret_cast<uintptr_t>(s0) & 15) == 0 ? nf / 4 : 0;  // float4 path when aligned
+#pragma unroll 4
+        for (int i = tid; i < nf4; i += kThreads)
+          reinterpret_cast<float4*>(stage)[i] = __ldg(reinterpret_cast<const float4*>(s0) + i);
+        for (int i = nf4 * 4 + tid; i < nf; i += kThreads) stage[i] = __ldg(s0 + i);
+        __syncthreads();
+      }
+      const float* st = stage + (tma_obs ? size_t(p0) * obs_dim : 0);
       const int prow = min(pass_rows, kM - p0);
       for (int u = tid; u < prow * kchunks; u += kThreads) {
         const int r = u % prow, kc = u / prow;
@@ -300,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int c = kc * 8 + i;
           float x = 0.f;
           if (r < pr && c < obs_dim) {
-            x = (stage[r * obs_dim + c] - __ldg(mean + c)) * (1.f / __ldg(stdv + c));
+            x = (st[r * obs_dim + c] - sh->wmean[c]) * sh->winv[c];
             x = fminf(fmaxf(x, -10.f), 10.f);
           }
           x8[i] = x;
@@ -310,44 +379,75 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncthreads();
     }
   }
+  phase(2);
   uint32_t wphase = 0, mphase = 0;
   run_net(D, P, wsm, abuf0, abuf1, sh, wphase, mphase, tid, stream);
   const uint32_t tbase = sh->tmem + (uint32_t((warp & 3) * 32) << 16);
-  if (warp < 4) {  // last layer: 32 (policy) / 16 (value) columns, one warp per TMEM lane group
-    if (!value_net) {
-      // policy mean + Gaussian sample
-      const uint64_t genv = uint64_t(env_offset + row);
-      const uint64_t s = stp_derive_seed(seed, 6 /* policy noise */, (genv << 32) | uint32_t(step));
-      float lp = 0.f;
-      for (int c0 = 0; c0 < D.n[3]; c0 += 16) {
+  if (!value_net) {
+    // policy head in row passes through shared memory (the
+    // operand buffers are free once the last MMA completed): TMEM -> mean
+    // tile [rows][out]; then every thread takes consecutive tile elements, so
+    // the mean / action stores are coalesced; the log-prob terms replace the
+    // means in place and each row is summed in column order by one thread.
+    // Per pass the buffer holds the tile, the rows' noise streams and the
+    // columns' standard deviations.
+    const int out = D.out;
+    const int bytes = (a0_elems + a1_elems) * 2 - out * 4 - 8;
+    const int cap = min(kM, bytes / (out * 4 + 8));
+    float* tile = reinterpret_cast<float*>(abuf0);
+    uint64_t* streams = reinterpret_cast<uint64_t*>(abuf0) + (cap * out + 1) / 2;
+    float* sdv = reinterpret_cast<float*>(streams + cap);
+    const int nch = D.n[3] / 16;
+    if (act_out && tid < out) sdv[tid] = expf(log_std[tid]);
+    for (int p0 = 0; p0 < rows; p0 += cap) {
+      const int pr = min(cap, rows - p0);
+      const bool mine = lrow >= p0 && lrow < p0 + pr;
+      if (act_out && mine && quarter_of(warp) == 0) {
+        const uint64_t genv = uint64_t(env_offset + row);
+        streams[lrow - p0] = stp_derive_seed(seed, 6 /* policy noise */, (genv << 32) | uint32_t(step));
+      }
+      for (int j = quarter_of(warp); j < nch; j += 4) {
         float v[16];
-        tmem_ld16(tbase + uint32_t(c0), v);
-        if (row < n_envs) {
+        tmem_ld16(tbase + uint32_t(16 * j), v);
+        if (mine)
           for (int i = 0; i < 16; ++i) {
-            const int c = c0 + i;
-            if (c >= D.out) break;
-            const float m = v[i] + P.bias[3][c];
-            mu_out[size_t(row) * D.out + c] = m;
-            if (act_out) {
-              // Box-Muller on two 24-bit counter-based uniforms
-              const float u1 = fmaxf(stp_uniformf(s, 2 * c), 1e-7f), u2 = stp_uniformf(s, 2 * c + 1);
-              const float eps = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
-              const float sd = expf(log_std[c]);
-              act_out[size_t(row) * D.out + c] = m + sd * eps;
-              lp += -0.5f * eps * eps - log_std[c] - 0.91893853320467274f;
-            }
+            const int c = 16 * j + i;
+            if (c < out) tile[(lrow - p0) * out + c] = v[i] + P.bias[3][c];
           }
+      }
+      __syncthreads();
+      const size_t g0 = (size_t(tile0) + p0) * out;
+      for (int i = tid; i < pr * out; i += kThreads) {
+        const int r = i / out, c = i - r * out;
+        const float m = tile[i];
+        mu_out[g0 + i] = m;
+        if (act_out) {
+          // Box-Muller on two 24-bit counter-based uniforms
+          const uint64_t ns = streams[r];
+          const float u1 = fmaxf(stp_uniformf(ns, 2 * c), 1e-7f), u2 = stp_uniformf(ns, 2 * c + 1);
+          const float eps = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+          const float sd = sdv[c];
+          act_out[g0 + i] = m + sd * eps;
+          tile[i] = -0.5f * eps * eps - log_std[c] - 0.91893853320467274f;
         }
       }
-      if (logp_out && row < n_envs) logp_out[row] = lp;
-    } else {
-      float v[16];
-      tmem_ld16(tbase, v);
-      if (row < n_envs) v_out[row] = v[0] + P.bias[3][0];
+      __syncthreads();
+      if (logp_out && tid < pr) {
+        float lp = 0.f;
+        if (act_out)
+          for (int c = 0; c < out; ++c) lp += tile[tid * out + c];
+        logp_out[tile0 + p0 + tid] = lp;
+      }
+      __syncthreads();
     }
+  } else if (warp < 4) {
+    float v[16];
+    tmem_ld16(tbase, v);
+    if (row < n_envs) v_out[row] = v[0] + P.bias[3][0];
   }
   tc_before_sync();
   __syncthreads();
+  phase(12);
   if (warp == 0) {
     tc_after_sync();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(sh->tmem));
@@ -355,6 +455,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace
+
+#ifdef STP_K4_PHASES
+extern "C" int stp_k4_phases(unsigned long long* out, int n) {
+  return int(cudaMemcpyFromSymbol(out, g_k4_phase, sizeof(unsigned long long) * size_t(n)));
+}
+#endif
 
 extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_dim, const float* obs_mean,
                                   const float* obs_std, const int32_t* dims_pi, const void* const* w_pi,
@@ -388,6 +494,13 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
       Pv.bias[l] = b_v[l];
     }
   }
+  auto aligned = [](const NetPtrs& P) {  // TMA bulk sources, float4 bias loads
+    for (int l = 0; l < 4; ++l)
+      if ((reinterpret_cast<uintptr_t>(P.w[l]) | reinterpret_cast<uintptr_t>(P.bias[l])) & 15) return false;
+    return true;
+  };
+  if (!aligned(Ppi) || (value_out && !aligned(Pv)))
+    return stp::fail(STP_EINVAL, "stp_policy_forward: weights and biases must be 16-byte aligned");
   auto check = [](const MlpDims& D) {
     for (int l = 0; l < 4; ++l)
       if (D.n[l] > 256 || D.k[l] > 256) return false;  // one UMMA N per layer, 256 TMEM columns
@@ -410,7 +523,7 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
   }
   const int a0 = kM * c0, a1 = kM * c1;
   const size_t kSmemMax = 227 * 1024;
-  const size_t base = 1024 + size_t(a0 + a1) * 2;
+  const size_t base = kHeader + size_t(a0 + a1) * 2;
   size_t smem = base + size_t(wmax) * 2;
   int wbuf = 0;  // 0: all weights resident
   for (MlpDims* D : {&Dpi, &Dv})
