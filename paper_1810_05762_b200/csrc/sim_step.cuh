@@ -315,14 +315,42 @@ __device__ __forceinline__ float fdiv(float a, float b) {
 }
 __device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
 
+#ifndef STP_SCATTER_SUM
+#define STP_SCATTER_SUM 1
+#endif
+
+// Four segment sums.  Reduce-scatter form: the first butterfly level trades
+// two of the four values (each half keeps the pair it owns), the second one,
+// the remaining levels carry one value; the four totals are then broadcast
+// from lanes 0, W/4, W/2, 3W/4 of the segment.  10 shuffles + 6 adds + 6
+// selects instead of 4 log2(W) shuffles + adds, and every lane ends with the
+// same bits.
 template <int W, class T>
 __device__ __forceinline__ void seg_sum4(T& a, T& b, T& c, T& d, unsigned mask) {
+  if constexpr (STP_SCATTER_SUM && W >= 4) {
+    const int lane = threadIdx.x & (W - 1);
+    const bool h1 = lane & (W / 2), h2 = lane & (W / 4);
+    T k0 = h1 ? c : a, k1 = h1 ? d : b;
+    const T s0 = h1 ? a : c, s1 = h1 ? b : d;
+    k0 += __shfl_xor_sync(mask, s0, W / 2, W);
+    k1 += __shfl_xor_sync(mask, s1, W / 2, W);
+    T k = h2 ? k1 : k0;
+    k += __shfl_xor_sync(mask, h2 ? k0 : k1, W / 4, W);
 #pragma unroll
-  for (int off = W / 2; off > 0; off >>= 1) {
-    a += __shfl_xor_sync(mask, a, off, W);
-    b += __shfl_xor_sync(mask, b, off, W);
-    c += __shfl_xor_sync(mask, c, off, W);
-    d += __shfl_xor_sync(mask, d, off, W);
+    for (int off = W / 8; off > 0; off >>= 1) k += __shfl_xor_sync(mask, k, off, W);
+    // lane holds total index 2 h1 + h2: a at lane 0, b at W/4, c at W/2, d at 3W/4
+    a = __shfl_sync(mask, k, 0, W);
+    b = __shfl_sync(mask, k, W / 4, W);
+    c = __shfl_sync(mask, k, W / 2, W);
+    d = __shfl_sync(mask, k, 3 * W / 4, W);
+  } else {
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(mask, a, off, W);
+      b += __shfl_xor_sync(mask, b, off, W);
+      c += __shfl_xor_sync(mask, c, off, W);
+      d += __shfl_xor_sync(mask, d, off, W);
+    }
   }
 }
 
@@ -333,6 +361,33 @@ __device__ __forceinline__ void seg_sum3(T& a, T& b, T& c, unsigned mask) {
     a += __shfl_xor_sync(mask, a, off, W);
     b += __shfl_xor_sync(mask, b, off, W);
     c += __shfl_xor_sync(mask, c, off, W);
+  }
+}
+
+// Two float pairs summed over the segment (the packed PCR loop's one
+// reduction per trip), in the reduce-scatter form of seg_sum4 when enabled.
+template <int W>
+__device__ __forceinline__ void seg_sum2x2(float2& q0, float2& q1, unsigned mask) {
+  if constexpr (STP_SCATTER_SUM && W >= 4) {
+    const int lane = threadIdx.x & (W - 1);
+    const bool h1 = lane & (W / 2), h2 = lane & (W / 4);
+    float2 keep = h1 ? q1 : q0;
+    const float2 send = h1 ? q0 : q1;
+    keep = __fadd2_rn(keep, make_float2(__shfl_xor_sync(mask, send.x, W / 2, W),
+                                        __shfl_xor_sync(mask, send.y, W / 2, W)));
+    float k = h2 ? keep.y : keep.x;
+    k += __shfl_xor_sync(mask, h2 ? keep.x : keep.y, W / 4, W);
+#pragma unroll
+    for (int off = W / 8; off > 0; off >>= 1) k += __shfl_xor_sync(mask, k, off, W);
+    // lane holds total 2 h1 + h2 of (q0.x, q0.y, q1.x, q1.y)
+    q0 = make_float2(__shfl_sync(mask, k, 0, W), __shfl_sync(mask, k, W / 4, W));
+    q1 = make_float2(__shfl_sync(mask, k, W / 2, W), __shfl_sync(mask, k, 3 * W / 4, W));
+  } else {
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {
+      q0 = __fadd2_rn(q0, make_float2(__shfl_xor_sync(mask, q0.x, off, W), __shfl_xor_sync(mask, q0.y, off, W)));
+      q1 = __fadd2_rn(q1, make_float2(__shfl_xor_sync(mask, q1.x, off, W), __shfl_xor_sync(mask, q1.y, off, W)));
+    }
   }
 }
 
@@ -1559,11 +1614,7 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
                 // one reduction per trip: (lb, zn) and (aa, ax) as two pairs
                 float2 q0 = make_float2(lbw * dot6p(rh, rh), dot6p(rh, ar));
                 float2 q1 = make_float2(dot6p(ar, ar), dot6p(ar, ap));
-#pragma unroll
-                for (int off = W / 2; off > 0; off >>= 1) {
-                  q0 = __fadd2_rn(q0, make_float2(__shfl_xor_sync(mask, q0.x, off, W), __shfl_xor_sync(mask, q0.y, off, W)));
-                  q1 = __fadd2_rn(q1, make_float2(__shfl_xor_sync(mask, q1.x, off, W), __shfl_xor_sync(mask, q1.y, off, W)));
-                }
+                seg_sum2x2<W>(q0, q1, mask);
                 const float zn = q0.y, aa = q1.x, ax = q1.y;
                 const float beta = fdiv(zn, zaz);
                 denom = aa + beta * (2.f * ax + beta * denom);
