@@ -63,8 +63,12 @@ __global__ void k_shapes_warp(const DevModel<T>* __restrict__ Mp, const T* __res
                               double* __restrict__ env_box, int2* __restrict__ env_cell, int* __restrict__ bin_count,
                               int* __restrict__ bins, unsigned hmask, int* __restrict__ ovf, int* __restrict__ n_ovf,
                               int* __restrict__ max_ext_bits, int* __restrict__ xcount) {
+  // the warp's shapes are staged in shared memory and written out as
+  // coalesced 8-byte words (one 136-byte struct per lane would scatter)
+  __shared__ WShape stage[4][32];  // launched with 128 threads
   const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, b = threadIdx.x & 31;
   if (e >= n) return;
+  WShape* sw = stage[threadIdx.x >> 5];
   const DevModel<T>& M = *Mp;
   const int B = M.nb;
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -105,7 +109,15 @@ __global__ void k_shapes_warp(const DevModel<T>* __restrict__ Mp, const T* __res
         hi[k] = s.hi[k];
       }
     }
-    ws[size_t(e) * B + b] = s;
+    sw[b] = s;
+  }
+  __syncwarp();
+  {
+    static_assert(sizeof(WShape) % 8 == 0, "WShape words");
+    constexpr int kWords = int(sizeof(WShape) / 8);
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(sw);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(ws + size_t(e) * B);
+    for (int i = b; i < B * kWords; i += 32) dst[i] = src[i];
   }
   for (int off = 16; off > 0; off >>= 1)
     for (int k = 0; k < 3; ++k) {
@@ -155,14 +167,34 @@ __global__ void k_env_query(int n, const double* __restrict__ env_box, const int
       if (slot < cap) pairs[slot] = make_int2(i, j);
     }
   };
-  for (int u = lane; u < side * side * kBinCap; u += 32) {
-    const int c = u / kBinCap, k = u % kBinCap;
-    const int cx = ci.x + c % side - rc, cy = ci.y + c / side - rc;
-    const unsigned h = cell_hash(cx, cy, hmask);
-    if (k >= min(bin_count[h], kBinCap)) continue;
-    const int j = bins[h * kBinCap + k];
-    const int2 cj = env_cell[j];
-    if (cj.x == cx && cj.y == cy) test(j);  // hash collisions: each env once, in its own cell
+  // kU candidates per lane per pass, their dependent loads (bin count -> bin
+  // entry -> cell -> box) issued side by side
+  constexpr int kU = 4;
+  const int total = side * side * kBinCap;
+  for (int u0 = lane; u0 < total; u0 += 32 * kU) {
+    int cx[kU], cy[kU], j[kU];
+    unsigned h[kU];
+    int cnt[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int u = u0 + 32 * q;
+      const int c = u / kBinCap;
+      cx[q] = ci.x + c % side - rc;
+      cy[q] = ci.y + c / side - rc;
+      h[q] = cell_hash(cx[q], cy[q], hmask);
+      cnt[q] = u < total ? bin_count[h[q]] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int k = (u0 + 32 * q) % kBinCap;
+      j[q] = k < min(cnt[q], kBinCap) ? bins[h[q] * kBinCap + k] : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      if (j[q] < 0) continue;
+      const int2 cj = env_cell[j[q]];
+      if (cj.x == cx[q] && cj.y == cy[q]) test(j[q]);  // hash collisions: each env once, in its own cell
+    }
   }
   const int no = *n_ovf;
   for (int k = lane; k < no; k += 32) test(ovf[k]);
@@ -321,14 +353,20 @@ __global__ void k_narrow_slots(const int2* __restrict__ pairs, const int* __rest
 
 // Islands of envs (solver.cpp:458-482 restricted to what couples envs): label
 // propagation over the contact edges, then island lists.  One CTA.
+// Contact-merged islands by label propagation in one CTA.  Labels live in
+// shared memory when the env count fits (`slab`), else in `label`; only edge
+// endpoints ever change label (every label value is an endpoint's index), so
+// the propagation and pointer-jumping passes run over the edges alone.
 __global__ void k_islands(int n, const int2* __restrict__ edges, const int* __restrict__ n_edges_p, int edge_cap,
                           int* __restrict__ label, uint8_t* __restrict__ merged, int* __restrict__ isl_of,
                           int* __restrict__ isl_size, int* __restrict__ isl_members, int* __restrict__ isl_count,
-                          int* __restrict__ err) {
+                          int* __restrict__ err, int labels_in_smem) {
+  extern __shared__ int slab[];
   __shared__ int changed;
+  int* L = labels_in_smem ? slab : label;
   const int ne = min(*n_edges_p, edge_cap);
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    label[e] = e;
+    L[e] = e;
     merged[e] = 0;
   }
   __syncthreads();
@@ -342,20 +380,21 @@ __global__ void k_islands(int n, const int2* __restrict__ edges, const int* __re
     __syncthreads();
     for (int i = threadIdx.x; i < ne; i += blockDim.x) {
       const int a = edges[i].x, b = edges[i].y;
-      const int la = label[a], lb = label[b];
+      const int la = L[a], lb = L[b];
       if (la != lb) {
         const int m = min(la, lb);
-        atomicMin(&label[a], m);
-        atomicMin(&label[b], m);
-        atomicMin(&label[max(la, lb)], m);
+        atomicMin(&L[a], m);
+        atomicMin(&L[b], m);
+        atomicMin(&L[max(la, lb)], m);
         changed = 1;
       }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {  // pointer jumping
-      const int l = label[e], ll = label[l];
+    for (int i = threadIdx.x; i < 2 * ne; i += blockDim.x) {  // pointer jumping
+      const int e = (i & 1) ? edges[i >> 1].y : edges[i >> 1].x;
+      const int l = L[e], ll = L[l];
       if (ll < l) {
-        atomicMin(&label[e], ll);
+        atomicMin(&L[e], ll);
         changed = 1;
       }
     }
@@ -363,7 +402,7 @@ __global__ void k_islands(int n, const int2* __restrict__ edges, const int* __re
     if (!changed) break;
   }
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    if (merged[e] && label[e] == e) {
+    if (merged[e] && L[e] == e) {
       const int i = atomicAdd(isl_count, 1);
       isl_of[e] = i;
       isl_size[i] = 0;
@@ -373,7 +412,7 @@ __global__ void k_islands(int n, const int2* __restrict__ edges, const int* __re
   __syncthreads();
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     if (!merged[e]) continue;
-    const int i = isl_of[label[e]];
+    const int i = isl_of[L[e]];
     const int pos = atomicAdd(&isl_size[i], 1);
     if (pos < kIslandMax) isl_members[i * kIslandMax + pos] = e;
     else atomicOr(err, 2);
@@ -572,8 +611,17 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
   k_narrow_slots<<<148 * 2, 256, 0, st>>>(P->pairs, P->counters, int(P->pair_cap), B, (long long)n * B, P->ws, margin,
                                           P->xslots, P->xcount, P->edges, edge_cap, P->icnt, P->icnt + 2);
   STP_CK(cudaGetLastError());
-  k_islands<<<1, 1024, 0, st>>>(n, P->edges, P->icnt, edge_cap, P->label, P->merged, P->isl_of, P->isl_size,
-                                P->isl_members, P->icnt + 1, P->icnt + 2);
+  // labels in shared memory up to 48K envs (192 KB), else in global scratch
+  const size_t lab_bytes = size_t(n) * sizeof(int);
+  const bool lab_smem = lab_bytes <= 192 * 1024;
+  static size_t lab_attr = 48 * 1024;
+  if (lab_smem && lab_bytes > lab_attr) {
+    STP_CK(cudaFuncSetAttribute(k_islands, cudaFuncAttributeMaxDynamicSharedMemorySize, int(192 * 1024)));
+    lab_attr = 192 * 1024;
+  }
+  k_islands<<<1, 1024, lab_smem ? lab_bytes : 0, st>>>(n, P->edges, P->icnt, edge_cap, P->label, P->merged,
+                                                       P->isl_of, P->isl_size, P->isl_members, P->icnt + 1,
+                                                       P->icnt + 2, int(lab_smem));
   STP_CK(cudaGetLastError());
   view->merged = P->merged;
   view->isl_members = P->isl_members;
