@@ -58,17 +58,12 @@ __device__ __forceinline__ unsigned cell_hash(int cx, int cy, unsigned hmask) {
 }
 
 template <class T>
-__global__ void k_shapes_warp(const DevModel<T>* __restrict__ Mp, const T* __restrict__ state,
-                              const double* __restrict__ origin, int n, int W, WShape* __restrict__ ws,
-                              double* __restrict__ env_box, int2* __restrict__ env_cell, int* __restrict__ bin_count,
-                              int* __restrict__ bins, unsigned hmask, int* __restrict__ ovf, int* __restrict__ n_ovf,
-                              int* __restrict__ max_ext_bits, int* __restrict__ xcount) {
-  // the warp's shapes are staged in shared memory and written out as
-  // coalesced 8-byte words (one 136-byte struct per lane would scatter)
-  __shared__ WShape stage[4][32];  // launched with 128 threads
-  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, b = threadIdx.x & 31;
-  if (e >= n) return;
-  WShape* sw = stage[threadIdx.x >> 5];
+__device__ __forceinline__ void shapes_of_env(const DevModel<T>* __restrict__ Mp, const T* __restrict__ state,
+                                              const double* __restrict__ origin, int e, int b, int W,
+                                              WShape* __restrict__ ws, WShape* sw, double* __restrict__ env_box,
+                                              int2* __restrict__ env_cell, int* __restrict__ bin_count,
+                                              int* __restrict__ bins, unsigned hmask, int* __restrict__ ovf,
+                                              int* __restrict__ n_ovf, int& ext_bits, int* __restrict__ xcount) {
   const DevModel<T>& M = *Mp;
   const int B = M.nb;
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -135,12 +130,32 @@ __global__ void k_shapes_warp(const DevModel<T>* __restrict__ Mp, const T* __res
     }
     const int cx = cell_of(0.5 * (lo[0] + hi[0])), cy = cell_of(0.5 * (lo[1] + hi[1]));
     env_cell[e] = make_int2(cx, cy);
-    const float ext = float(fmax(hi[0] - lo[0], hi[1] - lo[1]));
-    atomicMax(max_ext_bits, __float_as_int(__fmul_ru(ext, 1.0f)));  // positive floats order as ints
+    ext_bits = __float_as_int(__double2float_ru(fmax(hi[0] - lo[0], hi[1] - lo[1])));
     const unsigned h = cell_hash(cx, cy, hmask);
     const int slot = atomicAdd(&bin_count[h], 1);
     if (slot < kBinCap) bins[h * kBinCap + slot] = e;
     else ovf[atomicAdd(n_ovf, 1)] = e;
+  }
+}
+
+template <class T>
+__global__ void k_shapes_warp(const DevModel<T>* __restrict__ Mp, const T* __restrict__ state,
+                              const double* __restrict__ origin, int n, int W, WShape* __restrict__ ws,
+                              double* __restrict__ env_box, int2* __restrict__ env_cell, int* __restrict__ bin_count,
+                              int* __restrict__ bins, unsigned hmask, int* __restrict__ ovf, int* __restrict__ n_ovf,
+                              int* __restrict__ max_ext_bits, int* __restrict__ xcount) {
+  // the warp's shapes are staged in shared memory and written out as
+  // coalesced 8-byte words (one 136-byte struct per lane would scatter)
+  __shared__ WShape stage[4][32];  // launched with 128 threads
+  __shared__ int blk_ext[4];  // the block's largest env extent -> one atomicMax per block
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, b = threadIdx.x & 31;
+  if (b == 0) blk_ext[threadIdx.x >> 5] = 0;
+  if (e < n) shapes_of_env(Mp, state, origin, e, b, W, ws, stage[threadIdx.x >> 5], env_box, env_cell, bin_count,
+                           bins, hmask, ovf, n_ovf, blk_ext[threadIdx.x >> 5], xcount);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int m = max(max(blk_ext[0], blk_ext[1]), max(blk_ext[2], blk_ext[3]));
+    if (m > 0) atomicMax(max_ext_bits, m);  // positive floats order as ints
   }
 }
 
