@@ -317,11 +317,13 @@ def test_dense_terrain_contact_overflow_slots(precision):
     assert g.report()["overflow"].sum() == 0
 
 
-@pytest.mark.parametrize("n", [4096, 1000])
-def test_step_host_pipelined_matches_device_step(n):
+@pytest.mark.parametrize("n,pinned", [(4096, False), (1000, False), (4096, True), (64, True)])
+def test_step_host_pipelined_matches_device_step(n, pinned):
     """stp_step_host runs env chunks on their own streams (copies overlap the
     other chunks' kernels); results must be bit-identical to the one-launch
-    device path, including a step with pending external loads."""
+    device path, including a step with pending external loads.  With
+    page-locked output buffers the kernel writes reward / done into them
+    directly (no download)."""
     import torch
     a = VecEnv("humanoid", n_envs=n, seed=5)
     b = VecEnv("humanoid", n_envs=n, seed=5)
@@ -336,7 +338,12 @@ def test_step_host_pipelined_matches_device_step(n):
             b.set_external_loads(loads)
         od, rd, dd = a.step(torch.from_numpy(act).cuda())
         torch.cuda.synchronize()
-        oh, rh, dh = b.step_host(act)
+        if pinned:
+            bufs = [torch.full((n, a.obs_dim), -1.0).pin_memory(), torch.full((n,), -1.0).pin_memory(),
+                    torch.full((n,), 7, dtype=torch.uint8).pin_memory()]
+            oh, rh, dh = b.step_host(act, *[t.numpy() for t in bufs])
+        else:
+            oh, rh, dh = b.step_host(act)
         np.testing.assert_array_equal(od.cpu().numpy(), oh)
         np.testing.assert_array_equal(rd.cpu().numpy(), rh)
         np.testing.assert_array_equal(dd.cpu().numpy(), dh)
