@@ -465,6 +465,21 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
   s->seed = seed;
   s->env_offset = env_offset;
   s->W = s->B <= 8 ? 8 : (s->B <= 16 ? 16 : 32);
+  if (precision == STP_PRECISION_F32 && s->W < 32) {
+    // Several envs per warp only pay when that is what fits the launch into
+    // one wave of resident warps (3 blocks x 4 warps per SM): their lane
+    // groups diverge, so a shared warp runs ~1.25x longer than a full-warp
+    // env (measured, Ant: 64 envs 0.091 -> 0.056 ms, 1776: 0.097 -> 0.078,
+    // 4096: 0.205 -> 0.202 with W = 32; 2048: 0.098 with W = 16, 0.130 with 32).
+    int dev_sms = 0;
+    if (cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+      cudaGetLastError();
+      dev_sms = 148;
+    }
+    const long long resident = 12LL * dev_sms;
+    const long long narrow = (n_envs * (long long)s->W + 31) / 32;
+    if (!(n_envs > resident && narrow <= resident)) s->W = 32;
+  }
   bool boxes_shape = false;
   for (int b = 0; b < s->B; ++b) boxes_shape = boxes_shape || model->bodies[b].shape == STP_BOX;
   s->cpb = boxes_shape || task->kind == STP_TASK_HFH_TERRAIN ? 4 : 2;

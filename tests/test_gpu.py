@@ -130,6 +130,35 @@ def test_f32_kernel_statistical_parity(task, scale):
         assert q(dv, 50) <= 2e-3 and q(dv, 99) <= 1e-1 and (dv > 1e-2).mean() <= 0.10
 
 
+def test_f32_two_envs_per_warp_layout():
+    """2048 Ant envs are the one f32 case that packs two envs per warp (W = 16
+    fits them in one wave of resident warps); below one wave
+    every env gets a full warp.  Both layouts free-run within the fp32 bound
+    of the reference on the same states and torques."""
+    n, m = 2048, 32
+    wide = VecEnv("ant", n_envs=n, precision="f32", seed=5)  # W = 16
+    full = VecEnv("ant", n_envs=m, precision="f32", seed=5)  # W = 32
+    o = oracle.OracleEnv(full.model, full.task, full.cfg, m, seed=5)
+    o32 = oracle.OracleEnv(full.model, full.task, full.cfg, m, seed=5, precision="f32")
+    wide.reset()
+    s = wide.get_state()
+    for env in (full, o, o32):
+        env.set_state(s[:m])
+    tm = np.array([o.model.joints[j].max_torque for j in range(full.action_dim)])
+    rng = np.random.default_rng(3)
+    for t in range(5):
+        tq = rng.uniform(-1, 1, size=(n, full.action_dim)) * tm
+        wide.physics_step(tq)
+        for env in (full, o, o32):
+            env.physics_step(tq[:m])
+    ref = o.get_state()[..., :3]
+    restated = np.abs(ref - o32.get_state()[..., :3]).max()
+    for env in (wide, full):
+        err = np.abs(ref - env.get_state()[:m, ..., :3]).max()
+        print(f"W layout of {env.n_envs} envs: 5-step |dx| {err:.2e} (fp32 restatement {restated:.2e})")
+        assert err <= max(2e-3, 2 * restated)
+
+
 @pytest.mark.parametrize("task", ["humanoid", "ant"])
 def test_f32_free_running_short_horizon(task):
     """5 free-running steps from identical states: |dx| <= 2e-3 m, or within

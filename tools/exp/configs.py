@@ -35,6 +35,10 @@ def run(task, n, boxes=None, steps=30):
 
 
 if __name__ == "__main__":
+  if os.environ.get("ONLY") == "ant":
+    for n in (64, 512, 1024, 1776, 2048, 4096):
+      run("ant", n)
+    sys.exit(0)
   run("ant", 64)
   run("ant", 4096)
   run("humanoid", 1024)
