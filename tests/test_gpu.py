@@ -404,3 +404,25 @@ def test_divergent_env_is_rolled_back_and_flagged(precision):
     assert not np.array_equal(s1[0], s0[0])
     d, r = done.cpu().numpy(), rew.cpu().numpy()
     assert d[1] == 1 and r[1] == 0.0 and d[[0, 2, 3]].sum() == 0
+
+
+@pytest.mark.parametrize("task", ["humanoid", "ant"])
+def test_env_count_edges(task):
+    """An env's trajectory does not depend on how many envs share the handle
+    (every draw is keyed by the global env index): one env, a partial 4-warp
+    block, and both sides of the band where f32 Ant envs share warps
+    (3552 envs: two per warp; 3553: one per warp)."""
+    import torch
+    first = {}
+    for n in (1, 129, 3552, 3553):
+        env = VecEnv(task, n_envs=n, seed=11)
+        env.reset()
+        for t in range(4):
+            obs, _, _ = env.step(env.random_actions(t))
+        torch.cuda.synchronize()
+        first[n] = obs[:1].cpu().numpy()
+        env.close()
+    # same lane layout -> bit-identical; the packed layout sums in another order
+    np.testing.assert_array_equal(first[1], first[129])
+    np.testing.assert_array_equal(first[1], first[3553])
+    np.testing.assert_allclose(first[3552], first[1], atol=1e-3, rtol=0)
