@@ -22,6 +22,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 EXTRA = os.environ.get("STP_NVCC_EXTRA", "").split()
 FLAGS = EXTRA + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
+# fp32 step kernel: IEEE-approximate division / sqrt (<= 2 ulp, no slow-path
+# branches) and flush-to-zero — its parity is a stated fp32 envelope against
+# the reference, and the f64 instantiation (the exact parity instrument) is
+# not affected by these single-precision flags
+PER_SOURCE = {"sim_step_f32.cu": ["-ftz=true", "-prec-div=false", "-prec-sqrt=false"]}
 SOURCES = ["sim_step_f32.cu", "sim_step_f64.cu", "sim_host.cu", "sim_aux.cu", "sim_pairs.cu", "models.cpp", "policy_mlp.cu"]
 DEPS = ["sim_device.cuh", "sim_kernels.cuh", "sim_step.cuh", "sim_launch.h", "stp_rng.h", "stp_error.h"]
 
@@ -37,7 +42,7 @@ def _compile(src: str) -> tuple[str, str]:
                  [_mtime(os.path.join(CSRC, d)) for d in DEPS])
     if _mtime(obj) >= newest:
         return obj, ""
-    cmd = [NVCC] + ARCH + FLAGS + ["-c", path, "-o", obj]
+    cmd = [NVCC] + ARCH + FLAGS + PER_SOURCE.get(src, []) + ["-c", path, "-o", obj]
     if src.endswith(".cpp"):
         cmd = [NVCC] + ARCH + FLAGS + ["-x", "cu", "-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -49,7 +54,7 @@ def _compile(src: str) -> tuple[str, str]:
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     stamp = os.path.join(BUILD, "flags.txt")  # objects built with other flags are stale
-    flags = " ".join(ARCH + FLAGS)
+    flags = " ".join(ARCH + FLAGS) + repr(sorted(PER_SOURCE.items()))
     if not os.path.exists(stamp) or open(stamp).read() != flags:
         for f in os.listdir(BUILD):
             if f.endswith(".o"):
