@@ -1919,7 +1919,7 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
       const T yaw = atan2(T(2) * (qr.w * qr.z + qr.x * qr.y), T(1) - T(2) * (qr.y * qr.y + qr.z * qr.z));
       yaw_r = yaw;
       head_r = atan2(ty - xr.y, tx - xr.x);
-      const T cth = cos(head_r - yaw);
+      const T cth = cos_(head_r - yaw);
       const T rhead = cth > T(0.8) ? T(1) : cth / T(0.8);
       const T cvert = T(1) - T(2) * (qr.x * qr.x + qr.y * qr.y);
       const T rstand = cvert > T(0.93) ? T(1) : T(0);

@@ -1,5 +1,7 @@
 #!/bin/bash
 # where do spills (STL/LDL) of the f32 W=32 CPB=2 kernel come from?
+# same per-source flags as build.py PER_SOURCE for the fp32 TU
+STP_NVCC_EXTRA=${STP_NVCC_EXTRA:--ftz=true -prec-div=false -prec-sqrt=false}
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -cubin $STP_NVCC_EXTRA -I/root/repo/include -I/root/repo/paper_1810_05762_b200/csrc /root/repo/paper_1810_05762_b200/csrc/sim_step_f32.cu -o /tmp/spill.cubin 2>/dev/null
 nvdisasm -g /tmp/spill.cubin 2>/dev/null > /tmp/spill.sass
 python3 - <<'PY'
