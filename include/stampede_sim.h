@@ -16,6 +16,10 @@
  *    "host" pointers are ordinary (preferably pinned) host memory.
  *  - All calls on one handle are asynchronous on the given CUDA stream
  *    (NULL = the handle's own stream) unless documented as synchronous.
+ *    The synchronous accessors (state, loads, contacts, report, task state,
+ *    snapshots, terrain, the host-buffer steps) order themselves after the
+ *    most recent launch made on a caller's stream, so e.g. stp_get_state
+ *    right after an asynchronous stp_step sees that step.
  *    A handle is not reentrant (reference Scene is not either,
  *    solver.hpp:46-53); use one handle per GPU / per process.
  *  - Per-body state layout in host buffers is the reference's

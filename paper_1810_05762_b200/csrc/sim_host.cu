@@ -21,6 +21,12 @@
 struct stp_sim {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // Launches may run on a caller's stream (torch's current stream, the legacy
+  // default stream) while the accessors below run on the handle's non-blocking
+  // stream: the last caller-stream launch is recorded here and every accessor
+  // orders its copies after it (join_caller).
+  cudaEvent_t ev_caller = nullptr;
+  bool caller_pending = false;
   int precision = STP_PRECISION_F32;
   int W = 32, cpb = 2, cap = 64;
   stp_model model{};
@@ -386,13 +392,31 @@ int launch_t(stp_sim* s, int mode, const float* torques, const float* actions, f
   return STP_OK;
 }
 
+// order the handle's stream after the last launch made on a caller's stream
+int join_caller(stp_sim* s) {
+  if (s->caller_pending) {
+    CK(cudaStreamWaitEvent(s->stream, s->ev_caller, 0));
+    s->caller_pending = false;
+  }
+  return STP_OK;
+}
+
 int launch(stp_sim* s, int mode, const float* torques, const float* actions, float* obs, float* reward,
            uint8_t* done, const uint8_t* mask, cudaStream_t st, int e_begin = 0, int e_end = -1) {
+  if (st == s->stream) {
+    if (const int rc = join_caller(s)) return rc;
+  }
   const int rc = s->precision == STP_PRECISION_F64
                      ? launch_t<double>(s, mode, torques, actions, obs, reward, done, mask, st, e_begin, e_end)
                      : launch_t<float>(s, mode, torques, actions, obs, reward, done, mask, st, e_begin, e_end);
   if (rc) return rc;
   if (mode != 2) s->loads_pending = false;
+  bool own = st == s->stream;  // the chunk streams of stp_step_host join before it returns
+  for (int c = 0; c < stp_sim::kChunks; ++c) own = own || st == s->cs[c];
+  if (!own) {
+    CK(cudaEventRecord(s->ev_caller, st));
+    s->caller_pending = true;
+  }
   return STP_OK;
 }
 
@@ -497,6 +521,7 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
     return nullptr;
   }
   e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_caller, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     cuda_fail(e, "cudaStreamCreate");
     delete s;
@@ -546,6 +571,7 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
 
 void stp_destroy(stp_sim* s) {
   if (!s) return;
+  if (s->ev_caller) cudaEventSynchronize(s->ev_caller);
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (int c = 0; c < stp_sim::kChunks; ++c) {
     if (s->cs[c]) {
@@ -555,6 +581,7 @@ void stp_destroy(stp_sim* s) {
     if (s->ev_out[c]) cudaEventDestroy(s->ev_out[c]);
   }
   if (s->ev_in) cudaEventDestroy(s->ev_in);
+  if (s->ev_caller) cudaEventDestroy(s->ev_caller);
   stp::pair_scratch_free(s->pairs);
   for (void* p : s->allocations) cudaFree(p);
   if (s->stream) cudaStreamDestroy(s->stream);
@@ -563,6 +590,7 @@ void stp_destroy(stp_sim* s) {
 
 int stp_set_terrain(stp_sim* s, const stp_static_box* boxes, int32_t n) {
   if (!s || n < 0 || (n > 0 && !boxes)) return fail(STP_EINVAL, "stp_set_terrain: bad arguments");
+  if (const int rc_ = join_caller(s)) return rc_;
   std::vector<double> h(size_t(std::max(n, 1)) * 8);
   for (int i = 0; i < n; ++i) {
     const stp_static_box& b = boxes[i];
@@ -678,6 +706,7 @@ int64_t stp_snapshot_size(const stp_sim* s) {
 
 int stp_save_snapshot(stp_sim* s, uint8_t* buf, int64_t capacity) {
   if (!s || !buf) return fail(STP_EINVAL, "stp_save_snapshot: bad arguments");
+  if (const int rc_ = join_caller(s)) return rc_;
   const int64_t need = stp_snapshot_size(s);
   if (capacity < need) return fail(STP_EINVAL, "stp_save_snapshot: buffer too small");
   const uint64_t nb = uint64_t(s->n) * s->B;
@@ -689,6 +718,7 @@ int stp_save_snapshot(stp_sim* s, uint8_t* buf, int64_t capacity) {
 
 int stp_load_snapshot(stp_sim* s, const uint8_t* buf, int64_t size) {
   if (!s || !buf || size < 16) return fail(STP_EINVAL, "stp_load_snapshot: bad arguments");
+  if (const int rc_ = join_caller(s)) return rc_;
   uint32_t magic, version;
   uint64_t nb;
   std::memcpy(&magic, buf, 4);
@@ -706,6 +736,7 @@ int stp_load_snapshot(stp_sim* s, const uint8_t* buf, int64_t size) {
 int stp_detect_inter_agent(stp_sim* s, int32_t capacity, int32_t* count, int32_t* body_a, int32_t* body_b,
                            double* point, double* normal, double* separation) {
   if (!s || !count || capacity < 0) return fail(STP_EINVAL, "stp_detect_inter_agent: bad arguments");
+  if (const int rc_ = join_caller(s)) return rc_;
   bool overflow = false;
   int n = 0;
   cudaError_t e;
@@ -755,6 +786,7 @@ static void* pinned_view(void* p) {
 
 int stp_step_host(stp_sim* s, const float* actions, float* obs, float* reward, uint8_t* done) {
   if (!s || (s->J > 0 && !actions)) return fail(STP_EINVAL, "stp_step_host: bad arguments");
+  if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
   // reward / done (5 bytes per env) go straight from the kernel into
   // page-locked host buffers, saving two small downloads (~5 us of fixed
@@ -818,6 +850,7 @@ int stp_physics_step(stp_sim* s, const float* torques, void* stream) {
 
 int stp_physics_step_host(stp_sim* s, const double* torques) {
   if (!s) return fail(STP_EINVAL, "stp_physics_step_host: null handle");
+  if (const int rc_ = join_caller(s)) return rc_;
   if (s->J > 0 && !torques) return fail(STP_EINVAL, "clamp_torques: torque count must equal joint count");
   const size_t N = size_t(s->n);
   std::vector<float> t(N * s->J);
@@ -834,6 +867,7 @@ int stp_physics_step_host(stp_sim* s, const double* torques) {
 
 int stp_set_state(stp_sim* s, const double* state) {
   if (!s || !state) return fail(STP_EINVAL, "stp_set_state: bad arguments");
+  if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
   const int W = s->W, B = s->B, R = s->model.root;
   std::vector<double> origin(N * 2);
@@ -879,6 +913,7 @@ int stp_set_state(stp_sim* s, const double* state) {
 
 int stp_get_state(stp_sim* s, double* state) {
   if (!s || !state) return fail(STP_EINVAL, "stp_get_state: bad arguments");
+  if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
   const int W = s->W, B = s->B;
   std::vector<unsigned char> buf(N * stp::kStateFields * W * s->tsize);
@@ -901,6 +936,7 @@ int stp_get_state(stp_sim* s, double* state) {
 
 int stp_set_external_loads(stp_sim* s, const double* loads) {
   if (!s || !loads) return fail(STP_EINVAL, "stp_set_external_loads: bad arguments");
+  if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
   const int W = s->W, B = s->B;
   std::vector<unsigned char> buf(N * 6 * W * s->tsize, 0);
@@ -921,6 +957,7 @@ int stp_set_external_loads(stp_sim* s, const double* loads) {
 int stp_get_contacts(stp_sim* s, int32_t* count, int32_t* body_a, int32_t* body_b, double* point, double* normal,
                      double* separation, double* normal_impulse, double* tangential_impulse) {
   if (!s) return fail(STP_EINVAL, "stp_get_contacts: null handle");
+  if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n), C = size_t(s->cap);
   std::vector<int32_t> cnt(N), body(N * C);
   std::vector<double> data(N * C * stp::kCData);
@@ -950,6 +987,7 @@ int stp_get_contacts(stp_sim* s, int32_t* count, int32_t* body_a, int32_t* body_
 
 int stp_get_report(stp_sim* s, int32_t* newton, int32_t* krylov, uint8_t* failed, uint8_t* overflow) {
   if (!s) return fail(STP_EINVAL, "stp_get_report: null handle");
+  if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
   if (newton) CK(cudaMemcpyAsync(newton, s->d_newton, N * 4, cudaMemcpyDeviceToHost, s->stream));
   if (krylov) CK(cudaMemcpyAsync(krylov, s->d_krylov, N * 4, cudaMemcpyDeviceToHost, s->stream));
@@ -961,6 +999,7 @@ int stp_get_report(stp_sim* s, int32_t* newton, int32_t* krylov, uint8_t* failed
 
 int stp_get_task_state(stp_sim* s, double* target, int32_t* counters, double* last_tau) {
   if (!s) return fail(STP_EINVAL, "stp_get_task_state: null handle");
+  if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n), J = size_t(s->J);
   std::vector<double> origin(N * 2);
   std::vector<unsigned char> traw(N * 2 * s->tsize), lraw(N * std::max<size_t>(J, 1) * s->tsize);
@@ -982,6 +1021,7 @@ int stp_get_task_state(stp_sim* s, double* target, int32_t* counters, double* la
 
 int stp_set_task_state(stp_sim* s, const double* target, const int32_t* counters, const double* last_tau) {
   if (!s) return fail(STP_EINVAL, "stp_set_task_state: null handle");
+  if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n), J = size_t(s->J);
   std::vector<double> origin(N * 2);
   CK(cudaMemcpyAsync(origin.data(), s->d_origin, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));

@@ -426,3 +426,35 @@ def test_env_count_edges(task):
     np.testing.assert_array_equal(first[1], first[129])
     np.testing.assert_array_equal(first[1], first[3553])
     np.testing.assert_allclose(first[3552], first[1], atol=1e-3, rtol=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_accessors_order_after_caller_stream_launches(precision):
+    """reset / step run on the caller's stream (torch's current stream, here
+    the legacy default stream) and the synchronous accessors on the handle's
+    non-blocking stream: get_state / get_report called right after an
+    asynchronous launch must see its result, with no synchronize in between."""
+    import torch
+    task = abi.default_task(abi.TASK_HUMANOID)
+    g = VecEnv(model=abi.builtin_model("humanoid"), task_config=task, step_config=abi.default_step_config(),
+               n_envs=4096, precision=precision, seed=11)
+    g.reset()
+    torch.cuda.synchronize()
+    s_before = g.get_state()
+    for it in range(3):
+        torch.cuda._sleep(20_000_000)  # ~10 ms of GPU spin ahead of the launch on the same stream
+        g.reset()
+        s_async = g.get_state()  # no synchronize: must order after the reset kernel
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(s_async, g.get_state())
+        act = torch.rand((4096, g.action_dim), device="cuda") * 2 - 1
+        torch.cuda._sleep(20_000_000)
+        g.step(act)
+        s_async = g.get_state()
+        rep_async = g.report()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(s_async, g.get_state())
+        assert not np.array_equal(s_async, s_before)
+        np.testing.assert_array_equal(rep_async["krylov_iterations"], g.report()["krylov_iterations"])
+        s_before = s_async
