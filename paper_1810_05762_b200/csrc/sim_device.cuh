@@ -91,6 +91,10 @@ template <class T> __device__ __forceinline__ v3<T> vunit(v3<T> a) {  // vec.hpp
 template <class T> __device__ __forceinline__ bool vfinite(v3<T> a) {
   return isfinite(a.x) && isfinite(a.y) && isfinite(a.z);
 }
+// finiteness of many values with one test: x * 0 is NaN exactly when x is
+// +-inf or NaN, so a chain of fma(x, 0, z) from 0 stays +-0 unless some x is
+// not finite (one FMA per value instead of a compare and a predicate op)
+template <class T> __device__ __forceinline__ T nf_acc(T z, T x) { return fma(x, T(0), z); }
 template <class T> __device__ __forceinline__ T comp(v3<T> a, int k) { return k == 0 ? a.x : (k == 1 ? a.y : a.z); }
 
 // fp32 sine / cosine without sincosf's Payne-Hanek branch (a local-memory

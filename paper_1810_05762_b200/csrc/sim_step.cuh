@@ -1179,8 +1179,10 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
     // the constant off-diagonal block must be finite (krylov.cpp:113)
     bool off_fin = true;
     if (L.has_off) {
+      T z = T(0);
 #pragma unroll
-      for (int k = 0; k < 36; ++k) off_fin = off_fin && isfinite(L.at(R_HOFF + k));
+      for (int k = 0; k < 36; ++k) z = nf_acc(z, L.at(R_HOFF + k));
+      off_fin = isfinite(z);
     }
     const bool off_ok = isl_all(off_fin);
 
@@ -1360,11 +1362,12 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
         // arithmetic): z = M^-1 r = L^-T rhat, z.Az = rhat.Ahat rhat and
         // Ap.M^-1 Ap = |Ahat phat|^2.  Ahat has identity diagonal blocks, so
         // an iteration needs no diagonal product and no preconditioner solve.
-        bool fin = true;
+        T nz = T(0);
 #pragma unroll
-        for (int k = 0; k < 21; ++k) fin = fin && isfinite(H[k]);
+        for (int k = 0; k < 21; ++k) nz = nf_acc(nz, H[k]);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) fin = fin && isfinite(rhs[k]);
+        for (int k = 0; k < 6; ++k) nz = nf_acc(nz, rhs[k]);
+        const bool fin = isfinite(nz);
         ++newton_done;
         if (!off_ok || !isl_all(fin)) {  // reference throws (krylov.cpp:113-114)
           step_failed = true;
@@ -1733,9 +1736,10 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
           u[i] = sum * L.at(R_SCAT + i);
         }
         krylov_total += kk;
-        bool ufin = true;
+        T uz = T(0);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) ufin = ufin && isfinite(u[k]);
+        for (int k = 0; k < 6; ++k) uz = nf_acc(uz, u[k]);
+        const bool ufin = isfinite(uz);
         if (!isl_all(ufin)) {  // never hand back a poisoned iterate (:168-172)
 #pragma unroll
           for (int k = 0; k < 6; ++k) u[k] = T(0);
