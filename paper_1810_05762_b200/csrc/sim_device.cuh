@@ -118,6 +118,16 @@ __device__ __forceinline__ void sincos_(float a, float* s, float* c) {
   *c = ((q + 1) & 2) ? -cc : cc;
 }
 __device__ __forceinline__ void sincos_(double a, double* s, double* c) { sincos(a, s, c); }
+// (sin, cos) of atan2(y, x) without forming the angle: (y, x) / |(x, y)|, with
+// atan2(0, 0) = 0.  fp32 step only (the f64 instrument keeps the reference's
+// atan2 -> sin / cos; the two agree to a few ulp).
+__device__ __forceinline__ void unit_dir(float y, float x, float* s, float* c) {
+  const float r2 = x * x + y * y;
+  const bool z = !(r2 > 0.f);
+  const float inv = rsqrtf(z ? 1.f : r2);
+  *c = z ? 1.f : x * inv;
+  *s = z ? 0.f : y * inv;
+}
 template <class T> __device__ __forceinline__ T cos_(T a) {
   T s, c;
   sincos_(a, &s, &c);

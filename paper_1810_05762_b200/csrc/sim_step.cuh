@@ -1902,6 +1902,8 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
   // ---------------- K3: task epilogue (env_step) ---------
   bool reuse_angles = false, reuse_head = false;
   T yaw_r = T(0), head_r = T(0), ang_r = T(0);
+  constexpr bool kF32 = std::is_same<T, float>::value;
+  T sy_r = T(0), cy_r = T(1), sh_r = T(0), ch_r = T(1);  // fp32: yaw / heading unit vectors
   if (a.mode == 1) {
     const T tx_r = tx, ty_r = ty;
     const int R = M.root;
@@ -1920,10 +1922,17 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
       const T od0 = sqrt(ox_ * ox_ + oy_ * oy_);
       T S = T(0);
       if (od0 > T(0)) S = ((xr.x - prev_rx) * ox_ + (xr.y - prev_ry) * oy_) / od0 / cf.dt;
-      const T yaw = atan2(T(2) * (qr.w * qr.z + qr.x * qr.y), T(1) - T(2) * (qr.y * qr.y + qr.z * qr.z));
-      yaw_r = yaw;
-      head_r = atan2(ty - xr.y, tx - xr.x);
-      const T cth = cos_(head_r - yaw);
+      T cth;
+      if constexpr (kF32) {  // cos(heading - yaw) from the two unit vectors, no angles
+        unit_dir(T(2) * (qr.w * qr.z + qr.x * qr.y), T(1) - T(2) * (qr.y * qr.y + qr.z * qr.z), &sy_r, &cy_r);
+        unit_dir(ty - xr.y, tx - xr.x, &sh_r, &ch_r);
+        cth = ch_r * cy_r + sh_r * sy_r;
+      } else {
+        const T yaw = atan2(T(2) * (qr.w * qr.z + qr.x * qr.y), T(1) - T(2) * (qr.y * qr.y + qr.z * qr.z));
+        yaw_r = yaw;
+        head_r = atan2(ty - xr.y, tx - xr.x);
+        cth = cos_(head_r - yaw);
+      }
       const T rhead = cth > T(0.8) ? T(1) : cth / T(0.8);
       const T cvert = T(1) - T(2) * (qr.x * qr.x + qr.y * qr.y);
       const T rstand = cvert > T(0.93) ? T(1) : T(0);
@@ -1998,11 +2007,18 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
       const qt<T> qr2 = from<W>(q, R, mask);
       const v3<T> vr2 = from<W>(v, R, mask);
       const v3<T> wr2 = from<W>(w, R, mask);
-      const T yaw = reuse_angles ? yaw_r
-                                 : atan2(T(2) * (qr2.w * qr2.z + qr2.x * qr2.y),
-                                         T(1) - T(2) * (qr2.y * qr2.y + qr2.z * qr2.z));
-      T sy, cy;
-      sincos_(yaw, &sy, &cy);
+      T yaw = T(0), sy, cy;
+      if constexpr (kF32) {
+        sy = sy_r;
+        cy = cy_r;
+        if (!reuse_angles)
+          unit_dir(T(2) * (qr2.w * qr2.z + qr2.x * qr2.y), T(1) - T(2) * (qr2.y * qr2.y + qr2.z * qr2.z), &sy, &cy);
+      } else {
+        yaw = reuse_angles ? yaw_r
+                           : atan2(T(2) * (qr2.w * qr2.z + qr2.x * qr2.y),
+                                   T(1) - T(2) * (qr2.y * qr2.y + qr2.z * qr2.z));
+        sincos_(yaw, &sy, &cy);
+      }
       if (b == 0) {
         o[0] = float(xr2.z);
         o[1] = float(atan2(T(2) * (qr2.w * qr2.x + qr2.y * qr2.z), T(1) - T(2) * (qr2.x * qr2.x + qr2.y * qr2.y)));
@@ -2016,7 +2032,14 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
         o[7] = float(-sy * wr2.x + cy * wr2.y);
         o[8] = float(wr2.z);
         T sh, ch;
-        sincos_((reuse_head ? head_r : atan2(ty - xr2.y, tx - xr2.x)) - yaw, &sh, &ch);
+        if constexpr (kF32) {  // sin / cos of (heading - yaw) by the angle-difference identities
+          T sh0 = sh_r, ch0 = ch_r;
+          if (!reuse_head) unit_dir(ty - xr2.y, tx - xr2.x, &sh0, &ch0);
+          sh = sh0 * cy - ch0 * sy;
+          ch = ch0 * cy + sh0 * sy;
+        } else {
+          sincos_((reuse_head ? head_r : atan2(ty - xr2.y, tx - xr2.x)) - yaw, &sh, &ch);
+        }
         o[9] = float(sh);
         o[10] = float(ch);
         for (int f = 0; f < M.n_feet; ++f) o[11 + 3 * J + f] = ((feet_bits >> M.feet[f]) & 1) ? 1.f : 0.f;
