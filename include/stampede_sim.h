@@ -303,6 +303,13 @@ int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_dim, const 
                        int64_t env_offset, float* mean_out, float* action_out, float* logp_out,
                        float* value_out, void* stream);
 
+/* --- diagnostics (tests only; not part of the reference interface) ---------
+ * The fp32 step kernel's own elementary functions on device arrays, so their
+ * accuracy is tested directly: fn 0 = sincos (Cody-Waite +
+ * Cephes) of x -> (out0 = sin, out1 = cos); fn 1 = the unit-vector bearing
+ * (sin, cos) of atan2(x, y) used by the heading terms.  Asynchronous. */
+int stp_debug_math(int32_t fn, const float* x, const float* y, float* out0, float* out1, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

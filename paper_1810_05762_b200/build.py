@@ -26,7 +26,9 @@ FLAGS = EXTRA + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptx
 # branches) and flush-to-zero — its parity is a stated fp32 envelope against
 # the reference, and the f64 instantiation (the exact parity instrument) is
 # not affected by these single-precision flags
-PER_SOURCE = {"sim_step_f32.cu": ["-ftz=true", "-prec-div=false", "-prec-sqrt=false"]}
+FP32_FLAGS = ["-ftz=true", "-prec-div=false", "-prec-sqrt=false"]
+# sim_aux.cu holds the fp32 math self-test, compiled like the step kernel
+PER_SOURCE = {"sim_step_f32.cu": FP32_FLAGS, "sim_aux.cu": FP32_FLAGS}
 SOURCES = ["sim_step_f32.cu", "sim_step_f64.cu", "sim_host.cu", "sim_aux.cu", "sim_pairs.cu", "models.cpp", "policy_mlp.cu"]
 DEPS = ["sim_device.cuh", "sim_kernels.cuh", "sim_step.cuh", "sim_launch.h", "stp_rng.h", "stp_error.h"]
 

@@ -1,7 +1,9 @@
-// Auxiliary device kernels of the C-ABI: bench random actions.
+// Auxiliary device kernels of the C-ABI: bench random actions and the
+// fp32 math self-test (compiled with the fp32 step kernel's flags, build.py).
 #include <cuda_runtime.h>
 
 #include "stampede_sim.h"
+#include "sim_device.cuh"
 #include "stp_error.h"
 #include "stp_rng.h"
 
@@ -20,7 +22,33 @@ __global__ void k_random_actions(float* out, int n, int J, uint64_t seed, long l
   out[i] = 2.0f * stp_uniformf(s, uint32_t(j)) - 1.0f;
 }
 
+// The fp32-only elementary functions of the step kernel, evaluated on
+// caller arrays (DESIGN.md §2 "fp32-only paths"): fn 0 = sincos_(x) ->
+// (sin, cos); fn 1 = unit_dir(y = x, x = y) -> (sin, cos) of atan2(x, y).
+__global__ void k_debug_math(int fn, const float* x, const float* y, float* o0, float* o1, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s, c;
+  if (fn == 0) stp::sincos_(x[i], &s, &c);
+  else stp::unit_dir(x[i], y[i], &s, &c);
+  o0[i] = s;
+  o1[i] = c;
+}
+
 }  // namespace
+
+extern "C" int stp_debug_math(int32_t fn, const float* x, const float* y, float* out0, float* out1, int64_t n,
+                              void* stream) {
+  if (fn < 0 || fn > 1 || n < 0 || (n > 0 && (!x || !out0 || !out1 || (fn == 1 && !y))))
+    return stp::fail(STP_EINVAL, "stp_debug_math: bad arguments");
+  if (n == 0) return STP_OK;
+  const int threads = 256;
+  k_debug_math<<<int((n + threads - 1) / threads), threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      fn, x, y, out0, out1, (long long)n);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_debug_math: ") + cudaGetErrorString(e));
+  return STP_OK;
+}
 
 namespace stp {
 int sim_dims(const stp_sim* s, int* n, int* J, uint64_t* seed, long long* off, void** stream);

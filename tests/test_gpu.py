@@ -76,6 +76,7 @@ def _teacher_forced(task, precision, n=32, steps=60, scale=1.0, seed=7):
     o32 = oracle.OracleEnv(g.model, g.task, g.cfg, n, seed=seed, precision="f32")
     tm = np.array([g.model.joints[j].max_torque for j in range(g.action_dim)])
     dx, dv, rx, rv, mism, boundary = [], [], [], [], 0, 0
+    ill = []
     for t in range(steps):
         tq = o.random_actions(t) * tm * scale
         s = o.get_state()
@@ -87,6 +88,10 @@ def _teacher_forced(task, precision, n=32, steps=60, scale=1.0, seed=7):
         a, b, c = o.get_state(), g.get_state(), o32.get_state()
         ex, ev = _errs(a, b)
         fx, fv = _errs(a, c)
+        for e in np.nonzero(ex > 5e-3)[0]:  # beyond the stated max: is the input ill-conditioned?
+            if _bistable(g, s[e], tq[e], ex[e]):
+                ill.append(float(ex[e]))
+                ex[e] = 0.0
         dx.append(ex)
         dv.append(ev)
         rx.append(fx)
@@ -101,7 +106,33 @@ def _teacher_forced(task, precision, n=32, steps=60, scale=1.0, seed=7):
                 else:
                     mism += 1
     cat = np.concatenate
+    if ill:
+        print(f"ill-conditioned env-steps (the double reference itself moves by >= half the GPU error under "
+              f"1e-7 input perturbations; reported, not bounded): {len(ill)} with |dx| {ill}")
+    assert len(ill) <= max(2, 1e-4 * n * steps)
     return cat(dx), cat(dv), mism, boundary, cat(rx), cat(rv)
+
+
+def _bistable(g, pre, tq, err, trials=16):
+    """True when the double oracle's own result moves by >= err / 2 under
+    1e-7 m perturbations of the input positions: a discrete decision of the
+    reference algorithm (unilateral activity, speculative limit, near-stick
+    friction; SURVEY §8(c) "floor") sits at this input, so an fp32 path may
+    take either branch."""
+    o = oracle.OracleEnv(g.model, g.task, g.cfg, 1, seed=0)
+    o.set_state(pre[None])
+    o.physics_step(tq[None])
+    ref = o.get_state()[0]
+    rng = np.random.default_rng(0)
+    spread = 0.0
+    for _ in range(trials):
+        p = pre.copy()
+        p[..., :3] += rng.uniform(-1e-7, 1e-7, p[..., :3].shape)
+        o.set_state(p[None])
+        o.physics_step(tq[None])
+        spread = max(spread, np.abs(o.get_state()[0][..., :3] - ref[..., :3]).max())
+    o.close()
+    return spread >= 0.5 * err
 
 
 @pytest.mark.parametrize("task", ["humanoid", "ant"])
@@ -114,7 +145,11 @@ def test_f64_kernel_matches_oracle_teacher_forced(task):
 
 @pytest.mark.parametrize("task,scale", [("humanoid", 1.0), ("humanoid", 0.1), ("ant", 1.0)])
 def test_f32_kernel_statistical_parity(task, scale):
-    dx, dv, mism, boundary, rx, rv = _teacher_forced(task, "f32", scale=scale)
+    """SURVEY §8(c) protocol (1): teacher-forced one-step physics over
+    32 envs x 1000 steps (Humanoid, saturating torques: upright, falling and
+    lying) or 300 steps, contact lists bit-exact."""
+    steps = 1000 if (task, scale) == ("humanoid", 1.0) else 300
+    dx, dv, mism, boundary, rx, rv = _teacher_forced(task, "f32", scale=scale, steps=steps)
     q = lambda a, p: float(np.percentile(a, p))
     print(f"{task} scale {scale}: GPU dx p50 {q(dx, 50):.2e} p99 {q(dx, 99):.2e} max {dx.max():.2e};"
           f" rel dv p50 {q(dv, 50):.2e} p99 {q(dv, 99):.2e} >1e-2 {(dv > 1e-2).mean():.3f} |"
@@ -179,32 +214,54 @@ def test_f32_free_running_short_horizon(task):
     assert ours <= max(2e-3, 2 * restated)
 
 
-@pytest.mark.parametrize("name", ["humanoid", "ant"])
+@pytest.mark.parametrize("name", ["humanoid", "ant", "hfh"])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
 def test_env_step_against_reference_golden(name, precision):
-    """Teacher-forced replay of the reference's golden trajectory through the
-    full env_step (physics + reward + termination + obs)."""
+    """Teacher-forced replay of the reference's golden trajectory (compiled
+    reference physics + env layer, tests/golden/make_golden.py) through the
+    full env_step: physics, reward, termination, auto-reset, observation.
+    The Humanoid / HFH fixtures hold falls, auto-resets (the post state of a
+    done env is its reset state), the HFH grace and flagrun redraws.
+    f64: states 1e-7 m, rewards 1e-5 (float32 buffers), obs 1e-4.
+    f32: done bit-exact; states / obs / reward within tests/parity.py BOUNDS."""
+    import parity as P
     gz = np.load(os.path.join(GOLDEN, f"golden_{name}.npz"))
-    n = int(gz["n"])
+    n, S, A = int(gz["n"]), gz["states"], gz["actions"]
     env = VecEnv(name, n_envs=n, precision=precision, seed=int(gz["seed"]))
-    tol_x = 1e-7 if precision == "f64" else 5e-3
-    tol_r = 1e-4 if precision == "f64" else 0.5
-    worst = 0.0
+    m = env.model
+    J = env.action_dim
+    groups = P.obs_groups(J, m.n_feet, False)
+    worst, rew_err, obs_err = 0.0, [], {k: [] for k in groups}
     for t in range(int(gz["steps"])):
-        env.set_state(gz["pre"][t])
-        ts = env.task_state()
-        env.set_task_state(target=gz["target"][t], counters=gz["counters"][t], last_tau=ts["last_tau"])
-        o, r, d = env.step(gz["actions"][t].astype(np.float32))
-        if gz["done"][t].any():
-            np.testing.assert_array_equal(d, gz["done"][t])
-            continue  # auto-reset state: compared through the reset test below
+        env.set_state(S[t])
+        last = np.zeros((n, J)) if t == 0 else np.where(gz["done"][t - 1][:, None] == 1, 0.0,
+                                                        np.clip(A[t - 1], -1, 1))
+        env.set_task_state(target=gz["target"][t], counters=gz["counters"][t], last_tau=last)
+        o, r, d = env.step(A[t].astype(np.float32))
         np.testing.assert_array_equal(d, gz["done"][t])
         post = env.get_state()
-        worst = max(worst, np.abs(post[..., :3] - gz["post"][t][..., :3]).max())
-        assert np.abs(r - gz["reward"][t]).max() <= tol_r
-        if precision == "f64":
-            assert np.abs(o - gz["obs"][t]).max() <= 1e-4
-    assert worst <= tol_x
+        worst = max(worst, np.abs(post[..., :3] - S[t + 1][..., :3]).max())
+        rew_err.append(np.abs(r - gz["reward"][t]))
+        for k, cols in groups.items():
+            e = np.abs(o[:, cols].astype(np.float64) - gz["obs"][t][:, cols])
+            if k in P.RELATIVE:
+                e = e / np.maximum(1, np.abs(gz["obs"][t][:, cols]))
+            obs_err[k].append(e.max())
+    rew_err = np.concatenate(rew_err)
+    print(f"{name} {precision}: done events {int(gz['done'].sum())}, |dx| max {worst:.2e}, reward err max "
+          f"{rew_err.max():.2e}, obs max " + " ".join(f"{k} {max(v):.1e}" for k, v in obs_err.items()))
+    if name != "ant":
+        assert gz["done"].sum() > 0
+    if precision == "f64":
+        assert worst <= 1e-7 and rew_err.max() <= 1e-5  # reward / obs buffers are float32
+        assert max(max(v) for v in obs_err.values()) <= 1e-4
+    else:
+        assert worst <= P.BOUNDS["dx"][1]
+        assert np.percentile(rew_err, 99) <= P.BOUNDS["reward"][0] and rew_err.max() <= P.BOUNDS["reward"][1]
+        for k, v in obs_err.items():
+            mx = P.BOUNDS[k][1]
+            if mx is not None:
+                assert max(v) <= mx, (k, max(v))
 
 
 @pytest.mark.parametrize("task", ["humanoid", "ant", "hfh"])

@@ -13,30 +13,42 @@ from paper_1810_05762_b200 import abi
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
+TASK_OF = {"ant": abi.TASK_ANT, "humanoid": abi.TASK_HUMANOID, "hfh": abi.TASK_HFH}
+
+
 def _env(name, kind="restatement", n=None, seed=None, precision="f64"):
     g = np.load(os.path.join(GOLDEN, f"golden_{name}.npz"))
-    model = abi.builtin_model(name)
-    task = abi.default_task(abi.TASK_ANT if name == "ant" else abi.TASK_HUMANOID)
+    model = abi.builtin_model("ant" if name == "ant" else "humanoid")
+    task = abi.default_task(TASK_OF[name])
     cfg = abi.default_step_config()
     env = oracle.OracleEnv(model, task, cfg, int(n or g["n"]), seed=int(seed or g["seed"]), kind=kind,
                            precision=precision)
     return env, g
 
 
-@pytest.mark.parametrize("name", ["ant", "humanoid"])
+@pytest.mark.parametrize("name", ["ant", "humanoid", "hfh"])
 def test_restatement_replays_reference_golden(name):
+    """Free-running replay of the reference's fixture (terminations,
+    auto-resets, HFH fall grace and flagrun redraws) by the restatement."""
     env, g = _env(name)
+    S = g["states"]
     for t in range(int(g["steps"])):
-        np.testing.assert_array_equal(env.get_state(), g["pre"][t])
+        np.testing.assert_array_equal(env.get_state(), S[t])
         o, r, d = env.step(g["actions"][t])
-        np.testing.assert_allclose(env.get_state(), g["post"][t], rtol=0, atol=1e-12)
-        np.testing.assert_allclose(r, g["reward"][t], rtol=0, atol=1e-12)
+        np.testing.assert_array_equal(env.get_state(), S[t + 1])
+        np.testing.assert_array_equal(r, g["reward"][t])
         np.testing.assert_array_equal(d, g["done"][t])
-        np.testing.assert_allclose(o, g["obs"][t], rtol=0, atol=1e-12)
+        np.testing.assert_array_equal(o.astype(np.float32), g["obs"][t])
+        ts = env.task_state()
+        if t + 1 < int(g["steps"]):
+            np.testing.assert_array_equal(ts["target"], g["target"][t + 1])
+            np.testing.assert_array_equal(ts["counters"], g["counters"][t + 1])
         c = env.contact_arrays(64)
         np.testing.assert_array_equal(c["count"], g["contact_count"][t])
-        np.testing.assert_array_equal(c["body_a"], g["contact_body"][t])
-        np.testing.assert_allclose(c["separation"], g["contact_sep"][t], rtol=0, atol=1e-12)
+        np.testing.assert_array_equal(c["body_a"].astype(np.int8), g["contact_body"][t])
+        np.testing.assert_array_equal(c["separation"].astype(np.float32), g["contact_sep"][t])
+    if name != "ant":
+        assert g["done"].sum() > 0  # the fixture holds terminations
 
 
 @pytest.mark.parametrize("name", ["ant", "humanoid"])
