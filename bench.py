@@ -9,6 +9,10 @@ the fused sm_100a kernel.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+With --gpus N > 1 outside torchrun the script re-launches itself as N ranks
+(torch.distributed.run, 127.0.0.1); each rank steps its own 4096 envs
+(env_offset = rank * 4096) with no collective in the timed region.
+
 Timing: K steps, each bracketed by CUDA events on the launching stream with
 an L2 flush (a 256 MiB write, outside the events) between steps; a barrier +
 synchronize brackets the whole timed loop; the per-rank device time is the
@@ -120,47 +124,105 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(mhz)}
 
 
-def cpu_reference_rate(n_envs: int, steps: int, warmup: int, threads: int, budget_s: float = 20.0):
+def _cpu_info():
+    """lscpu model name, logical CPUs and physical cores of this host."""
+    model, sockets, cores_per = None, 1, None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            v = v.strip()
+            if k.strip() == "Model name":
+                model = v
+            elif k.strip() == "Socket(s)":
+                sockets = int(v)
+            elif k.strip() == "Core(s) per socket":
+                cores_per = int(v)
+    except (OSError, ValueError, subprocess.SubprocessError):
+        pass
+    logical = os.cpu_count() or 1
+    try:
+        logical = len(os.sched_getaffinity(0))
+    except AttributeError:
+        pass
+    return {"cpu_model": model, "logical_cpus": logical,
+            "physical_cores": sockets * cores_per if cores_per else None}
+
+
+def cpu_reference_rate(n_envs: int, steps: int, warmup: int, threads: int, budget_s: float = 20.0,
+                       single_thread_s: float = 0.0):
     """Reference stampede::physics::step + restated env layer on host cores.
 
-    Runs oracle/_ref (the compiled reference, its Release flags) when it was
-    built, else the restated oracle port.  Bounded sample: the env count is
-    cut so the timed part stays within ~budget_s.
+    Runs oracle/_ref (the compiled, unmodified reference, its Release flags)
+    when it was built, else the restated oracle port.  The model, task and
+    step config come from the oracle's own reader of assets/humanoid.model
+    (oracle/model_text.py), so this arm never loads the product library.
+    Bounded sample: the env count is cut so the timed part stays within
+    ~budget_s.  With single_thread_s > 0 the same workload is also timed on
+    one thread (n = all cores and n = 1).
     """
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
     from oracle import OracleEnv, available
-    from paper_1810_05762_b200 import abi
+    import model_text
+    from paper_1810_05762_b200 import abi  # ctypes struct layouts only (no library load)
     kind = "reference_fast" if available("reference_fast") else "restatement"
-    model = abi.builtin_model("humanoid")
-    task = abi.default_task(abi.TASK_HUMANOID)
-    cfg = abi.default_step_config()
-    # calibrate on a small batch, then size the sample
-    probe_n = min(n_envs, 256)
-    env = OracleEnv(model, task, cfg, probe_n, seed=SEED, nthreads=threads, kind=kind)
-    for s in range(2):
-        env.step(env.random_actions(s))
-    t0 = time.perf_counter()
-    env.step(env.random_actions(2))
-    rate = probe_n / max(time.perf_counter() - t0, 1e-6)
-    env.close()
-    per_step_budget = budget_s / max(1, steps)
-    n_sample = int(max(16, min(n_envs, rate * per_step_budget)))
-    env = OracleEnv(model, task, cfg, n_sample, seed=SEED, nthreads=threads, kind=kind)
-    acts = [env.random_actions(s) for s in range(warmup + steps)]
-    for s in range(warmup):
-        env.step(acts[s])
-    t0 = time.perf_counter()
-    for s in range(steps):
-        env.step(acts[warmup + s])
-    dt = time.perf_counter() - t0
-    env.close()
-    value = n_sample * steps / dt
-    return {"value": value, "unit": "env-steps/s", "cores": threads,
-            "kind": "reference" if kind.startswith("reference") else "port",
-            "sample": f"{n_sample} of {n_envs} Humanoid envs x {steps} env_steps (random actions, auto-reset), "
-                      f"{'oracle/_ref/libstampede_ref_fast.so: unmodified stampede::physics::step, -O3 -march=native, util::ThreadPool' if kind.startswith('reference') else 'oracle/liboracle.so restatement'}"
-                      f" + restated env layer"}
+    model = model_text.load_model("humanoid")
+    task = model_text.default_task(abi.TASK_HUMANOID)
+    cfg = model_text.default_step_config()
+
+    def measure(nthreads, budget, n_steps, n_warm):
+        probe_n = min(n_envs, 64 * nthreads)
+        env = OracleEnv(model, task, cfg, probe_n, seed=SEED, nthreads=nthreads, kind=kind)
+        for s in range(2):
+            env.step(env.random_actions(s))
+        t0 = time.perf_counter()
+        env.step(env.random_actions(2))
+        rate = probe_n / max(time.perf_counter() - t0, 1e-6)
+        env.close()
+        n_sample = int(max(16, min(n_envs, rate * budget / max(1, n_steps))))
+        env = OracleEnv(model, task, cfg, n_sample, seed=SEED, nthreads=nthreads, kind=kind)
+        acts = [env.random_actions(s) for s in range(n_warm + n_steps)]
+        for s in range(n_warm):
+            env.step(acts[s])
+        t0 = time.perf_counter()
+        for s in range(n_steps):
+            env.step(acts[n_warm + s])
+        dt = time.perf_counter() - t0
+        env.close()
+        return n_sample * n_steps / dt, n_sample
+
+    value, n_sample = measure(threads, budget_s, steps, warmup)
+    info = _cpu_info()
+    out = {"value": value, "unit": "env-steps/s", "cores": threads,
+           "kind": "reference" if kind.startswith("reference") else "port",
+           "sample": f"{n_sample} of {n_envs} Humanoid envs x {steps} env_steps (random actions, auto-reset), "
+                     f"{'oracle/_ref/libstampede_ref_fast.so: unmodified stampede::physics::step, -O3 -march=native, util::ThreadPool(' + str(threads) + ')' if kind.startswith('reference') else 'oracle/liboracle.so restatement'}"
+                     f" + restated env layer; model from assets/humanoid.model via oracle/model_text.py",
+           **info}
+    if single_thread_s > 0:
+        v1, n1 = measure(1, single_thread_s, 2, 1)
+        out["value_1_thread"] = v1
+        out["sample_1_thread"] = f"{n1} envs x 2 env_steps on 1 thread"
+    return out
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args) -> None:
+    """`--gpus N` (N > 1) outside torchrun: re-run this script as N ranks of
+    one node through torch.distributed.run on 127.0.0.1 (the driver's own
+    launch sets WORLD_SIZE and skips this).  Rank 0 prints the line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    sys.exit(subprocess.run(cmd, env=env).returncode)
 
 
 def dist_setup(args):
@@ -171,24 +233,50 @@ def dist_setup(args):
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            import torch
+            if torch.cuda.device_count() < world:
+                raise SystemExit(f"bench.py --gpus {world}: only {torch.cuda.device_count()} GPU(s) visible")
+            torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     return world, rank, local
+
+
+def bench_config(world: int) -> dict:
+    """The workload description, identical in both arms."""
+    return {"workload": "humanoid_run_flat_4096envs_random_actions", "envs_per_gpu": N_ENVS, "task": TASK,
+            "parallelism": f"dp{world} (env shards, no collective)",
+            "l2": "flushed between timed steps (256 MiB write)", "auto_reset": True}
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    r = cpu_reference_rate(N_ENVS, max(1, args.steps), max(0, args.warmup), threads, budget_s=90.0)
+    threads = _cpu_info()["logical_cpus"]
+    budget = float(os.environ.get("STP_BENCH_CPU_BUDGET_S", "90"))
+    r = cpu_reference_rate(N_ENVS, max(1, args.steps), max(0, args.warmup), threads, budget_s=budget,
+                           single_thread_s=min(10.0, budget / 6))
     line = {"metric": "env-steps/sec (Humanoid, 4096 envs/GPU)", "value": r["value"], "unit": "env-steps/s",
-            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * N_ENVS / r["value"] if r["value"] else None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "humanoid_run_flat_4096envs_random_actions", "envs_per_gpu": N_ENVS,
-                       "task": TASK, "parallelism": "cpu-threads"},
-            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": r["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * N_ENVS / r["value"] if r["value"] else None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": bench_config(world),
+            "cpu_baseline": r,
+            "e2e": {"value": r["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "CPU reference on the host cores of rank 0 only (one sample of the per-GPU workload)",
+            "repo_libraries_loaded": _repo_libraries_loaded()}
     print(json.dumps(line), flush=True)
+
+
+def _repo_libraries_loaded():
+    """Shared objects under this repo mapped into the process (the reference
+    arm must show only oracle/_ref/*.so)."""
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")}
+    except OSError:
+        return None
+    return sorted(os.path.relpath(p, ROOT) for p in paths if os.path.realpath(p).startswith(os.path.realpath(ROOT)))
 
 
 def run_ours(args, world, rank, local):
@@ -196,6 +284,7 @@ def run_ours(args, world, rank, local):
     from paper_1810_05762_b200.sim import VecEnv
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    assert torch.cuda.is_available(), "bench.py --impl ours needs a CUDA device (no CPU fallback)"
     env = VecEnv(TASK, n_envs=N_ENVS, device=local, seed=SEED, env_offset=rank * N_ENVS)
     K, Wm = args.steps, args.warmup
     # synthetic inputs resident in HBM before timing: one action batch per step
@@ -204,7 +293,6 @@ def run_ours(args, world, rank, local):
     rew = torch.empty((N_ENVS,), device=dev)
     done = torch.empty((N_ENVS,), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
-    krylov = []
     for s in range(Wm):
         env.step(acts[s], obs, rew, done)
     torch.cuda.synchronize()
@@ -230,9 +318,12 @@ def run_ours(args, world, rank, local):
     kry_mean = float(rep["krylov_iterations"].mean())
     failed = int(rep["failed"].sum())
     t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    per_rank_ms = [dev_ms]
     if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    job_ms = float(t.item())
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        torch.distributed.all_gather(allt, t)
+        per_rank_ms = [float(x.item()) for x in allt]
+    job_ms = max(per_rank_ms)
     value = world * N_ENVS * K / (job_ms / 1e3)
     ms_per_step = job_ms / K
 
@@ -375,17 +466,19 @@ def run_ours(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_rate(N_ENVS, 3, 1, os.cpu_count() or 1, budget_s=15.0)
+            cpu = cpu_reference_rate(N_ENVS, 5, 1, _cpu_info()["logical_cpus"], budget_s=20.0,
+                                     single_thread_s=6.0)
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"unavailable: {ex!r}"}
+    per_rank = [N_ENVS * K / (ms / 1e3) for ms in per_rank_ms]
     if rank == 0:
         line = {"metric": "env-steps/sec (Humanoid, 4096 envs/GPU)", "value": value, "unit": "env-steps/s",
                 "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": "humanoid_run_flat_4096envs_random_actions", "envs_per_gpu": N_ENVS,
-                           "task": TASK, "parallelism": f"dp{world} (env shards, no collective)",
-                           "l2": "flushed between timed steps (256 MiB write)", "auto_reset": True},
+                "config": bench_config(world),
+                "per_rank_env_steps_per_s": per_rank,
+                "weak_scaling_fraction_of_ideal": value / sum(per_rank),
                 "e2e": {"value": e2e_value, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "path": "stp_step_host (pinned host buffers)"},
                 "gpu_launches": K, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "rollout": rollout, "ppo": ppo,
@@ -403,7 +496,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    self_launch(args)
     world, rank, local = dist_setup(args)
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}; reporting n_gpus = {world}", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

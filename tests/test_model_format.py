@@ -90,3 +90,19 @@ def test_minimal_document_parses():
 def test_malformed_documents_are_rejected(bad, msg):
     with pytest.raises(ValueError, match=msg.replace("(", r"\(").replace(")", r"\)")):
         abi.model_from_text(bad)
+
+
+@pytest.mark.parametrize("name", ["ant", "humanoid"])
+def test_oracle_reader_matches_builtin(name):
+    """The oracle's own reader (oracle/model_text.py, used by bench.py's CPU
+    arms so they never load the product library) yields the same bytes as the
+    product's built-in model, and the same defaults."""
+    import ctypes as C
+
+    import model_text
+    a, b = model_text.load_model(name), abi.builtin_model(name)
+    assert bytes(a) == bytes(b)
+    assert bytes(model_text.default_step_config()) == bytes(abi.default_step_config())
+    for k in (abi.TASK_ANT, abi.TASK_HUMANOID, abi.TASK_HFH, abi.TASK_HFH_TERRAIN):
+        assert bytes(model_text.default_task(k)) == bytes(abi.default_task(k))
+    assert C.sizeof(a) == C.sizeof(abi.Model)
