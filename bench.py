@@ -388,7 +388,12 @@ def run_ours(args, world, rank, local):
         pkern = PolicyKernel(pmodel, dev)
         pst = RunningStat(env.obs_dim, device=dev)
         env.last_obs = env.reset()
-        pst.push(env.last_obs)
+        first = RunningStat(env.obs_dim, device=dev)
+        first.push(env.last_obs)
+        if world > 1:
+            pst.merge_allreduce(first)  # same global statistics on every rank
+        else:
+            pst._merge(first.n, first.mean, first.m2)
         times = []
         for it in range(3):
             if world > 1:

@@ -541,11 +541,13 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
     }
     smem = base + size_t(wbuf) * 2;
   }
-  static size_t configured = 0;
-  if (smem > configured) {
+  static size_t configured[64] = {};  // per device (the attribute is)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || smem > configured[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_policy_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_policy_mlp attr: ") + cudaGetErrorString(e));
-    configured = smem;
+    if (dev >= 0 && dev < 64) configured[dev] = smem;
   }
   const dim3 grid((n_envs + kM - 1) / kM, value_out ? 2 : 1);
   k_policy_mlp<<<grid, kThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(

@@ -4,6 +4,7 @@
 
 #include "stampede_sim.h"
 #include "sim_device.cuh"
+#include "sim_launch.h"
 #include "stp_error.h"
 #include "stp_rng.h"
 
@@ -52,6 +53,9 @@ extern "C" int stp_debug_math(int32_t fn, const float* x, const float* y, float*
 
 namespace stp {
 int sim_dims(const stp_sim* s, int* n, int* J, uint64_t* seed, long long* off, void** stream);
+int sim_device(const stp_sim* s);
+int sim_order(stp_sim* s, void* stream);
+int sim_mark(stp_sim* s, void* stream);
 }
 
 extern "C" int stp_random_actions(stp_sim* sim, float* actions, uint64_t step, void* stream) {
@@ -63,11 +67,13 @@ extern "C" int stp_random_actions(stp_sim* sim, float* actions, uint64_t step, v
     return stp::fail(STP_EINVAL, "stp_random_actions: bad arguments");
   const long long total = (long long)n * J;
   if (total == 0) return STP_OK;
+  const stp::DeviceGuard dg_(stp::sim_device(sim));
   const int threads = 256;
   const int blocks = int((total + threads - 1) / threads);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream ? stream : own);
-  k_random_actions<<<blocks, threads, 0, st>>>(actions, n, J, seed, off, step);
+  void* sv = stream ? stream : own;
+  if (const int rc = stp::sim_order(sim, sv)) return rc;  // in call order with the handle's other work
+  k_random_actions<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(sv)>>>(actions, n, J, seed, off, step);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_random_actions: ") + cudaGetErrorString(e));
-  return STP_OK;
+  return stp::sim_mark(sim, sv);
 }

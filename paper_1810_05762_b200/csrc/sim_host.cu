@@ -21,12 +21,15 @@
 struct stp_sim {
   int device = 0;
   cudaStream_t stream = nullptr;
-  // Launches may run on a caller's stream (torch's current stream, the legacy
-  // default stream) while the accessors below run on the handle's non-blocking
-  // stream: the last caller-stream launch is recorded here and every accessor
-  // orders its copies after it (join_caller).
-  cudaEvent_t ev_caller = nullptr;
-  bool caller_pending = false;
+  // Launches may run on any stream (a caller's: torch's current stream, the
+  // legacy default stream; NULL: the handle's own non-blocking stream) and the
+  // accessors run on the handle's stream.  A handle is one sequential object
+  // (the reference's Scene): every launch is recorded in ev_last and the next
+  // launch or accessor on another stream waits on it (order_after_last), so
+  // work on one handle executes in call order whatever streams are mixed.
+  cudaEvent_t ev_caller = nullptr;  // ev_last
+  cudaStream_t last_stream = nullptr;
+  bool caller_pending = false;      // ev_last holds an unfinished launch
   int precision = STP_PRECISION_F32;
   int W = 32, cpb = 2, cap = 64;
   stp_model model{};
@@ -376,9 +379,11 @@ int launch_t(stp_sim* s, int mode, const float* torques, const float* actions, f
     // agents of the pre-step state (collide.cpp:300-343) merge envs into
     // islands solved together (solver.cpp:458-502); all on the device
     stp::IslandView v{};
+    const int cap = sizeof(T) == 4 ? stp::kIslandMax : stp::kIslandMax / 2;  // island_cap<T>
     cudaError_t e = stp::prepare_islands<T>(s->pairs, reinterpret_cast<const stp::DevModel<T>*>(s->d_model), s->B,
                                             reinterpret_cast<const T*>(s->d_state), s->d_origin, s->n, s->W,
-                                            s->cfg.contact_margin, &v, st);
+                                            s->cfg.contact_margin, cap, stp::island_launch_budget<T>(s->cpb), &v,
+                                            st);
     if (e != cudaSuccess) return cuda_fail(e, "inter-agent island preparation");
     a.merged = v.merged;
     a.isl_members = v.isl_members;
@@ -386,37 +391,53 @@ int launch_t(stp_sim* s, int mode, const float* torques, const float* actions, f
     a.isl_err = v.err;
     a.xslots = v.xslots;
     a.xcount = v.xcount;
+    a.big_count = v.big_count;
+    a.big_off = v.big_off;
+    a.big_size = v.big_size;
+    a.big_members = v.big_members;
+    a.big_bar = v.big_bar;
+    a.big_xch = reinterpret_cast<T*>(v.big_xch);
   }
   const cudaError_t e = stp::launch_env_step<T>(a, s->W, s->cpb, st);
   if (e != cudaSuccess) return cuda_fail(e, "k_env_step launch");
   return STP_OK;
 }
 
-// order the handle's stream after the last launch made on a caller's stream
-int join_caller(stp_sim* s) {
-  if (s->caller_pending) {
-    CK(cudaStreamWaitEvent(s->stream, s->ev_caller, 0));
-    s->caller_pending = false;
-  }
+// order stream `st` after the handle's last launch when that was made on
+// another stream
+int order_after_last(stp_sim* s, cudaStream_t st) {
+  if (s->caller_pending && s->last_stream != st) CK(cudaStreamWaitEvent(st, s->ev_caller, 0));
   return STP_OK;
+}
+// record a launch made on `st` as the handle's last one
+int mark_last(stp_sim* s, cudaStream_t st) {
+  CK(cudaEventRecord(s->ev_caller, st));
+  s->last_stream = st;
+  s->caller_pending = true;
+  return STP_OK;
+}
+// the accessors (handle's stream, synchronous): after every earlier launch
+int join_caller(stp_sim* s) { return order_after_last(s, s->stream); }
+
+bool is_chunk_stream(const stp_sim* s, cudaStream_t st) {
+  for (int c = 0; c < stp_sim::kChunks; ++c)
+    if (st == s->cs[c]) return true;
+  return false;
 }
 
 int launch(stp_sim* s, int mode, const float* torques, const float* actions, float* obs, float* reward,
            uint8_t* done, const uint8_t* mask, cudaStream_t st, int e_begin = 0, int e_end = -1) {
-  if (st == s->stream) {
-    if (const int rc = join_caller(s)) return rc;
-  }
+  // stp_step_host's chunk streams are ordered by that call itself (ev_in /
+  // ev_out), so its chunks overlap one another
+  const bool chunk = is_chunk_stream(s, st);
+  if (!chunk)
+    if (const int rc = order_after_last(s, st)) return rc;
   const int rc = s->precision == STP_PRECISION_F64
                      ? launch_t<double>(s, mode, torques, actions, obs, reward, done, mask, st, e_begin, e_end)
                      : launch_t<float>(s, mode, torques, actions, obs, reward, done, mask, st, e_begin, e_end);
   if (rc) return rc;
   if (mode != 2) s->loads_pending = false;
-  bool own = st == s->stream;  // the chunk streams of stp_step_host join before it returns
-  for (int c = 0; c < stp_sim::kChunks; ++c) own = own || st == s->cs[c];
-  if (!own) {
-    CK(cudaEventRecord(s->ev_caller, st));
-    s->caller_pending = true;
-  }
+  if (!chunk) return mark_last(s, st);
   return STP_OK;
 }
 
@@ -445,6 +466,10 @@ int sim_dims(const stp_sim* s, int* n, int* J, uint64_t* seed, long long* off, v
   *stream = reinterpret_cast<void*>(s->stream);
   return STP_OK;
 }
+int sim_device(const stp_sim* s) { return s ? s->device : 0; }
+// call-order sequencing of launches made outside this file (sim_aux.cu)
+int sim_order(stp_sim* s, void* st) { return order_after_last(s, reinterpret_cast<cudaStream_t>(st)); }
+int sim_mark(stp_sim* s, void* st) { return mark_last(s, reinterpret_cast<cudaStream_t>(st)); }
 }  // namespace stp
 
 extern "C" {
@@ -514,12 +539,15 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
     stp_destroy(s);
     return nullptr;
   };
-  cudaError_t e = cudaSetDevice(device);
+  int dev_count = 0;
+  cudaError_t e = cudaGetDeviceCount(&dev_count);
+  if (e == cudaSuccess && (device < 0 || device >= dev_count)) e = cudaErrorInvalidDevice;
   if (e != cudaSuccess) {
     cuda_fail(e, "cudaSetDevice");
     delete s;
     return nullptr;
   }
+  const stp::DeviceGuard dg_(device);  // the caller's current device is restored on return
   e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_caller, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -571,6 +599,7 @@ stp_sim* stp_create(const stp_model* model, const stp_task* task, const stp_step
 
 void stp_destroy(stp_sim* s) {
   if (!s) return;
+  const stp::DeviceGuard dg_(s->device);
   if (s->ev_caller) cudaEventSynchronize(s->ev_caller);
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (int c = 0; c < stp_sim::kChunks; ++c) {
@@ -589,6 +618,7 @@ void stp_destroy(stp_sim* s) {
 }
 
 int stp_set_terrain(stp_sim* s, const stp_static_box* boxes, int32_t n) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s || n < 0 || (n > 0 && !boxes)) return fail(STP_EINVAL, "stp_set_terrain: bad arguments");
   if (const int rc_ = join_caller(s)) return rc_;
   std::vector<double> h(size_t(std::max(n, 1)) * 8);
@@ -701,10 +731,12 @@ constexpr uint32_t kSnapshotVersion = 1;
 }  // namespace
 
 int64_t stp_snapshot_size(const stp_sim* s) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   return s ? int64_t(16) + int64_t(s->n) * s->B * STP_STATE_STRIDE * 8 : 0;
 }
 
 int stp_save_snapshot(stp_sim* s, uint8_t* buf, int64_t capacity) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s || !buf) return fail(STP_EINVAL, "stp_save_snapshot: bad arguments");
   if (const int rc_ = join_caller(s)) return rc_;
   const int64_t need = stp_snapshot_size(s);
@@ -717,6 +749,7 @@ int stp_save_snapshot(stp_sim* s, uint8_t* buf, int64_t capacity) {
 }
 
 int stp_load_snapshot(stp_sim* s, const uint8_t* buf, int64_t size) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s || !buf || size < 16) return fail(STP_EINVAL, "stp_load_snapshot: bad arguments");
   if (const int rc_ = join_caller(s)) return rc_;
   uint32_t magic, version;
@@ -735,6 +768,7 @@ int stp_load_snapshot(stp_sim* s, const uint8_t* buf, int64_t size) {
 
 int stp_detect_inter_agent(stp_sim* s, int32_t capacity, int32_t* count, int32_t* body_a, int32_t* body_b,
                            double* point, double* normal, double* separation) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s || !count || capacity < 0) return fail(STP_EINVAL, "stp_detect_inter_agent: bad arguments");
   if (const int rc_ = join_caller(s)) return rc_;
   bool overflow = false;
@@ -758,11 +792,13 @@ int stp_detect_inter_agent(stp_sim* s, int32_t capacity, int32_t* count, int32_t
 void* stp_stream(const stp_sim* s) { return s ? reinterpret_cast<void*>(s->stream) : nullptr; }
 
 int stp_reset(stp_sim* s, const uint8_t* mask, float* obs, void* stream) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s) return fail(STP_EINVAL, "stp_reset: null handle");
   return launch(s, 2, nullptr, nullptr, obs, nullptr, nullptr, mask, pick(s, stream));
 }
 
 int stp_step(stp_sim* s, const float* actions, float* obs, float* reward, uint8_t* done, void* stream) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s) return fail(STP_EINVAL, "stp_step: null handle");
   if (s->J > 0 && !actions) return fail(STP_EINVAL, "env_step: actions required");
   return launch(s, 1, nullptr, actions, obs, reward, done, nullptr, pick(s, stream));
@@ -785,6 +821,7 @@ static void* pinned_view(void* p) {
 }
 
 int stp_step_host(stp_sim* s, const float* actions, float* obs, float* reward, uint8_t* done) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s || (s->J > 0 && !actions)) return fail(STP_EINVAL, "stp_step_host: bad arguments");
   if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
@@ -839,16 +876,18 @@ int stp_step_host(stp_sim* s, const float* actions, float* obs, float* reward, u
   // later work on the handle's stream is ordered after every chunk
   for (int c = 0; c < C; ++c) CK(cudaStreamWaitEvent(s->stream, s->ev_out[c], 0));
   CK(cudaStreamSynchronize(s->stream));
-  return STP_OK;
+  return mark_last(s, s->stream);
 }
 
 int stp_physics_step(stp_sim* s, const float* torques, void* stream) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s) return fail(STP_EINVAL, "stp_physics_step: null handle");
   if (s->J > 0 && !torques) return fail(STP_EINVAL, "clamp_torques: torque count must equal joint count");
   return launch(s, 0, torques, nullptr, nullptr, nullptr, nullptr, nullptr, pick(s, stream));
 }
 
 int stp_physics_step_host(stp_sim* s, const double* torques) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s) return fail(STP_EINVAL, "stp_physics_step_host: null handle");
   if (const int rc_ = join_caller(s)) return rc_;
   if (s->J > 0 && !torques) return fail(STP_EINVAL, "clamp_torques: torque count must equal joint count");
@@ -866,6 +905,7 @@ int stp_physics_step_host(stp_sim* s, const double* torques) {
 
 
 int stp_set_state(stp_sim* s, const double* state) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s || !state) return fail(STP_EINVAL, "stp_set_state: bad arguments");
   if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
@@ -912,6 +952,7 @@ int stp_set_state(stp_sim* s, const double* state) {
 }
 
 int stp_get_state(stp_sim* s, double* state) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s || !state) return fail(STP_EINVAL, "stp_get_state: bad arguments");
   if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
@@ -935,6 +976,7 @@ int stp_get_state(stp_sim* s, double* state) {
 }
 
 int stp_set_external_loads(stp_sim* s, const double* loads) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s || !loads) return fail(STP_EINVAL, "stp_set_external_loads: bad arguments");
   if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
@@ -956,6 +998,7 @@ int stp_set_external_loads(stp_sim* s, const double* loads) {
 
 int stp_get_contacts(stp_sim* s, int32_t* count, int32_t* body_a, int32_t* body_b, double* point, double* normal,
                      double* separation, double* normal_impulse, double* tangential_impulse) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s) return fail(STP_EINVAL, "stp_get_contacts: null handle");
   if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n), C = size_t(s->cap);
@@ -986,6 +1029,7 @@ int stp_get_contacts(stp_sim* s, int32_t* count, int32_t* body_a, int32_t* body_
 }
 
 int stp_get_report(stp_sim* s, int32_t* newton, int32_t* krylov, uint8_t* failed, uint8_t* overflow) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s) return fail(STP_EINVAL, "stp_get_report: null handle");
   if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n);
@@ -998,6 +1042,7 @@ int stp_get_report(stp_sim* s, int32_t* newton, int32_t* krylov, uint8_t* failed
 }
 
 int stp_get_task_state(stp_sim* s, double* target, int32_t* counters, double* last_tau) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s) return fail(STP_EINVAL, "stp_get_task_state: null handle");
   if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n), J = size_t(s->J);
@@ -1020,6 +1065,7 @@ int stp_get_task_state(stp_sim* s, double* target, int32_t* counters, double* la
 }
 
 int stp_set_task_state(stp_sim* s, const double* target, const int32_t* counters, const double* last_tau) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
   if (!s) return fail(STP_EINVAL, "stp_set_task_state: null handle");
   if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n), J = size_t(s->J);

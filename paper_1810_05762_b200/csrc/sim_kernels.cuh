@@ -37,7 +37,8 @@ struct XSlot {
   double sep;
 };
 constexpr int kXSlots = 4;      // cross contacts per body
-constexpr int kIslandMax = 8;   // envs per merged island (one warp each)
+constexpr int kIslandMax = 8;   // envs per merged island of the one-CTA launch (one warp each)
+constexpr int kBigIslands = 64; // islands larger than that per step (multi-CTA launch)
 
 template <class T>
 struct KArgs {
@@ -89,7 +90,21 @@ struct KArgs {
   const XSlot* xslots;        // [n * B][kXSlots] cross contacts of each body
   const int* xcount;          // [n * B]
   const int* isl_err;         // preparation overflow bits (see IslandView)
+  // islands larger than one CTA's warps (multi-CTA launch, sim_pairs.cu
+  // k_islands): CTA c of the launch takes part p of big island i; the
+  // island's warps exchange through a global area and a global barrier
+  int isl_big_mode;           // 0: one CTA per island (isl_members), 1: big islands
+  const int* big_count;       // number of big islands this step
+  const int* big_off;         // [kBigIslands] first member in big_members
+  const int* big_size;        // [kBigIslands] member count
+  const int* big_members;     // member envs (unordered within an island)
+  int* big_bar;               // [kBigIslands] barrier arrival counters (zeroed per step)
+  T* big_xch;                 // [sum of sizes][kBigStride] exchange / reduction area
 };
+// per-env entries of the big islands' global exchange area: 32 lanes x kXch,
+// 4 reduction partials, 1 vote
+constexpr int kXchEntries = 21;
+constexpr int kBigStride = 32 * kXchEntries + 5;
 
 enum { C_FRAME = 0, C_FLAG = 1, C_FALL = 2, C_NEXTP = 3, C_EPISODE = 4, C_FLAGDRAW = 5, C_PERTDRAW = 6 };
 constexpr int kGridCols = 64;

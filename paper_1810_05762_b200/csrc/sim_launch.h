@@ -5,6 +5,30 @@
 #include "sim_kernels.cuh"
 
 namespace stp {
+// Runs an entry point on its handle's device and restores the caller's
+// current device afterwards (handles on several GPUs in one process).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != device && cudaSetDevice(device) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+// per-device one-time kernel attribute setup (cudaFuncSetAttribute is per device)
+inline bool first_on_device(bool (&done)[64]) {
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) return true;
+  if (done[d]) return false;
+  done[d] = true;
+  return true;
+}
+
 // Global scratch rows per lane of every env (sim_step.cuh: G_QH, G_HD, G_LC,
 // then 12 overflow contact slots of 11 rows for the terrain instantiation,
 // whose 4 first slots per body live in shared memory, then the island mode's
@@ -19,19 +43,34 @@ constexpr int kScratchRows = 55 + 11 * kSpillSlots + kXSlotRows * kXSlots;
 template <class T>
 cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s);
 
+// CTAs of the island launch that are co-resident on the current device (the
+// budget of big-island parts per step, sim_step.cuh big_island_ctas).
+template <class T>
+int island_launch_budget(int cpb);
+
 struct PairScratch;
 // Device view of the step's inter-agent coupling (prepare_islands).
 struct IslandView {
-  const uint8_t* merged;
+  const uint8_t* merged;  // 1: stepped by an island launch, 2: island over budget (stepped alone, flagged)
   const int* isl_members;
   const int* isl_count;
-  int* err;  // bit 1: more than kXSlots cross contacts on a body, 2: island larger than kIslandMax
+  int* err;  // bit 1: more than kXSlots cross contacts on a body, 4: contact edges dropped,
+             // 8: candidate env pairs dropped (pair capacity)
   const XSlot* xslots;
   const int* xcount;
+  // islands larger than `cap` envs (multi-CTA launch)
+  const int* big_count;
+  const int* big_off;
+  const int* big_size;
+  const int* big_members;
+  int* big_bar;
+  void* big_xch;
 };
+// cap = envs per one-CTA island (island_cap<T>), max_parts = island_launch_budget
 template <class T>
 cudaError_t prepare_islands(PairScratch*& scratch, const DevModel<T>* model, int B, const T* state,
-                            const double* origin, int n, int W, double margin, IslandView* view, cudaStream_t st);
+                            const double* origin, int n, int W, double margin, int cap, int max_parts,
+                            IslandView* view, cudaStream_t st);
 
 // Inter-agent contact detection (sim_pairs.cu): the reference's dynamic-pair
 // contacts of every env of a sim, global body indices, reference order.

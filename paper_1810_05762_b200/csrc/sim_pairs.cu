@@ -312,6 +312,7 @@ __global__ void k_narrow_slots(const int2* __restrict__ pairs, const int* __rest
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int np = min(*n_pairs_p, pair_cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && *n_pairs_p > pair_cap) atomicOr(err, 8);  // candidates dropped
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < np; w += nwarps) {
     const int2 pr = pairs[w];
     for (int u = lane; u < B * B; u += 32) {
@@ -374,15 +375,22 @@ __global__ void k_narrow_slots(const int2* __restrict__ pairs, const int* __rest
 // the propagation and pointer-jumping passes run over the edges alone.
 __global__ void k_islands(int n, const int2* __restrict__ edges, const int* __restrict__ n_edges_p, int edge_cap,
                           int* __restrict__ label, uint8_t* __restrict__ merged, int* __restrict__ isl_of,
-                          int* __restrict__ isl_size, int* __restrict__ isl_members, int* __restrict__ isl_count,
-                          int* __restrict__ err, int labels_in_smem) {
+                          int* __restrict__ isl_size, int* __restrict__ isl_fill, int* __restrict__ isl_big,
+                          int* __restrict__ isl_members, int* __restrict__ isl_count, int* __restrict__ err,
+                          int labels_in_smem, int cap, int max_parts, int* __restrict__ big_count,
+                          int* __restrict__ big_off, int* __restrict__ big_size, int* __restrict__ big_fill,
+                          int* __restrict__ big_members, int* __restrict__ big_bar) {
   extern __shared__ int slab[];
-  __shared__ int changed;
+  __shared__ int changed, any_big;
   int* L = labels_in_smem ? slab : label;
   const int ne = min(*n_edges_p, edge_cap);
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     L[e] = e;
     merged[e] = 0;
+  }
+  if (threadIdx.x == 0) {
+    any_big = 0;
+    *big_count = 0;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < ne; i += blockDim.x) {
@@ -416,21 +424,61 @@ __global__ void k_islands(int n, const int2* __restrict__ edges, const int* __re
     __syncthreads();
     if (!changed) break;
   }
+  // one record per island (root = its smallest env), then the sizes
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     if (merged[e] && L[e] == e) {
       const int i = atomicAdd(isl_count, 1);
       isl_of[e] = i;
       isl_size[i] = 0;
+      isl_fill[i] = 0;
+      isl_big[i] = -1;
       for (int k = 0; k < kIslandMax; ++k) isl_members[i * kIslandMax + k] = -1;
     }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n; e += blockDim.x)
+    if (merged[e]) atomicAdd(&isl_size[isl_of[L[e]]], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < n; e += blockDim.x)
+    if (merged[e] && L[e] == e && isl_size[isl_of[e]] > cap) any_big = 1;
+  __syncthreads();
+  if (any_big && threadIdx.x == 0) {
+    // islands larger than one CTA: records in root order (deterministic), as
+    // long as their CTA parts fit the co-resident budget of the launch;
+    // beyond it an island is stepped env by env and flagged (merged = 2)
+    int nb = 0, off = 0, parts = 0;
+    for (int e = 0; e < n; ++e) {
+      if (!merged[e] || L[e] != e) continue;
+      const int i = isl_of[e], m = isl_size[i];
+      if (m <= cap) continue;
+      const int p = (m + cap - 1) / cap;
+      if (nb < kBigIslands && parts + p <= max_parts) {
+        big_off[nb] = off;
+        big_size[nb] = m;
+        big_fill[nb] = 0;
+        big_bar[nb] = 0;
+        isl_big[i] = nb++;
+        off += m;
+        parts += p;
+      } else {
+        isl_big[i] = -2;
+        atomicOr(err, 2);
+      }
+    }
+    *big_count = nb;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     if (!merged[e]) continue;
     const int i = isl_of[L[e]];
-    const int pos = atomicAdd(&isl_size[i], 1);
-    if (pos < kIslandMax) isl_members[i * kIslandMax + pos] = e;
-    else atomicOr(err, 2);
+    const int bi = isl_big[i];
+    if (bi >= 0) {
+      big_members[big_off[bi] + atomicAdd(&big_fill[bi], 1)] = e;
+    } else if (bi == -2) {
+      merged[e] = 2;
+    } else {
+      isl_members[i * kIslandMax + atomicAdd(&isl_fill[i], 1)] = e;
+    }
   }
 }
 
@@ -467,7 +515,12 @@ struct PairScratch {
   int2* edges = nullptr;
   int* icnt = nullptr;  // [0] edges, [1] islands, [2] error bits
   int *label = nullptr, *isl_of = nullptr, *isl_size = nullptr, *isl_members = nullptr;
+  int *isl_fill = nullptr, *isl_big = nullptr;
   uint8_t* merged = nullptr;
+  // big islands: [0] count, then off / size / fill / barrier [kBigIslands] each
+  int* big = nullptr;
+  int* big_members = nullptr;
+  void* big_xch = nullptr;  // [n][kBigStride] doubles (either precision fits)
 };
 
 void pair_scratch_free(PairScratch* p) {
@@ -476,7 +529,8 @@ void pair_scratch_free(PairScratch* p) {
                   (void*)p->cidx, (void*)p->scidx, p->tmp, (void*)p->xslots, (void*)p->xcount, (void*)p->edges,
                   (void*)p->icnt, (void*)p->label, (void*)p->isl_of, (void*)p->isl_size, (void*)p->isl_members,
                   (void*)p->merged, (void*)p->env_cell, (void*)p->bin_count, (void*)p->bins, (void*)p->ovf,
-                  (void*)p->gcnt})
+                  (void*)p->gcnt, (void*)p->isl_fill, (void*)p->isl_big, (void*)p->big, (void*)p->big_members,
+                  p->big_xch})
     if (q) cudaFree(q);
   delete p;
 }
@@ -588,7 +642,8 @@ cudaError_t detect_pairs(PairScratch*& P, const DevModel<T>* model, int B, const
 // slots per body, env islands and the merged flags (no host round trip).
 template <class T>
 cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, const T* state, const double* origin,
-                            int n, int W, double margin, IslandView* view, cudaStream_t st) {
+                            int n, int W, double margin, int cap, int max_parts, IslandView* view,
+                            cudaStream_t st) {
   cudaError_t e = cudaSuccess;
 #define STP_CK(x)                   \
   do {                              \
@@ -606,7 +661,8 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
   }
   if (P->isl_n < size_t(n)) {
     for (void* q : {(void*)P->xslots, (void*)P->xcount, (void*)P->edges, (void*)P->icnt, (void*)P->label,
-                    (void*)P->isl_of, (void*)P->isl_size, (void*)P->isl_members, (void*)P->merged})
+                    (void*)P->isl_of, (void*)P->isl_size, (void*)P->isl_members, (void*)P->merged,
+                    (void*)P->isl_fill, (void*)P->isl_big, (void*)P->big, (void*)P->big_members, P->big_xch})
       if (q) cudaFree(q);
     P->isl_n = n;
     STP_CK(cudaMalloc(&P->xslots, sizeof(XSlot) * size_t(n) * B * kXSlots));
@@ -618,6 +674,11 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
     STP_CK(cudaMalloc(&P->isl_size, sizeof(int) * (n / 2 + 1)));
     STP_CK(cudaMalloc(&P->isl_members, sizeof(int) * (n / 2 + 1) * kIslandMax));
     STP_CK(cudaMalloc(&P->merged, n));
+    STP_CK(cudaMalloc(&P->isl_fill, sizeof(int) * (n / 2 + 1)));
+    STP_CK(cudaMalloc(&P->isl_big, sizeof(int) * (n / 2 + 1)));
+    STP_CK(cudaMalloc(&P->big, sizeof(int) * (1 + 4 * kBigIslands)));
+    STP_CK(cudaMalloc(&P->big_members, sizeof(int) * n));
+    STP_CK(cudaMalloc(&P->big_xch, sizeof(double) * kBigStride * size_t(n)));
   }
   const int edge_cap = n * B * kXSlots;
   STP_CK(cudaMemsetAsync(P->counters, 0, sizeof(int) * 2, st));
@@ -629,14 +690,14 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
   // labels in shared memory up to 48K envs (192 KB), else in global scratch
   const size_t lab_bytes = size_t(n) * sizeof(int);
   const bool lab_smem = lab_bytes <= 192 * 1024;
-  static size_t lab_attr = 48 * 1024;
-  if (lab_smem && lab_bytes > lab_attr) {
+  static bool lab_attr[64] = {};  // per device
+  if (lab_smem && lab_bytes > 48 * 1024 && first_on_device(lab_attr))
     STP_CK(cudaFuncSetAttribute(k_islands, cudaFuncAttributeMaxDynamicSharedMemorySize, int(192 * 1024)));
-    lab_attr = 192 * 1024;
-  }
-  k_islands<<<1, 1024, lab_smem ? lab_bytes : 0, st>>>(n, P->edges, P->icnt, edge_cap, P->label, P->merged,
-                                                       P->isl_of, P->isl_size, P->isl_members, P->icnt + 1,
-                                                       P->icnt + 2, int(lab_smem));
+  int* bg = P->big;
+  k_islands<<<1, 1024, lab_smem ? lab_bytes : 0, st>>>(
+      n, P->edges, P->icnt, edge_cap, P->label, P->merged, P->isl_of, P->isl_size, P->isl_fill, P->isl_big,
+      P->isl_members, P->icnt + 1, P->icnt + 2, int(lab_smem), cap, max_parts, bg, bg + 1, bg + 1 + kBigIslands,
+      bg + 1 + 2 * kBigIslands, P->big_members, bg + 1 + 3 * kBigIslands);
   STP_CK(cudaGetLastError());
   view->merged = P->merged;
   view->isl_members = P->isl_members;
@@ -644,14 +705,20 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
   view->err = P->icnt + 2;
   view->xslots = P->xslots;
   view->xcount = P->xcount;
+  view->big_count = bg;
+  view->big_off = bg + 1;
+  view->big_size = bg + 1 + kBigIslands;
+  view->big_members = P->big_members;
+  view->big_bar = bg + 1 + 3 * kBigIslands;
+  view->big_xch = P->big_xch;
   return cudaSuccess;
 #undef STP_CK
 }
 
 template cudaError_t prepare_islands<float>(PairScratch*&, const DevModel<float>*, int, const float*, const double*,
-                                            int, int, double, IslandView*, cudaStream_t);
+                                            int, int, double, int, int, IslandView*, cudaStream_t);
 template cudaError_t prepare_islands<double>(PairScratch*&, const DevModel<double>*, int, const double*,
-                                             const double*, int, int, double, IslandView*, cudaStream_t);
+                                             const double*, int, int, double, int, int, IslandView*, cudaStream_t);
 
 template cudaError_t detect_pairs<float>(PairScratch*&, const DevModel<float>*, int, const float*, const double*, int,
                                          int, double, int, int*, int32_t*, int32_t*, double*, double*, double*, bool*,

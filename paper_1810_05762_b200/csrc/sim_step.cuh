@@ -15,6 +15,8 @@
 // Instantiated per precision in sim_step_f32.cu / sim_step_f64.cu.
 #pragma once
 #include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "sim_kernels.cuh"
@@ -429,40 +431,68 @@ template <class T>
 __host__ __device__ constexpr int island_cap() {
   return sizeof(T) == 4 ? kIslandMax : kIslandMax / 2;
 }
-constexpr int kXch = 21;  // per-lane exchange entries (Mi is the largest)
+constexpr int kXch = kXchEntries;  // per-lane exchange entries (Mi is the largest)
 
 template <class T, int W, int CPB, bool ISL = false>
 __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
     k_env_step(const KArgs<T> a) {
   int e;
   int isl_m = 1, isl_w = 0;  // island size and this warp's place in it
+  const int* mem = nullptr;  // the island's member envs (unordered)
+  int* bar_ctr = nullptr;    // big islands: global barrier counter
+  T* big_area = nullptr;     // big islands: the island's global exchange area
   if constexpr (ISL) {
     static_assert(W == 32, "island mode: one env per warp");
-    if (blockIdx.x >= unsigned(*a.isl_count)) return;
-    const int* mem = a.isl_members + blockIdx.x * kIslandMax;
-    isl_m = 0;
-    for (int k = 0; k < kIslandMax; ++k) isl_m += mem[k] >= 0;
-    if (isl_m > island_cap<T>() || *a.isl_err) {
-      // island beyond this instantiation's capacity, or cross contacts were
-      // dropped in preparation: not stepped, flagged (stp_get_report overflow)
-      if (threadIdx.x == 0 && a.overflow_out)
-        for (int k = 0; k < kIslandMax; ++k)
-          if (mem[k] >= 0) a.overflow_out[mem[k]] = 1;
-      if (isl_m > island_cap<T>()) return;
-    }
-    isl_w = threadIdx.x >> 5;
-    if (isl_w >= isl_m) return;  // before the first island barrier
-    e = -1;
-    for (int k = 0; k < isl_m; ++k) {
-      int rank = 0;
-      for (int j = 0; j < isl_m; ++j) rank += mem[j] < mem[k];
-      if (rank == isl_w) e = mem[k];
+    constexpr int cap = island_cap<T>();
+    if (a.isl_big_mode) {
+      // this CTA's (big island, part): parts of an island are consecutive CTAs
+      const int nbig = *a.big_count;
+      int acc = 0, bi = -1, part = 0;
+      for (int i = 0; i < nbig; ++i) {
+        const int p = (a.big_size[i] + cap - 1) / cap;
+        if (int(blockIdx.x) < acc + p) {
+          bi = i;
+          part = int(blockIdx.x) - acc;
+          break;
+        }
+        acc += p;
+      }
+      if (bi < 0) return;
+      isl_m = a.big_size[bi];
+      mem = a.big_members + a.big_off[bi];
+      isl_w = part * cap + int(threadIdx.x >> 5);
+      if (isl_w >= isl_m) return;  // never arrives at the island barrier
+      bar_ctr = a.big_bar + bi;
+      big_area = a.big_xch + size_t(a.big_off[bi]) * kBigStride;
+      // env = the member of rank isl_w (index order = the reference's slot order)
+      const int ln = threadIdx.x & 31;
+      int found = -1;
+      for (int k = ln; k < isl_m; k += 32) {
+        const int mk = mem[k];
+        int rank = 0;
+        for (int j = 0; j < isl_m; ++j) rank += mem[j] < mk;
+        if (rank == isl_w) found = mk;
+      }
+      e = __reduce_max_sync(0xffffffffu, found);
+    } else {
+      if (blockIdx.x >= unsigned(*a.isl_count)) return;
+      mem = a.isl_members + blockIdx.x * kIslandMax;
+      isl_m = 0;
+      for (int k = 0; k < kIslandMax; ++k) isl_m += mem[k] >= 0;
+      isl_w = threadIdx.x >> 5;
+      if (isl_w >= isl_m) return;  // before the first island barrier (big islands: isl_m = 0 here)
+      e = -1;
+      for (int k = 0; k < isl_m; ++k) {
+        int rank = 0;
+        for (int j = 0; j < isl_m; ++j) rank += mem[j] < mem[k];
+        if (rank == isl_w) e = mem[k];
+      }
     }
   } else {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     e = a.e_begin + tid / W;
     if (e >= a.n) return;  // whole segments exit together
-    if (a.merged && a.merged[e]) return;  // stepped by the island launch
+    if (a.merged && a.merged[e] == 1) return;  // stepped by the island launch
   }
   const int lane = threadIdx.x & 31;
   const int b = lane % W;
@@ -483,12 +513,36 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
   extern __shared__ unsigned char smem_raw[];
   Lane<T, W> L;
   L.sm = reinterpret_cast<T*>(smem_raw) + (threadIdx.x >> 5) * (smem_rows<CPB>() * 32);
-  // island exchange area (ISL): per-lane entries, reduction partials, votes
+  // island exchange area (ISL): per-lane entries, reduction partials, votes;
+  // shared memory for one-CTA islands, a global area for big islands
   T* xch = reinterpret_cast<T*>(smem_raw) + (ISL ? island_cap<T>() : 0) * smem_rows<CPB>() * 32;
   T* red = xch + (ISL ? island_cap<T>() * 32 * kXch : 0);
   int* vote = reinterpret_cast<int*>(red + 4 * island_cap<T>());
+  if (ISL && big_area) {
+    xch = big_area;
+    red = xch + size_t(isl_m) * 32 * kXch;
+    vote = reinterpret_cast<int*>(red + 4 * isl_m);
+  }
+  int bar_gen = 0;
   auto isl_bar = [&]() {
-    if constexpr (ISL) asm volatile("bar.sync 1, %0;\n" ::"r"(32 * isl_m) : "memory");
+    if constexpr (ISL) {
+      if (bar_ctr) {
+        // all warps of a big island (several CTAs, co-resident by the
+        // cooperative launch): generation-counted global barrier
+        __syncwarp();
+        ++bar_gen;
+        if ((threadIdx.x & 31) == 0) {
+          __threadfence();
+          atomicAdd(bar_ctr, 1);
+          const int target = bar_gen * isl_m;
+          while (*reinterpret_cast<volatile int*>(bar_ctr) < target) __nanosleep(32);
+          __threadfence();
+        }
+        __syncwarp();
+      } else {
+        asm volatile("bar.sync 1, %0;\n" ::"r"(32 * isl_m) : "memory");
+      }
+    }
   };
   // segment sums / votes over the whole island (the warp forms without ISL)
   auto isl_sum = [&](T v) -> T {
@@ -1122,7 +1176,6 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
           ord[s2] = ord[s2 - 1];
           ord[s2 - 1] = t;
         }
-      const int* mem = a.isl_members + blockIdx.x * kIslandMax;
       T* my = xch + (isl_w * 32 + lane) * kXch;
       my[0] = inv_m;
       my[1] = Iinv.xx;
@@ -2116,7 +2169,13 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
     }
   }
   if (a.mode != 2 && a.overflow_out) {
-    const bool ov = __any_sync(mask, overflow);
+    bool ov = __any_sync(mask, overflow);
+    // flagged in the island preparation (reported, never silent): island
+    // steps when cross contacts were dropped; an env whose island did not
+    // fit the island launches (merged 2, stepped alone) or when candidate
+    // env pairs were dropped (bit 8)
+    if constexpr (ISL) ov = ov || *a.isl_err != 0;
+    else if (a.merged) ov = ov || a.merged[e] == 2 || (*a.isl_err & 8) != 0;
     if (b == 0) a.overflow_out[e] = ov ? 1 : 0;
   }
 }
@@ -2125,12 +2184,11 @@ template <class T, int W, int CPB>
 static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
   constexpr int threads = kStepThreads;
   const size_t smem = size_t(threads / 32) * smem_rows<CPB>() * 32 * sizeof(T);
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[64] = {};
+  if (first_on_device(configured)) {
     cudaError_t err = cudaFuncSetAttribute(k_env_step<T, W, CPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(smem));
     if (err != cudaSuccess) return err;
-    configured = true;
   }
   const long long total = (long long)(a.n - a.e_begin) * W;
   const int blocks = int((total + threads - 1) / threads);
@@ -2138,21 +2196,62 @@ static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <class T, int CPB>
+int big_island_ctas();
+
 template <class T, int W, int CPB>
 static cudaError_t launch_island(const KArgs<T>& a, cudaStream_t s) {
   constexpr int cap = island_cap<T>();
   const size_t smem = size_t(cap) * smem_rows<CPB>() * 32 * sizeof(T) + size_t(cap) * 32 * kXch * sizeof(T) +
                       size_t(4 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[64] = {};
+  if (first_on_device(configured)) {
     cudaError_t err = cudaFuncSetAttribute(k_env_step<T, W, CPB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(smem));
     if (err != cudaSuccess) return err;
-    configured = true;
   }
   const int grid = (a.n - a.e_begin) / 2 > 0 ? (a.n - a.e_begin) / 2 : 1;  // at most n/2 merged islands
   k_env_step<T, W, CPB, true><<<grid, 32 * cap, smem, s>>>(a);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !a.big_count) return e;
+  // islands with more envs than one CTA holds: consecutive CTAs per island,
+  // all co-resident (cooperative launch) so the island's global barrier
+  // cannot wait on an unscheduled CTA; CTAs without a part exit at once
+  KArgs<T> b = a;
+  b.isl_big_mode = 1;
+  void* args[] = {&b};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_env_step<T, W, CPB, true>),
+                                     dim3(big_island_ctas<T, CPB>()), dim3(32 * cap), args, smem, s);
+}
+
+// co-resident CTAs of the island launch on this device: the part budget of
+// the big islands (k_islands flags islands beyond it)
+template <class T, int CPB>
+int big_island_ctas() {
+  static int per_dev[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 1;
+  if (!per_dev[dev]) {
+    constexpr int cap = island_cap<T>();
+    const size_t smem = size_t(cap) * smem_rows<CPB>() * 32 * sizeof(T) + size_t(cap) * 32 * kXch * sizeof(T) +
+                        size_t(4 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
+    cudaFuncSetAttribute(k_env_step<T, 32, CPB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_env_step<T, 32, CPB, true>, 32 * cap, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    per_dev[dev] = per_sm * sms > 0 ? per_sm * sms : 1;
+  }
+  return per_dev[dev];
+}
+
+template <class T>
+int island_launch_budget(int cpb) {
+  // STP_ISLAND_BUDGET (tests only) lowers the budget to exercise the
+  // over-budget path (islands stepped env by env and flagged)
+  static const char* env = getenv("STP_ISLAND_BUDGET");
+  const int lim = cpb <= 2 ? big_island_ctas<T, 2>() : big_island_ctas<T, 4>();
+  return env ? std::min(lim, atoi(env)) : lim;
 }
 
 template <class T>

@@ -2,4 +2,5 @@
 
 namespace stp {
 template cudaError_t launch_env_step<float>(const KArgs<float>&, int, int, cudaStream_t);
+template int island_launch_budget<float>(int);
 }  // namespace stp

@@ -2,4 +2,5 @@
 
 namespace stp {
 template cudaError_t launch_env_step<double>(const KArgs<double>&, int, int, cudaStream_t);
+template int island_launch_budget<double>(int);
 }  // namespace stp

@@ -179,7 +179,9 @@ def rollout(env, kernel, obs_stat: RunningStat, frames: int, seed: int, step0: i
     """Collect `frames` env steps for every agent of this rank on the GPU.
     Returns [T, N] tensors and the raw observations (for the RunningStat)."""
     dev = torch.device("cuda", env.device)
-    obs = env.reset() if step0 == 0 else env.last_obs
+    obs = getattr(env, "last_obs", None)
+    if obs is None:  # first rollout of a fresh env (train.py resets once and sets last_obs)
+        obs = env.reset()
     N, O = obs.shape
     A = env.action_dim
     buf = {k: [] for k in ("obs", "act", "logp", "val", "rew", "done")}

@@ -47,7 +47,16 @@ def main(argv=None):
     learner = PPOLearner(model, cfg)  # broadcasts rank 0's parameters
     kern = PolicyKernel(model, dev)
     stat = RunningStat(env.obs_dim, device=dev)
-    stat.push(env.reset())
+    # the initial observations enter the statistics like every later batch:
+    # pushed locally, then merged over ranks (one allreduce), so every rank
+    # whitens with the same global statistics
+    env.last_obs = env.reset()
+    first = RunningStat(env.obs_dim, device=dev)
+    first.push(env.last_obs)
+    if world > 1:
+        stat.merge_allreduce(first)
+    else:
+        stat._merge(first.n, first.mean, first.m2)
     step = 0
     for it in range(args.iters):
         if world > 1:

@@ -180,3 +180,24 @@ def no_plane(cfg):
 
 def tile(state, n):
     return np.repeat(state[None], n, axis=0)
+
+
+def chain_state(st, model, chains, dx=0.45):
+    """Agents of each run [start, start + length) turned by 90 degrees about
+    their roots and set side by side 0.45 m apart: neighbours touch hand to
+    hand (<= 3 inter-agent contacts per body), one island per run."""
+    q = quat_axis_angle((0, 0, 1), np.pi / 2)
+    r = model.root
+    for start, length in chains:
+        x0, y0 = st[start, r, 0], st[start, r, 1]
+        for k in range(length):
+            e = start + k
+            root = st[e, r, :3].copy()
+            for b in range(model.n_bodies):
+                st[e, b, :3] = root + qrot(q, st[e, b, :3] - root)
+                st[e, b, 3:7] = qmul(q, st[e, b, 3:7])
+                st[e, b, 7:10] = qrot(q, st[e, b, 7:10])
+                st[e, b, 10:13] = qrot(q, st[e, b, 10:13])
+            st[e, :, 0] += x0 + k * dx - st[e, r, 0]
+            st[e, :, 1] += y0 - st[e, r, 1]
+    return st

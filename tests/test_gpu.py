@@ -515,3 +515,51 @@ def test_accessors_order_after_caller_stream_launches(precision):
         assert not np.array_equal(s_async, s_before)
         np.testing.assert_array_equal(rep_async["krylov_iterations"], g.report()["krylov_iterations"])
         s_before = s_async
+
+
+@pytest.mark.parametrize("first", ["handle", "torch_side_stream"])
+def test_launches_in_call_order_across_streams(first):
+    """a launch on one stream must run after the handle's earlier
+    launches on any other stream (the handle's own stream via NULL, another
+    caller stream).  A 10 ms GPU spin delays the first launch; the second,
+    issued at once on torch's default stream, must still see its result."""
+    import ctypes as C
+    import torch
+    n = 1024
+    a = VecEnv("humanoid", n_envs=n, seed=17)
+    b = VecEnv("humanoid", n_envs=n, seed=17)
+    acts = [a.random_actions(t) for t in range(2)]
+    torch.cuda.synchronize()
+    if first == "handle":
+        ext = torch.cuda.ExternalStream(a.stream)
+        with torch.cuda.stream(ext):
+            torch.cuda._sleep(20_000_000)
+        assert a.lib.stp_step(a._h, C.c_void_p(acts[0].data_ptr()), None, None, None, None) == 0  # NULL stream
+    else:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            torch.cuda._sleep(20_000_000)
+            a.step(acts[0])
+    o1, r1, d1 = a.step(acts[1])  # torch's current (legacy default) stream
+    torch.cuda.synchronize()
+    b.step(acts[0])
+    torch.cuda.synchronize()
+    o2, r2, d2 = b.step(acts[1])
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(r1, r2)
+    np.testing.assert_array_equal(a.get_state(), b.get_state())
+
+
+def test_handle_restores_callers_device():
+    """entry points run on the handle's device and leave the
+    caller's current device unchanged (stp_create included)."""
+    import torch
+    torch.cuda.set_device(0)
+    g = VecEnv("humanoid", n_envs=8, seed=1, device=0)
+    g.step(g.random_actions(0))
+    torch.cuda.synchronize()
+    assert torch.cuda.current_device() == 0
+    with pytest.raises((ValueError, RuntimeError)):
+        VecEnv("humanoid", n_envs=8, seed=1, device=torch.cuda.device_count())  # no such device
+    assert torch.cuda.current_device() == 0

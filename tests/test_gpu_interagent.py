@@ -167,3 +167,89 @@ def test_contact_merged_islands_match_reference(precision):
         assert dx.max() <= 1e-7 and dv.max() <= 1e-4
     else:
         assert np.quantile(dx, 0.99) <= 1e-4 and dx.max() <= 5e-3
+
+
+def _chains(o, n, chains):
+    o.set_state(S.chain_state(o.get_state(), o.model, chains))
+
+
+@pytest.mark.skipif(not oracle.available("reference"), reason="compiled reference (oracle/_ref) not built")
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_big_islands_match_reference(precision):
+    """Islands of any size (solver.cpp:458-502 has no cap): a 12-agent chain
+    and a 5-agent chain (more envs than one island CTA holds: 8 in f32, 4 in
+    f64) are solved by the multi-CTA island launch as one system each.
+    Teacher-forced against the compiled reference: f64 |dx| <= 1e-7 m with
+    identical ordered contact lists, f32 the SURVEY §8(c) bounds; no env
+    reports an overflow."""
+    n = 24
+    g = VecEnv("hfh", n_envs=n, precision=precision, seed=41)
+    o = oracle.OracleEnv(g.model, g.task, g.cfg, n, seed=41, kind="reference")
+    _chains(o, n, [(0, 12), (12, 5), (18, 2)])
+    tm = np.array([g.model.joints[j].max_torque for j in range(g.action_dim)])
+    dxs = []
+    for t in range(5):
+        s = o.get_state()
+        g.set_state(s)
+        if t == 0:  # the chains really are single islands: consecutive members touch
+            d = g.detect_inter_agent()
+            nb = g.n_bodies
+            links = {(a // nb, b // nb) for a, b in zip(d["body_a"].tolist(), d["body_b"].tolist())}
+            for start, length in [(0, 12), (12, 5)]:
+                assert all((e, e + 1) in links for e in range(start, start + length - 1)), links
+        tq = o.random_actions(t) * tm
+        o.physics_step(tq)
+        g.physics_step(tq)
+        so, sg = o.get_state(), g.get_state()
+        if precision == "f64":
+            co, cg = o.contact_arrays(g.contact_capacity), g.contact_arrays()
+            np.testing.assert_array_equal(co["count"], cg["count"])
+            for e in range(n):
+                c = co["count"][e]
+                np.testing.assert_array_equal(co["body_a"][e, :c], cg["body_a"][e, :c])
+                np.testing.assert_array_equal(co["body_b"][e, :c], cg["body_b"][e, :c])
+        dxs.append(np.abs(so[..., :3] - sg[..., :3]).max(axis=(1, 2)))
+        rep = g.report()
+        assert rep["overflow"].sum() == 0 and rep["failed"].sum() == 0
+    dx = np.concatenate(dxs)
+    print(f"{precision}: |dx| max {dx.max():.2e} p99 {np.quantile(dx, 0.99):.2e}")
+    if precision == "f64":
+        assert dx.max() <= 1e-7
+    else:
+        assert np.quantile(dx, 0.99) <= 1e-4 and dx.max() <= 5e-3
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_island_over_launch_budget_is_flagged_and_stepped(precision):
+    """An island whose CTA parts exceed the co-resident budget (lowered to 1
+    here through STP_ISLAND_BUDGET) is not frozen: its envs step one by one
+    without the cross contacts, report overflow, and env_step writes their
+    obs / reward / done."""
+    import os
+    import subprocess
+    import sys
+    ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys, numpy as np, torch
+sys.path.insert(0, {ROOT!r})
+from paper_1810_05762_b200.sim import VecEnv
+sys.path.insert(0, {os.path.join(ROOT, "tests")!r})
+from scenes import chain_state
+g = VecEnv("hfh", n_envs=24, precision="{precision}", seed=41)
+st = chain_state(g.get_state(), g.model, [(0, 12)])
+g.set_state(st)
+a = torch.zeros((24, g.action_dim), device="cuda")
+obs = torch.full((24, g.obs_dim), float("nan"), device="cuda")
+rew = torch.full((24,), float("nan"), device="cuda")
+done = torch.full((24,), 7, dtype=torch.uint8, device="cuda")
+g.step(a, obs, rew, done)
+torch.cuda.synchronize()
+rep = g.report()
+assert rep["overflow"][:12].all() and not rep["overflow"][12:].any(), rep["overflow"]
+assert torch.isfinite(obs).all() and torch.isfinite(rew).all() and (done <= 1).all()
+assert not np.array_equal(g.get_state()[:12], st[:12])
+print("ok")
+"""
+    env = dict(os.environ, STP_ISLAND_BUDGET="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
