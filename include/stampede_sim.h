@@ -303,6 +303,19 @@ int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_dim, const 
                        int64_t env_offset, float* mean_out, float* action_out, float* logp_out,
                        float* value_out, void* stream);
 
+/* assemble_system (solver.hpp:41-44, solver.cpp:419-446) on the device path:
+ * the first Newton linearisation of env `env` for host torques [N*J] (N*m)
+ * exactly as the step kernel assembles it — H dense row-major [6S x 6S] over
+ * the S dynamic bodies in body order (AssembledSystem::body_to_slot), the
+ * reference's block-pointer aliasing applied to block (parent, child) when
+ * stp_step_config.reference_alias_quirk is set; rhs [6S] — and the Krylov
+ * iterations of each Newton iteration (krylov[newton_iters]).  The handle's
+ * state is left unchanged.  Envs without inter-agent coupling, handles with
+ * one env per warp (every handle below one wave of resident warps).  Any
+ * output may be NULL; n_slots receives S. */
+int stp_debug_first_system(stp_sim* sim, int32_t env, const double* torques, double* H, double* rhs,
+                           int32_t* krylov, int32_t* n_slots);
+
 /* --- diagnostics (tests only; not part of the reference interface) ---------
  * The fp32 step kernel's own elementary functions on device arrays, so their
  * accuracy is tested directly: fn 0 = sincos (Cody-Waite +

@@ -59,6 +59,8 @@ struct stp_sim {
   double* d_boxes = nullptr;
   int n_boxes = 0;
   void* d_scratch = nullptr;
+  void* d_dbg = nullptr;  // assemble_system hook capture (stp_debug_first_system)
+  int dbg_env = -1;
   // terrain broadphase grid
   int grid_nx = 0, grid_ny = 0;
   double grid_x0 = 0, grid_y0 = 0, grid_inv = 0;
@@ -351,6 +353,8 @@ stp::KArgs<T> make_args(stp_sim* s, int mode) {
   a.n_boxes = s->n_boxes;
   a.boxes = s->d_boxes;
   a.scratch = reinterpret_cast<T*>(s->d_scratch);
+  a.dbg = s->dbg_env >= 0 ? reinterpret_cast<T*>(s->d_dbg) : nullptr;
+  a.dbg_env = s->dbg_env;
   a.grid_nx = s->grid_nx;
   a.grid_ny = s->grid_ny;
   a.grid_x0 = s->grid_x0;
@@ -1088,6 +1092,98 @@ int stp_set_task_state(stp_sim* s, const double* target, const int32_t* counters
   }
   if (counters) CK(cudaMemcpyAsync(s->d_counters, counters, N * 8 * 4, cudaMemcpyHostToDevice, s->stream));
   CK(cudaStreamSynchronize(s->stream));
+  return STP_OK;
+}
+
+// assemble_system (solver.hpp:41-44, solver.cpp:419-446) on the device path:
+// the first Newton linearisation of env `env` as the step kernel builds it
+// (H over the dynamic bodies' slots, dense row-major [6S][6S], with the
+// reference's block-pointer aliasing applied to block (parent, child); rhs
+// [6S]) and the Krylov iterations of each Newton iteration.  The state is
+// restored afterwards; pending external loads apply (and are kept).
+int stp_debug_first_system(stp_sim* s, int32_t env, const double* torques, double* H, double* rhs,
+                           int32_t* krylov, int32_t* n_slots) {
+  const stp::DeviceGuard dg_(s ? s->device : 0);
+  if (!s || env < 0 || env >= s->n || (s->J > 0 && !torques))
+    return fail(STP_EINVAL, "stp_debug_first_system: bad arguments");
+  if (s->task.inter_agent_collisions) return fail(STP_EINVAL, "stp_debug_first_system: single-env islands only");
+  if (s->W != 32) return fail(STP_EINVAL, "stp_debug_first_system: handles with one env per warp only");
+  if (const int rc_ = join_caller(s)) return rc_;
+  const size_t N = size_t(s->n), ts = s->tsize, W = size_t(s->W), B = size_t(s->B);
+  const size_t dbg_elems = 32 * stp::kDbgStride + stp::kDbgNewton;
+  if (!s->d_dbg)
+    if (const int rc = dalloc(s, &s->d_dbg, dbg_elems * 8)) return rc;
+  // save what a physics step changes
+  void *st = nullptr, *org = nullptr, *ld = nullptr;
+  const size_t st_bytes = N * stp::kStateFields * W * ts, org_bytes = N * 2 * sizeof(double),
+               ld_bytes = N * 6 * W * ts;
+  CK(cudaMalloc(&st, st_bytes));
+  CK(cudaMalloc(&org, org_bytes));
+  CK(cudaMalloc(&ld, ld_bytes));
+  const bool loads = s->loads_pending;
+  CK(cudaMemcpyAsync(st, s->d_state, st_bytes, cudaMemcpyDeviceToDevice, s->stream));
+  CK(cudaMemcpyAsync(org, s->d_origin, org_bytes, cudaMemcpyDeviceToDevice, s->stream));
+  CK(cudaMemcpyAsync(ld, s->d_loads, ld_bytes, cudaMemcpyDeviceToDevice, s->stream));
+  CK(cudaMemsetAsync(s->d_dbg, 0, dbg_elems * ts, s->stream));
+  std::vector<float> t(N * s->J);
+  for (size_t i = 0; i < t.size(); ++i) t[i] = float(torques[i]);
+  if (!t.empty()) CK(cudaMemcpyAsync(s->d_act, t.data(), t.size() * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  s->dbg_env = env;
+  int rc = launch(s, 0, s->d_act, nullptr, nullptr, nullptr, nullptr, nullptr, s->stream);
+  s->dbg_env = -1;
+  std::vector<unsigned char> raw(dbg_elems * ts);
+  if (!rc) {
+    CK(cudaMemcpyAsync(raw.data(), s->d_dbg, raw.size(), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(s->d_state, st, st_bytes, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->d_origin, org, org_bytes, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->d_loads, ld, ld_bytes, cudaMemcpyDeviceToDevice, s->stream));
+    s->loads_pending = loads;
+  }
+  CK(cudaStreamSynchronize(s->stream));
+  cudaFree(st);
+  cudaFree(org);
+  cudaFree(ld);
+  if (rc) return rc;
+  auto val = [&](size_t i) -> double {
+    if (ts == 8) return reinterpret_cast<const double*>(raw.data())[i];
+    return double(reinterpret_cast<const float*>(raw.data())[i]);
+  };
+  // slots: dynamic bodies in body order (assemble_system's body_to_slot)
+  int slot[STP_MAX_BODIES];
+  int S = 0;
+  for (size_t b = 0; b < B; ++b) slot[b] = s->model.bodies[b].is_static ? -1 : S++;
+  const size_t n6 = size_t(6) * S;
+  if (n_slots) *n_slots = S;
+  auto sidx = [](int r, int c) { return r >= c ? r * (r + 1) / 2 + c : c * (c + 1) / 2 + r; };
+  if (H) std::fill(H, H + n6 * n6, 0.0);
+  for (size_t b = 0; b < B; ++b) {
+    if (slot[b] < 0) continue;
+    const size_t o = b * stp::kDbgStride, i0 = size_t(6) * slot[b];
+    if (H)
+      for (int r = 0; r < 6; ++r)
+        for (int c = 0; c < 6; ++c) H[(i0 + r) * n6 + i0 + c] = val(o + sidx(r, c));
+    if (rhs)
+      for (int r = 0; r < 6; ++r) rhs[i0 + r] = val(o + 21 + r);
+  }
+  for (int j = 0; H && j < s->J; ++j) {
+    const stp_joint& jd = s->model.joints[j];
+    const int c = jd.child, p = jd.parent;
+    if (slot[c] < 0 || slot[p] < 0) continue;
+    const size_t o = size_t(c) * stp::kDbgStride, ci = size_t(6) * slot[c], pi = size_t(6) * slot[p];
+    double hcp[36];
+    for (int k = 0; k < 36; ++k) hcp[k] = val(o + 27 + k);
+    const double d0 = val(o + 63);
+    const double ja0[6] = {-1, 0, 0, val(o + 64), val(o + 65), val(o + 66)};
+    const double jb0[6] = {1, 0, 0, val(o + 67), val(o + 68), val(o + 69)};
+    for (int r = 0; r < 6; ++r)
+      for (int k = 0; k < 6; ++k) {
+        H[(ci + r) * n6 + pi + k] = hcp[r * 6 + k];                             // H(child, parent)
+        H[(pi + k) * n6 + ci + r] = hcp[r * 6 + k] - d0 * ja0[k] * jb0[r];      // H(parent, child)
+      }
+  }
+  if (krylov)
+    for (int it = 0; it < s->cfg.newton_iters && it < stp::kDbgNewton; ++it)
+      krylov[it] = int32_t(val(32 * stp::kDbgStride + it));
   return STP_OK;
 }
 

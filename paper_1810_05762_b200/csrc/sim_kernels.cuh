@@ -100,7 +100,16 @@ struct KArgs {
   const int* big_members;     // member envs (unordered within an island)
   int* big_bar;               // [kBigIslands] barrier arrival counters (zeroed per step)
   T* big_xch;                 // [sum of sizes][kBigStride] exchange / reduction area
+  // assemble_system hook (stp_debug_first_system): env dbg_env writes its first
+  // Newton linearisation per lane [kDbgStride] and its Krylov count per Newton
+  T* dbg;
+  int dbg_env;
 };
+// per lane: H_bb (21, packed), rhs (6), H(child, parent) (36, row-major incl.
+// the active limit term), aliasing quirk d0, ja angular (3), jb angular (3);
+// then kDbgNewton Krylov counts at 32 * kDbgStride
+constexpr int kDbgStride = 21 + 6 + 36 + 7;
+constexpr int kDbgNewton = 64;
 // per-env entries of the big islands' global exchange area: 32 lanes x kXch,
 // 4 reduction partials, 1 vote
 constexpr int kXchEntries = 21;

@@ -433,7 +433,7 @@ __host__ __device__ constexpr int island_cap() {
 }
 constexpr int kXch = kXchEntries;  // per-lane exchange entries (Mi is the largest)
 
-template <class T, int W, int CPB, bool ISL = false>
+template <class T, int W, int CPB, bool ISL = false, bool DBG = false>
 __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
     k_env_step(const KArgs<T> a) {
   int e;
@@ -1415,6 +1415,26 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
         // arithmetic): z = M^-1 r = L^-T rhat, z.Az = rhat.Ahat rhat and
         // Ap.M^-1 Ap = |Ahat phat|^2.  Ahat has identity diagonal blocks, so
         // an iteration needs no diagonal product and no preconditioner solve.
+        if constexpr (DBG) {
+          if (it == 0 && e == a.dbg_env) {  // assemble_system hook (solver.hpp:41-44)
+            T* d = a.dbg + b * kDbgStride;
+#pragma unroll
+            for (int k = 0; k < 21; ++k) d[k] = H[k];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) d[21 + k] = rhs[k];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+#pragma unroll
+              for (int c = 0; c < 6; ++c)
+                d[27 + k * 6 + c] = !L.has_off ? T(0)
+                                                : L.at(R_HOFF + k * 6 + c) +
+                                                      (k >= 3 && c >= 3 ? L.lim_s * comp(L.lim_a, k - 3) *
+                                                                              comp(L.lim_a, c - 3)
+                                                                        : T(0));
+#pragma unroll
+            for (int k = 0; k < 7; ++k) d[63 + k] = L.quirk ? L.at(R_QRK + k) : T(0);
+          }
+        }
         T nz = T(0);
 #pragma unroll
         for (int k = 0; k < 21; ++k) nz = nf_acc(nz, H[k]);
@@ -1789,6 +1809,9 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
           u[i] = sum * L.at(R_SCAT + i);
         }
         krylov_total += kk;
+        if constexpr (DBG) {
+          if (e == a.dbg_env && b == 0 && it < kDbgNewton) a.dbg[32 * kDbgStride + it] = T(kk);
+        }
         T uz = T(0);
 #pragma unroll
         for (int k = 0; k < 6; ++k) uz = nf_acc(uz, u[k]);
@@ -2180,19 +2203,19 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
   }
 }
 
-template <class T, int W, int CPB>
+template <class T, int W, int CPB, bool DBG = false>
 static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
   constexpr int threads = kStepThreads;
   const size_t smem = size_t(threads / 32) * smem_rows<CPB>() * 32 * sizeof(T);
   static bool configured[64] = {};
   if (first_on_device(configured)) {
-    cudaError_t err = cudaFuncSetAttribute(k_env_step<T, W, CPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(smem));
+    cudaError_t err = cudaFuncSetAttribute(k_env_step<T, W, CPB, false, DBG>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (err != cudaSuccess) return err;
   }
   const long long total = (long long)(a.n - a.e_begin) * W;
   const int blocks = int((total + threads - 1) / threads);
-  k_env_step<T, W, CPB><<<blocks, threads, smem, s>>>(a);
+  k_env_step<T, W, CPB, false, DBG><<<blocks, threads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -2256,6 +2279,10 @@ int island_launch_budget(int cpb) {
 
 template <class T>
 cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s) {
+  if (a.dbg) {  // assemble_system hook: its own instantiation (no cost on the hot path)
+    if (lanes != 32 || a.merged) return cudaErrorInvalidValue;
+    return cpb <= 2 ? launch_one<T, 32, 2, true>(a, s) : launch_one<T, 32, 4, true>(a, s);
+  }
   if (a.merged) {  // inter-agent collisions: independent envs, then the merged islands
     if (lanes != 32) return cudaErrorInvalidValue;
     cudaError_t e = cpb <= 2 ? launch_one<T, 32, 2>(a, s) : launch_one<T, 32, 4>(a, s);

@@ -248,6 +248,19 @@ class VecEnv:
                "get_report")
         return dict(newton_iterations=newton, krylov_iterations=krylov, failed=failed, overflow=overflow)
 
+    def first_system(self, env: int, torques):
+        """assemble_system (solver.hpp:41-44) of env `env` as the CUDA step
+        builds it: (H [6S, 6S], rhs [6S], krylov iterations per Newton
+        iteration, S); the state is left unchanged."""
+        t = np.ascontiguousarray(torques, dtype=np.float64).reshape(self.n_envs, self.action_dim)
+        S = sum(1 for b in range(self.n_bodies) if not self.model.bodies[b].is_static)
+        H, rhs = np.zeros((6 * S, 6 * S)), np.zeros(6 * S)
+        kry = np.zeros(max(1, self.cfg.newton_iters), np.int32)
+        ns = np.zeros(1, np.int32)
+        _raise(self.lib.stp_debug_first_system(self._h, int(env), _ptr(t), _ptr(H), _ptr(rhs), _ptr(kry), _ptr(ns)),
+               "first_system")
+        return H, rhs, kry[:self.cfg.newton_iters], int(ns[0])
+
     def task_state(self):
         N, J = self.n_envs, self.action_dim
         target, counters, last = np.zeros((N, 2)), np.zeros((N, 8), np.int32), np.zeros((N, max(J, 1)))
