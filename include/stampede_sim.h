@@ -310,8 +310,7 @@ int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_dim, const 
  * reference's block-pointer aliasing applied to block (parent, child) when
  * stp_step_config.reference_alias_quirk is set; rhs [6S] — and the Krylov
  * iterations of each Newton iteration (krylov[newton_iters]).  The handle's
- * state is left unchanged.  Envs without inter-agent coupling, handles with
- * one env per warp (every handle below one wave of resident warps).  Any
+ * state is left unchanged.  Envs without inter-agent coupling only.  Any
  * output may be NULL; n_slots receives S. */
 int stp_debug_first_system(stp_sim* sim, int32_t env, const double* torques, double* H, double* rhs,
                            int32_t* krylov, int32_t* n_slots);

@@ -1107,7 +1107,6 @@ int stp_debug_first_system(stp_sim* s, int32_t env, const double* torques, doubl
   if (!s || env < 0 || env >= s->n || (s->J > 0 && !torques))
     return fail(STP_EINVAL, "stp_debug_first_system: bad arguments");
   if (s->task.inter_agent_collisions) return fail(STP_EINVAL, "stp_debug_first_system: single-env islands only");
-  if (s->W != 32) return fail(STP_EINVAL, "stp_debug_first_system: handles with one env per warp only");
   if (const int rc_ = join_caller(s)) return rc_;
   const size_t N = size_t(s->n), ts = s->tsize, W = size_t(s->W), B = size_t(s->B);
   const size_t dbg_elems = 32 * stp::kDbgStride + stp::kDbgNewton;

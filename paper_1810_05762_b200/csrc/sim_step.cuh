@@ -2279,9 +2279,11 @@ int island_launch_budget(int cpb) {
 
 template <class T>
 cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s) {
-  if (a.dbg) {  // assemble_system hook: its own instantiation (no cost on the hot path)
-    if (lanes != 32 || a.merged) return cudaErrorInvalidValue;
-    return cpb <= 2 ? launch_one<T, 32, 2, true>(a, s) : launch_one<T, 32, 4, true>(a, s);
+  if (a.dbg) {  // assemble_system hook: its own instantiations (no cost on the hot path)
+    if (a.merged) return cudaErrorInvalidValue;
+    if (lanes == 32) return cpb <= 2 ? launch_one<T, 32, 2, true>(a, s) : launch_one<T, 32, 4, true>(a, s);
+    if (lanes == 16) return cpb <= 2 ? launch_one<T, 16, 2, true>(a, s) : launch_one<T, 16, 4, true>(a, s);
+    return cpb <= 2 ? launch_one<T, 8, 2, true>(a, s) : launch_one<T, 8, 4, true>(a, s);
   }
   if (a.merged) {  // inter-agent collisions: independent envs, then the merged islands
     if (lanes != 32) return cudaErrorInvalidValue;
