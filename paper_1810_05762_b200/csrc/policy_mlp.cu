@@ -2,17 +2,27 @@
 //
 // SPEC.md:366-409 (SELU MLP, Gaussian policy), :446-454 (observation
 // whitening), Table 4 (Humanoid [256, 128, 64], Ant [128, 64, 32]).
-// One CTA = 128 environments = one M=128 tcgen05 tile:
-//   obs (fp32, HBM) -> whiten + clip(+-10) -> bf16 operand in smem
-//   -> 4 x tcgen05.mma (bf16 x bf16 -> fp32 accumulator in TMEM)
-//   -> tcgen05.ld epilogue: bias + SELU -> bf16 -> next layer's smem operand
+//
+// Swapped operands (the small-batch GEMM form): each layer computes
+// D^T = W X^T, so the hidden units run along the UMMA M = 128 dimension
+// (a 256-wide layer is two M blocks) and the environments along N.  A CTA owns
+// NT = 16 / 32 / 64 environments of one net (blockIdx.y: 0 policy, 1 value),
+// so a 4096-env forward is 128 CTAs on the 148 SMs instead of 64 CTAs of 128
+// envs, and every epilogue thread handles one hidden unit x 16 environments
+// (tcgen05.ld 32x32b: TMEM lane = hidden unit):
+//   obs tile (fp32, TMA bulk copy) -> whiten + clip(+-10) -> bf16 B operand
+//   -> per layer tcgen05.mma (W: bf16 K-major A operand from smem, X^T: bf16
+//      MN-major B operand, fp32 accumulator in TMEM)
+//   -> epilogue: bias + SELU -> bf16 -> the next layer's B operand (16-byte
+//      stores of 8 consecutive environments, conflict-free)
 //   -> last layer: mean (+ log_std, counter-based Gaussian sample, log-prob)
-// for the policy net, then the same chain for the value net.  Weights (packed
-// bf16, K-major 8x16B core-matrix layout) are staged into smem with TMA bulk
-// copies (cp.async.bulk) completing on an mbarrier; nets whose weights do not
-// fit next to the operands (e.g. the 241-wide terrain observation) stream each
-// layer's weights in contiguous K-block chunks through one buffer, every chunk
-// accumulating into the same TMEM accumulator.
+//      or value.
+// Weights (packed bf16 [K/8][N_out][8], the K-major core-matrix layout) are
+// staged into smem with TMA bulk copies (cp.async.bulk) completing on an
+// mbarrier; nets whose weights do not fit next to the operands (the 241-wide
+// terrain observation) stream each layer's weights in contiguous K-block
+// chunks through one buffer, every chunk accumulating into the same TMEM
+// accumulator.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -23,8 +33,9 @@
 
 namespace {
 
-constexpr int kM = 128;        // rows (envs) per CTA = UMMA M
-constexpr int kThreads = 512;  // 16 warps: warps w, w+4, w+8, w+12 share TMEM lanes 32(w%4).. (16-column chunks round-robin)
+constexpr int kM = 128;        // UMMA M: hidden units per M block (TMEM lanes)
+constexpr int kThreads = 512;  // 16 warps: warps w, w+4, w+8, w+12 share TMEM lanes 32(w%4).. (units round-robin)
+constexpr int kMaxNT = 64;     // environments per CTA (UMMA N)
 constexpr float kSeluL = 1.0507009873554805f, kSeluA = 1.6732632423543772f;
 
 struct MlpDims {
@@ -43,11 +54,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// UMMA shared-memory descriptor, SWIZZLE_NONE K-major canonical layout
-// (cute/arch/mma_sm100_desc.hpp SmemDescriptor): core matrix = 8 rows x 16 B
-// contiguous; LBO = byte stride between K-adjacent core matrices, SBO = byte
-// stride between 8-row groups.  Our packing [k/8][rows][8] gives SBO = 128 B
-// and LBO = rows * 16 B.
+// UMMA shared-memory descriptor, SWIZZLE_NONE canonical layouts
+// (cute/arch/mma_sm100_desc.hpp SmemDescriptor); core matrix = 8 x 16 B
+// contiguous.  K-major (weights, [k/8][m][8]): LBO = stride between
+// K-adjacent core matrices (m * 16 B), SBO = stride between 8-row groups
+// (128 B).  MN-major (activations X^T, [n/8][k][8 envs]): LBO = stride between
+// K-adjacent core matrices (128 B), SBO = stride between 8-environment groups
+// (k * 16 B) (checked on B200 against the torch reference, tests/test_gpu_policy.py).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= uint64_t((saddr >> 4) & 0x3fff);
@@ -58,13 +71,14 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// Instruction descriptor kind::f16: bf16 x bf16 -> f32, both K-major
-// (cute/arch/mma_sm100_desc.hpp InstrDescriptor).
+// Instruction descriptor kind::f16: bf16 x bf16 -> f32, A K-major, B
+// MN-major (cute/arch/mma_sm100_desc.hpp InstrDescriptor: b_major bit 16).
 __device__ __forceinline__ uint32_t umma_idesc(int m, int n) {
   uint32_t d = 0;
   d |= 1u << 4;                    // c_format = F32
   d |= 1u << 7;                    // a_format = BF16
   d |= 1u << 10;                   // b_format = BF16
+  d |= 1u << 16;                   // b_major = MN (environments contiguous)
   d |= uint32_t(n >> 3) << 17;     // n_dim
   d |= uint32_t(m >> 4) << 24;     // m_dim
   return d;
@@ -135,21 +149,21 @@ __device__ __forceinline__ float selu(float x) {
   return x > 0.f ? kSeluL * x : neg;
 }
 
-// Write 8 bf16 (16 B) of row `row`, K-chunk `kc` into a [k/8][128][8] operand.
-__device__ __forceinline__ int quarter_of(int warp) { return warp >> 2; }
 
-__device__ __forceinline__ void st_chunk(__nv_bfloat16* buf, int kc, int row, const float* x8) {
+// 8 bf16 = one 16-byte chunk of the MN-major operand X^T: row k (hidden unit
+// or observation column), environments n0..n0+7 (n0 % 8 == 0).
+__device__ __forceinline__ void st_xt(__nv_bfloat16* buf, int kpad, int k, int n0, const float* x8) {
   __nv_bfloat162 p[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(x8[2 * i], x8[2 * i + 1]);
-  *reinterpret_cast<uint4*>(buf + (size_t(kc) * kM + row) * 8) = *reinterpret_cast<uint4*>(p);
+  *reinterpret_cast<uint4*>(buf + (size_t(n0 >> 3) * kpad + k) * 8) = *reinterpret_cast<uint4*>(p);
 }
 
 // Experiment-only phase timestamps (tools/exp/k4_phases.py builds with
 // -DSTP_K4_PHASES): thread 0 of each CTA records %globaltimer at phase ends.
 #ifdef STP_K4_PHASES
 constexpr int kPhases = 16;
-__device__ unsigned long long g_k4_phase[512 * kPhases];
+__device__ unsigned long long g_k4_phase[1024 * kPhases];
 __device__ __forceinline__ void phase(int i) {
   if (threadIdx.x == 0) {
     unsigned long long t;
@@ -167,43 +181,61 @@ struct Smem {
   uint64_t bar_mma;    // layer accumulator ready
   uint64_t bar_chunk;  // streaming mode: a chunk's MMAs done (weight buffer free)
   uint32_t tmem;
-  float wmean[256];  // whitening: per-column mean and 1 / std of the observation
-  float winv[256];
+  alignas(16) float wmean[256];  // whitening: per-column mean and std (TMA bulk destinations: 16-byte aligned)
+  alignas(16) float winv[256];
+  uint64_t streams[kMaxNT];  // policy noise stream per environment of the tile
+  float sdv[256];            // exp(log_std) per action
+  alignas(16) float bias[4][256];  // the net's biases (TMA bulk copies, padded widths)
 };
-constexpr int kHeader = 3072;  // Smem, rounded to the operand alignment
+constexpr int kHeader = 8192;  // Smem, rounded to the operand alignment
 static_assert(sizeof(Smem) <= kHeader, "Smem header");
+constexpr int kTmemCols = 2 * kMaxNT;  // two M blocks x NT accumulator columns
 
-// One 4-layer net over the CTA's 128 rows; A operand of layer 0 already in abuf0.
-// Returns with the final accumulator (n[3] columns) in TMEM.
-__device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4], __nv_bfloat16* abuf0,
-                        __nv_bfloat16* abuf1, Smem* sh, uint32_t& wphase, uint32_t& mphase, int tid,
-                        bool stream) {
-  const int warp = tid >> 5;
-  const int row = (warp & 3) * 32 + (tid & 31);  // TMEM lane = tile row
-  const int quarter = quarter_of(warp);          // epilogue chunk phase (0..3)
-  // resident mode: the 4 weight blobs were issued by the caller
+// One 4-layer net over the CTA's NT environments; B operand of layer 0 already
+// in xb0.  Returns with the last layer's accumulator (rows = outputs) in TMEM.
+// bg(l) runs on every thread while layer l's MMAs execute (work that does
+// not depend on the net: the policy noise).
+template <class BG>
+__device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4], __nv_bfloat16* xb0,
+                        __nv_bfloat16* xb1, Smem* sh, uint32_t& wphase, uint32_t& mphase, int tid, bool stream,
+                        int NT, BG&& bg) {
+  const int warp = tid >> 5, lane = tid & 31;
+  const int sp = warp & 3;   // TMEM subpartition: lanes 32 sp ..
+  const int wq = warp >> 2;  // 0..3: unit phase within the subpartition
   if (!stream) {
     mbar_wait(&sh->bar_w, wphase);
     wphase ^= 1;
   }
   phase(3);
   uint32_t cphase = 0;  // streaming mode, issuing thread only
-  __nv_bfloat16* a_in = abuf0;
-  __nv_bfloat16* a_out = abuf1;
+  __nv_bfloat16* x_in = xb0;
+  __nv_bfloat16* x_out = xb1;
+  const uint32_t idesc = umma_idesc(kM, NT);
   for (int l = 0; l < 4; ++l) {
+    const int mblocks = (D.n[l] + kM - 1) / kM;
     fence_async_smem();  // generic-proxy operand writes -> visible to the tensor core
     __syncthreads();
     if (tid == 0) {
       tc_after_sync();
-      const uint32_t idesc = umma_idesc(kM, D.n[l]);
-      const uint32_t a0 = smem_u32(a_in), b0 = smem_u32(wsm[stream ? 0 : l]);
-      if (!stream) {
-        for (int ks = 0; ks < D.k[l] / 16; ++ks) {
-          // K step of 16 = two 8-element core-matrix columns
-          const uint64_t da = umma_desc(a0 + uint32_t(ks) * 2 * kM * 16, kM * 16, 128);
-          const uint64_t db = umma_desc(b0 + uint32_t(ks) * 2 * D.n[l] * 16, uint32_t(D.n[l]) * 16, 128);
-          mma_bf16(sh->tmem, da, db, idesc, ks > 0);
+      const uint32_t xa = smem_u32(x_in);
+      const uint32_t xsbo = uint32_t(D.k[l]) * 16;  // 8-environment group stride of X^T
+      const uint32_t wlbo = uint32_t(D.n[l]) * 16;  // K-group stride of W
+      auto issue = [&](uint32_t w0, int ks0, int nks, int kg0) {
+        // K steps [ks0, ks0 + nks) of 16 for every M block; kg0 = global K step
+        // of ks0.  The descriptors are linear in the start address (bits 0-13,
+        // address >> 4), so each step adds a constant
+        const uint64_t db0 = umma_desc(xa + uint32_t(kg0) * 256, 128, xsbo);
+        for (int mb = 0; mb < mblocks; ++mb) {
+          uint64_t da = umma_desc(w0 + uint32_t(mb) * kM * 16, wlbo, 128), db = db0;
+          for (int ks = 0; ks < nks; ++ks) {
+            mma_bf16(sh->tmem + uint32_t(mb * NT), da, db, idesc, kg0 + ks > 0);
+            da += uint64_t(2 * wlbo) >> 4;
+            db += 256 >> 4;
+          }
         }
+      };
+      if (!stream) {
+        issue(smem_u32(wsm[l]), 0, D.k[l] / 16, 0);
       } else {
         // K blocks [kb0, kb0 + nb) of the packed [k/8][n][8] weight are one
         // contiguous range: stage it, accumulate its MMAs, free the buffer
@@ -215,12 +247,7 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
           bulk_g2s(wsm[0], P.w[l] + size_t(kb0) * 8 * D.n[l], bytes, &sh->bar_w);
           mbar_wait(&sh->bar_w, wphase);
           wphase ^= 1;
-          for (int ks = 0; ks < nb / 2; ++ks) {
-            const int kg = kb0 / 2 + ks;  // global K step of 16
-            const uint64_t da = umma_desc(a0 + uint32_t(kg) * 2 * kM * 16, kM * 16, 128);
-            const uint64_t db = umma_desc(b0 + uint32_t(ks) * 2 * D.n[l] * 16, uint32_t(D.n[l]) * 16, 128);
-            mma_bf16(sh->tmem, da, db, idesc, kg > 0);
-          }
+          issue(smem_u32(wsm[0]), 0, nb / 2, kb0 / 2);
           if (kb0 + nb < kbt) {
             umma_commit(&sh->bar_chunk);
             mbar_wait(&sh->bar_chunk, cphase);
@@ -230,43 +257,39 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
       }
       umma_commit(&sh->bar_mma);
     }
+    bg(l);
     mbar_wait(&sh->bar_mma, mphase);
     mphase ^= 1;
     tc_after_sync();
     phase(4 + 2 * l);
     if (l == 3) break;
-    // epilogue: bias + SELU -> bf16 -> next operand (this thread's row, every
-    // 4th 16-column chunk)
-    const uint32_t tbase = sh->tmem + (uint32_t((warp & 3) * 32) << 16);
-    const int nch = D.n[l] / 16;
-    for (int j = quarter; j < nch; j += 4) {
-      // bias loads first: their latency overlaps the TMEM load's
-      const float4* b4 = reinterpret_cast<const float4*>(P.bias[l] + 16 * j);
-      float4 bq[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) bq[q] = __ldg(b4 + q);
+    // epilogue: units (M block, 16-environment chunk) of this subpartition
+    // round-robin over its 4 warps; lane = hidden unit h, 16 environments
+    const int nch = NT / 16, units = mblocks * nch;
+    const int kout = D.k[l + 1];  // = D.n[l] (padded width): K rows of the next operand
+    for (int u = wq; u < units; u += 4) {
+      const int mb = u / nch, ch = u - mb * nch;
+      const int h = mb * kM + sp * 32 + lane;
+      if (mb * kM + sp * 32 >= D.n[l]) continue;  // warp-uniform: no valid unit in this subpartition
+      const float bias = h < D.n[l] ? sh->bias[l][h] : 0.f;
       float v[16];
-      tmem_ld16(tbase + uint32_t(16 * j), v);
+      tmem_ld16(sh->tmem + (uint32_t(sp * 32) << 16) + uint32_t(mb * NT + ch * 16), v);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 b = bq[q];
-        v[4 * q] = selu(v[4 * q] + b.x);
-        v[4 * q + 1] = selu(v[4 * q + 1] + b.y);
-        v[4 * q + 2] = selu(v[4 * q + 2] + b.z);
-        v[4 * q + 3] = selu(v[4 * q + 3] + b.w);
+      for (int i = 0; i < 16; ++i) v[i] = selu(v[i] + bias);
+      if (h < kout) {
+        st_xt(x_out, kout, h, ch * 16, v);
+        st_xt(x_out, kout, h, ch * 16 + 8, v + 8);
       }
-      st_chunk(a_out, 2 * j, row, v);
-      st_chunk(a_out, 2 * j + 1, row, v + 8);
     }
     tc_before_sync();
     phase(5 + 2 * l);
-    __nv_bfloat16* t = a_in;
-    a_in = a_out;
-    a_out = t;
+    __nv_bfloat16* t = x_in;
+    x_in = x_out;
+    x_out = t;
   }
 }
 
-// K4 kernel: blockIdx.x = 128-env tile, blockIdx.y = net (0 policy, 1 value).
+// K4 kernel: blockIdx.x = NT-environment tile, blockIdx.y = net (0 policy, 1 value).
 __global__ void __launch_bounds__(kThreads, 1)
     k_policy_mlp(const float* __restrict__ obs, int n_envs, int obs_dim, const float* __restrict__ mean,
                  const float* __restrict__ stdv, const __grid_constant__ MlpDims Dpi,
@@ -274,22 +297,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const __grid_constant__ NetPtrs Pv,
                  const float* __restrict__ log_std, uint64_t seed, uint64_t step, long long env_offset,
                  float* __restrict__ mu_out, float* __restrict__ act_out, float* __restrict__ logp_out,
-                 float* __restrict__ v_out, int a0_elems, int a1_elems, int wbuf_elems) {
+                 float* __restrict__ v_out, int x0_elems, int x1_elems, int wbuf_elems, int NT, int eps_elems) {
   extern __shared__ __align__(1024) unsigned char smem[];
   Smem* sh = reinterpret_cast<Smem*>(smem);
   phase(0);
-  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(smem + kHeader);
-  // operand ping-pong: abuf0 holds layer 0/2 inputs, abuf1 layer 1/3 inputs
-  __nv_bfloat16* abuf0 = base;
-  __nv_bfloat16* abuf1 = base + a0_elems;
-  __nv_bfloat16* wbase = base + a0_elems + a1_elems;
+  float* eps = reinterpret_cast<float*>(smem + kHeader);  // policy noise [env][out]
+  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(smem + kHeader + size_t(eps_elems) * 4);
+  // operand ping-pong: xb0 holds layer 0/2 inputs, xb1 layer 1/3 inputs
+  __nv_bfloat16* xb0 = base;
+  __nv_bfloat16* xb1 = base + x0_elems;
+  __nv_bfloat16* wbase = base + x0_elems + x1_elems;
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
+  const int warp = tid >> 5, lane = tid & 31;
   const bool value_net = blockIdx.y == 1;
   const MlpDims& D = value_net ? Dv : Dpi;
   const NetPtrs& P = value_net ? Pv : Ppi;
-  const int lrow = (warp & 3) * 32 + (tid & 31);  // TMEM lane / tile row of this thread
-  const int row = blockIdx.x * kM + lrow;
 
   __nv_bfloat16* wsm[4];
   int off = 0;
@@ -297,20 +319,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     wsm[l] = wbase + off;
     off += D.k[l] * D.n[l];
   }
-  // whitened, clipped observation rows -> bf16 operand (RunningStat,
-  // SPEC.md:446-454).  The tile's rows are one contiguous block of global
-  // memory staged into the (still unused) layer-1 operand buffer: by one TMA
-  // bulk copy when its size and address allow (issued first, then the 4 weight
-  // blobs, all completing on mbarriers while the CTA waits for the first),
-  // else by coalesced loads in row passes that fit the buffer.  Each
-  // (row, 8-column chunk) is then whitened and written as one 16-byte chunk.
-  float* stage = reinterpret_cast<float*>(abuf1);
-  const int tile0 = blockIdx.x * kM;
-  const int rows = min(kM, n_envs - tile0);
+  // The tile's observation rows are one contiguous block of global memory,
+  // staged into the (still unused) layer-1 operand buffer by one TMA bulk copy
+  // when its size and address allow (issued first, then the 4 weight blobs, all
+  // completing on mbarriers), else by coalesced loads.
+  float* stage = reinterpret_cast<float*>(xb1);
+  const int tile0 = blockIdx.x * NT;
+  const int rows = min(NT, n_envs - tile0);
   const float* src = obs + size_t(tile0) * obs_dim;
   const uint32_t tile_bytes = uint32_t(rows) * uint32_t(obs_dim) * 4u;
-  const bool tma_obs = (tile_bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
-                       tile_bytes <= uint32_t(a1_elems) * 2u;
+  const bool tma_obs = (tile_bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  // the whitening statistics by TMA too when they are 16-byte multiples
+  const uint32_t stat_bytes = uint32_t(obs_dim) * 4u;
+  const bool tma_stat = tma_obs && (stat_bytes & 15) == 0 &&
+                        ((reinterpret_cast<uintptr_t>(mean) | reinterpret_cast<uintptr_t>(stdv)) & 15) == 0;
   const bool stream = wbuf_elems > 0;
   if (tid == 0) {
     mbar_init(&sh->bar_obs, 1);
@@ -318,9 +340,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&sh->bar_mma, 1);
     mbar_init(&sh->bar_chunk, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    // biases (16-byte multiples: padded to 16 outputs) always by TMA on bar_obs
+    uint32_t bias_bytes = 0;
+    for (int l = 0; l < 4; ++l) bias_bytes += uint32_t(D.n[l]) * 4;
+    mbar_expect_tx(&sh->bar_obs, bias_bytes + (tma_obs ? tile_bytes : 0) + (tma_stat ? 2 * stat_bytes : 0));
+    for (int l = 0; l < 4; ++l) bulk_g2s(sh->bias[l], P.bias[l], uint32_t(D.n[l]) * 4, &sh->bar_obs);
     if (tma_obs) {
-      mbar_expect_tx(&sh->bar_obs, tile_bytes);
       bulk_g2s(stage, src, tile_bytes, &sh->bar_obs);
+      if (tma_stat) {
+        bulk_g2s(sh->wmean, mean, stat_bytes, &sh->bar_obs);
+        bulk_g2s(sh->winv, stdv, stat_bytes, &sh->bar_obs);  // the standard deviations themselves
+      }
     }
     if (!stream) {
       uint32_t bytes = 0;
@@ -329,128 +359,130 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int l = 0; l < 4; ++l) bulk_g2s(wsm[l], P.w[l], uint32_t(D.k[l]) * D.n[l] * 2, &sh->bar_w);
     }
   }
-  if (warp == 0) {  // TMEM: 256 columns (max layer width)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&sh->tmem)));
+  if (warp == 0) {  // TMEM: two M blocks x NT columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&sh->tmem)),
+                 "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
-  for (int c = tid; c < obs_dim; c += kThreads) {
-    sh->wmean[c] = __ldg(mean + c);
-    sh->winv[c] = 1.f / __ldg(stdv + c);
+  if (!tma_stat)
+    for (int c = tid; c < obs_dim; c += kThreads) {
+      sh->wmean[c] = __ldg(mean + c);
+      sh->winv[c] = __ldg(stdv + c);
+    }
+  if (!value_net && act_out) {
+    for (int r = tid; r < rows; r += kThreads)
+      sh->streams[r] = stp_derive_seed(seed, 6 /* policy noise */, (uint64_t(env_offset + tile0 + r) << 32) |
+                                                                       uint32_t(step));
+  }
+  if (!tma_obs) {
+    const int nf = rows * obs_dim;
+    for (int i = tid; i < nf; i += kThreads) stage[i] = __ldg(src + i);
   }
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
   phase(1);
-
+  // whitened, clipped observations (RunningStat) -> X^T:
+  // one (observation column k, 8-environment group) chunk per thread and pass
   {
-    const int pass_rows = tma_obs ? kM : min(kM, (a1_elems * 2) / (obs_dim * 4));
-    const int kchunks = D.k[0] / 8;
-    if (tma_obs) mbar_wait(&sh->bar_obs, 0);
+    mbar_wait(&sh->bar_obs, 0);
+    for (int c = tid; c < obs_dim; c += kThreads) sh->winv[c] = 1.f / sh->winv[c];
+    __syncthreads();
     phase(11);
-    for (int p0 = 0; p0 < kM; p0 += pass_rows) {
-      const int pr = max(0, min(pass_rows, rows - p0));
-      if (!tma_obs) {
-        const int nf = pr * obs_dim;
-        const float* s0 = src + size_t(p0) * obs_dim;
-        const int nf4 = (reinterpret_cast<uintptr_t>(s0) & 15) == 0 ? nf / 4 : 0;  // float4 path when aligned
-#pragma unroll 4
-        for (int i = tid; i < nf4; i += kThreads)
-          reinterpret_cast<float4*>(stage)[i] = __ldg(reinterpret_cast<const float4*>(s0) + i);
-        for (int i = nf4 * 4 + tid; i < nf; i += kThreads) stage[i] = __ldg(s0 + i);
-        __syncthreads();
-      }
-      const float* st = stage + (tma_obs ? size_t(p0) * obs_dim : 0);
-      const int prow = min(pass_rows, kM - p0);
-      for (int u = tid; u < prow * kchunks; u += kThreads) {
-        const int r = u % prow, kc = u / prow;
-        float x8[8];
+    const int kpad = D.k[0], ngr = NT / 8;
+    for (int u = tid; u < kpad * ngr; u += kThreads) {
+      const int k = u % kpad, g = u / kpad;
+      float x8[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int c = kc * 8 + i;
-          float x = 0.f;
-          if (r < pr && c < obs_dim) {
-            x = (st[r * obs_dim + c] - sh->wmean[c]) * sh->winv[c];
-            x = fminf(fmaxf(x, -10.f), 10.f);
-          }
-          x8[i] = x;
+      for (int i = 0; i < 8; ++i) {
+        const int r = g * 8 + i;
+        float x = 0.f;
+        if (r < rows && k < obs_dim) {
+          x = (stage[r * obs_dim + k] - sh->wmean[k]) * sh->winv[k];
+          x = fminf(fmaxf(x, -10.f), 10.f);
         }
-        st_chunk(abuf0, kc, p0 + r, x8);
+        x8[i] = x;
       }
-      __syncthreads();
+      st_xt(xb0, kpad, k, g * 8, x8);
     }
   }
   phase(2);
   uint32_t wphase = 0, mphase = 0;
-  run_net(D, P, wsm, abuf0, abuf1, sh, wphase, mphase, tid, stream);
-  const uint32_t tbase = sh->tmem + (uint32_t((warp & 3) * 32) << 16);
-  if (!value_net) {
-    // policy head in row passes through shared memory (the
-    // operand buffers are free once the last MMA completed): TMEM -> mean
-    // tile [rows][out]; then every thread takes consecutive tile elements, so
-    // the mean / action stores are coalesced; the log-prob terms replace the
-    // means in place and each row is summed in column order by one thread.
-    // Per pass the buffer holds the tile, the rows' noise streams and the
-    // columns' standard deviations.
-    const int out = D.out;
-    const int bytes = (a0_elems + a1_elems) * 2 - out * 4 - 8;
-    const int cap = min(kM, bytes / (out * 4 + 8));
-    float* tile = reinterpret_cast<float*>(abuf0);
-    uint64_t* streams = reinterpret_cast<uint64_t*>(abuf0) + (cap * out + 1) / 2;
-    float* sdv = reinterpret_cast<float*>(streams + cap);
-    const int nch = D.n[3] / 16;
-    if (act_out && tid < out) sdv[tid] = expf(log_std[tid]);
-    for (int p0 = 0; p0 < rows; p0 += cap) {
-      const int pr = min(cap, rows - p0);
-      const bool mine = lrow >= p0 && lrow < p0 + pr;
-      if (act_out && mine && quarter_of(warp) == 0) {
-        const uint64_t genv = uint64_t(env_offset + row);
-        streams[lrow - p0] = stp_derive_seed(seed, 6 /* policy noise */, (genv << 32) | uint32_t(step));
-      }
-      for (int j = quarter_of(warp); j < nch; j += 4) {
-        float v[16];
-        tmem_ld16(tbase + uint32_t(16 * j), v);
-        if (mine)
-          for (int i = 0; i < 16; ++i) {
-            const int c = 16 * j + i;
-            if (c < out) tile[(lrow - p0) * out + c] = v[i] + P.bias[3][c];
-          }
-      }
-      __syncthreads();
-      const size_t g0 = (size_t(tile0) + p0) * out;
-      for (int i = tid; i < pr * out; i += kThreads) {
-        const int r = i / out, c = i - r * out;
-        const float m = tile[i];
-        mu_out[g0 + i] = m;
-        if (act_out) {
-          // Box-Muller on two 24-bit counter-based uniforms
-          const uint64_t ns = streams[r];
-          const float u1 = fmaxf(stp_uniformf(ns, 2 * c), 1e-7f), u2 = stp_uniformf(ns, 2 * c + 1);
-          const float eps = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
-          const float sd = sdv[c];
-          act_out[g0 + i] = m + sd * eps;
-          tile[i] = -0.5f * eps * eps - log_std[c] - 0.91893853320467274f;
-        }
-      }
-      __syncthreads();
-      if (logp_out && tid < pr) {
-        float lp = 0.f;
-        if (act_out)
-          for (int c = 0; c < out; ++c) lp += tile[tid * out + c];
-        logp_out[tile0 + p0 + tid] = lp;
-      }
-      __syncthreads();
+  // policy noise (Box-Muller on two 24-bit counter-based uniforms per element,
+  // fast log / cos: |err| ~1e-6) in four slices, drawn while the four layers'
+  // MMAs run
+  const bool draw = !value_net && act_out;
+  const int n_eps = draw ? rows * D.out : 0;
+  auto noise = [&](int l) {
+    if (l == 0 && draw)  // exp(log_std) (a global load: off the prologue's critical path)
+      for (int c = tid; c < D.out; c += kThreads) sh->sdv[c] = expf(log_std[c]);
+    const int e0 = n_eps * l / 4, e1 = n_eps * (l + 1) / 4;
+    for (int i = e0 + tid; i < e1; i += kThreads) {
+      const int r = i / D.out, c = i - r * D.out;
+      // one 64-bit hash per element: two 24-bit uniforms (bits 40-63, 16-39)
+      const uint64_t z = stp_mix64(sh->streams[r] + uint64_t(c));
+      const float u1 = fmaxf(float(z >> 40) * (1.f / 16777216.f), 1e-7f);
+      const float u2 = float((z >> 16) & 0xffffffu) * (1.f / 16777216.f);
+      eps[i] = sqrtf(-2.f * __logf(u1)) * __cosf(6.2831853071795865f * u2);
     }
-  } else if (warp < 4) {
+  };
+  run_net(D, P, wsm, xb0, xb1, sh, wphase, mphase, tid, stream, NT, noise);
+  // last layer: TMEM lane = output, columns = environments
+  const int sp = warp & 3, wq = warp >> 2, nch = NT / 16;
+  if (!value_net) {
+    // policy head: the mean tile [env][out] through shared
+    // memory (the operand buffers are free once the last MMA completed), then
+    // every thread takes consecutive tile elements, so the mean / action
+    // stores are coalesced; the log-prob terms replace the means in place and
+    // each environment's row is summed in column order by one thread
+    const int out = D.out;
+    float* tile = reinterpret_cast<float*>(base);
+    for (int u = wq; u < nch * ((out + 31) / 32); u += 4) {
+      const int ch = u % nch, blk = u / nch;
+      if (blk != sp) continue;  // outputs 32 sp .. of M block 0 live in subpartition sp
+      float v[16];
+      tmem_ld16(sh->tmem + (uint32_t(sp * 32) << 16) + uint32_t(ch * 16), v);
+      const int c = sp * 32 + lane;
+      if (c < out) {
+        const float bias = sh->bias[3][c];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) tile[(ch * 16 + i) * out + c] = v[i] + bias;
+      }
+    }
+    __syncthreads();
+    const size_t g0 = size_t(tile0) * out;
+    for (int i = tid; i < rows * out; i += kThreads) {
+      const int r = i / out, c = i - r * out;
+      const float m = tile[i];
+      mu_out[g0 + i] = m;
+      if (act_out) {
+        const float ep = eps[i];  // drawn during the MMAs (same [env][out] indexing)
+        act_out[g0 + i] = m + sh->sdv[c] * ep;
+        tile[i] = -0.5f * ep * ep - log_std[c] - 0.91893853320467274f;
+      }
+    }
+    __syncthreads();
+    if (logp_out && tid < rows) {
+      float lp = 0.f;
+      if (act_out)
+        for (int c = 0; c < out; ++c) lp += tile[tid * out + c];
+      logp_out[tile0 + tid] = lp;
+    }
+  } else if (sp == 0 && wq < nch) {
     float v[16];
-    tmem_ld16(tbase, v);
-    if (row < n_envs) v_out[row] = v[0] + P.bias[3][0];
+    tmem_ld16(sh->tmem + uint32_t(wq * 16), v);
+    if (lane == 0) {
+      const float bias = sh->bias[3][0];
+      for (int i = 0; i < 16; ++i)
+        if (wq * 16 + i < rows) v_out[tile0 + wq * 16 + i] = v[i] + bias;
+    }
   }
   tc_before_sync();
   __syncthreads();
   phase(12);
   if (warp == 0) {
     tc_after_sync();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(sh->tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(sh->tmem), "n"(kTmemCols));
   }
 }
 
@@ -516,21 +548,31 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
   };
   const int wmax = value_out ? (welems(Dpi) > welems(Dv) ? welems(Dpi) : welems(Dv)) : welems(Dpi);
   auto mx = [](int a, int b) { return a > b ? a : b; };
+  if (Dpi.out > kM) return stp::fail(STP_EINVAL, "stp_policy_forward: at most 128 actions");
+  // environments per CTA (UMMA N): the largest of 64 / 32 / 16 that still
+  // gives ~one CTA per SM over both nets
+  const int nets = value_out ? 2 : 1;
+  const int NT = (n_envs + 63) / 64 * nets >= 120 ? 64 : (n_envs + 31) / 32 * nets >= 120 ? 32 : 16;
   int c0 = mx(Dpi.k[0], Dpi.k[2]), c1 = mx(Dpi.k[1], Dpi.k[3]);
   if (value_out) {
     c0 = mx(c0, mx(Dv.k[0], Dv.k[2]));
     c1 = mx(c1, mx(Dv.k[1], Dv.k[3]));
   }
-  const int a0 = kM * c0, a1 = kM * c1;
+  const int x0 = NT * c0;
+  const int x1 = mx(NT * c1, (NT * obs_dim * 4 + 1) / 2);  // X^T operands; x1 also stages the fp32 obs tile
   const size_t kSmemMax = 227 * 1024;
-  const size_t base = kHeader + size_t(a0 + a1) * 2;
-  size_t smem = base + size_t(wmax) * 2;
+  // + one M block of K-major rows (2 KB): a layer narrower than 128 outputs is
+  // read as a full M = 128 block, the extra rows' results are never used
+  const size_t kOverRead = size_t(kM) * 16;
+  const int eps_elems = action_out ? ((NT * Dpi.out + 3) / 4 * 4) : 0;  // noise tile, 16-byte multiple
+  const size_t base = kHeader + size_t(eps_elems) * 4 + size_t(x0 + x1) * 2;
+  size_t smem = base + size_t(wmax) * 2 + kOverRead;
   int wbuf = 0;  // 0: all weights resident
   for (MlpDims* D : {&Dpi, &Dv})
     for (int l = 0; l < 4; ++l) D->kb_chunk[l] = D->k[l] / 8;
   if (smem > kSmemMax) {
     // stream: one weight buffer filling the rest of shared memory
-    wbuf = int((kSmemMax - base) / 2) / 128 * 128;
+    wbuf = int((kSmemMax - base - kOverRead) / 2) / 128 * 128;
     for (MlpDims* D : {&Dpi, &Dv}) {
       if (D == &Dv && !value_out) continue;
       for (int l = 0; l < 4; ++l) {
@@ -539,7 +581,7 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
           return stp::fail(STP_EINVAL, "stp_policy_forward: network too large for shared memory");
       }
     }
-    smem = base + size_t(wbuf) * 2;
+    smem = base + size_t(wbuf) * 2 + kOverRead;
   }
   static size_t configured[64] = {};  // per device (the attribute is)
   int dev = 0;
@@ -549,10 +591,10 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
     if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_policy_mlp attr: ") + cudaGetErrorString(e));
     if (dev >= 0 && dev < 64) configured[dev] = smem;
   }
-  const dim3 grid((n_envs + kM - 1) / kM, value_out ? 2 : 1);
+  const dim3 grid((n_envs + NT - 1) / NT, nets);
   k_policy_mlp<<<grid, kThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
       obs, n_envs, obs_dim, obs_mean, obs_std, Dpi, Ppi, Dv, Pv, log_std, seed, step, env_offset, mean_out,
-      action_out, logp_out, value_out, a0, a1, wbuf);
+      action_out, logp_out, value_out, x0, x1, wbuf, NT, eps_elems);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_policy_mlp: ") + cudaGetErrorString(e));
   return STP_OK;

@@ -181,8 +181,9 @@ def kernel_noise(seed: int, env: int, step: int, act_dim: int) -> np.ndarray:
     s = _mix64(_mix64(_mix64(seed) ^ 6) ^ ((env << 32) | (step & 0xFFFFFFFF)))
     out = np.zeros(act_dim, np.float32)
     for c in range(act_dim):
-        u1 = np.float32((_mix64((s + 2 * c) & 0xFFFFFFFFFFFFFFFF) >> 40) * (1.0 / 16777216.0))
-        u2 = np.float32((_mix64((s + 2 * c + 1) & 0xFFFFFFFFFFFFFFFF) >> 40) * (1.0 / 16777216.0))
+        z = _mix64((s + c) & 0xFFFFFFFFFFFFFFFF)  # one hash per element: bits 40-63 and 16-39
+        u1 = np.float32((z >> 40) * (1.0 / 16777216.0))
+        u2 = np.float32(((z >> 16) & 0xFFFFFF) * (1.0 / 16777216.0))
         u1 = max(u1, np.float32(1e-7))
         out[c] = math.sqrt(-2.0 * math.log(u1)) * math.cos(2 * math.pi * u2)
     return out

@@ -62,7 +62,8 @@ def run():
     torch.cuda.synchronize()
     kern.forward(obs, m_, s_, step=99)
     torch.cuda.synchronize()
-    ctas = 2 * ((n + 127) // 128)
+    nt = 64 if (n + 63) // 64 * 2 >= 120 else 32 if (n + 31) // 32 * 2 >= 120 else 16  # stp_policy_forward's NT
+    ctas = 2 * ((n + nt - 1) // nt)
     buf = np.zeros(ctas * 16, dtype=np.uint64)
     lib.stp_k4_phases(buf.ctypes.data, buf.size)
     t = buf.reshape(ctas, 16).astype(np.int64)
