@@ -408,9 +408,11 @@ def run_ours(args, world, rank, local):
                 pst.merge_allreduce(loc)
             else:
                 pst._merge(loc.n, loc.mean, loc.m2)
-            adv, ret = gae(data["rew"], data["val"], data["done"], last_val, pcfg.gamma, pcfg.lam)
+            ast = torch.zeros(3, dtype=torch.float64, device=dev)
+            adv, ret = gae(data["rew"], data["val"], data["done"], last_val, pcfg.gamma, pcfg.lam, stats=ast)
             stats = learner.update(pst.whiten(data["obs"].reshape(-1, env.obs_dim)),
-                                   data["act"].reshape(-1, env.action_dim), None, adv.reshape(-1), ret.reshape(-1))
+                                   data["act"].reshape(-1, env.action_dim), None, adv.reshape(-1), ret.reshape(-1),
+                                   adv_stats=ast)
             pkern.refresh()
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)

@@ -303,6 +303,17 @@ int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_dim, const 
                        int64_t env_offset, float* mean_out, float* action_out, float* logp_out,
                        float* value_out, void* stream);
 
+/* --- PPO learner data path (config C5) ----------------
+ * compute_gae over the rollout buffer, all device pointers
+ * of [T][N] (time-major) fp32 rewards / values, uint8 dones, fp32 bootstrap
+ * values [N]:  delta_t = r_t + gamma V_{t+1} (1 - done_t) - V_t,
+ * A_t = delta_t + gamma lambda (1 - done_t) A_{t+1}, returns = A + V.
+ * stats (device double[3], may be NULL) accumulates count, sum(A), sum(A^2)
+ * for the (global) advantage normalisation; the caller
+ * zeroes it.  Asynchronous on `stream`. */
+int stp_gae(const float* rewards, const float* values, const uint8_t* dones, const float* last_value, int32_t T,
+            int32_t N, float gamma, float lam, float* advantages, float* returns, double* stats, void* stream);
+
 /* assemble_system (solver.hpp:41-44, solver.cpp:419-446) on the device path:
  * the first Newton linearisation of env `env` for host torques [N*J] (N*m)
  * exactly as the step kernel assembles it — H dense row-major [6S x 6S] over

@@ -1,5 +1,6 @@
-// Auxiliary device kernels of the C-ABI: bench random actions and the
-// fp32 math self-test (compiled with the fp32 step kernel's flags, build.py).
+// Auxiliary device kernels of the C-ABI: bench random actions, the PPO
+// learner's GAE and the fp32 math self-test (compiled with the fp32 step
+// kernel's flags, build.py; GAE uses no division / sqrt).
 #include <cuda_runtime.h>
 
 #include "stampede_sim.h"
@@ -36,7 +37,74 @@ __global__ void k_debug_math(int fn, const float* x, const float* y, float* o0, 
   o1[i] = c;
 }
 
+// compute_gae for the PPO learner's rollout buffer [T][N]:
+// one thread per environment runs the backward recursion
+//   delta_t = r_t + gamma V_{t+1} (1 - done_t) - V_t
+//   A_t = delta_t + gamma lambda (1 - done_t) A_{t+1},  R_t = A_t + V_t
+// (V_T = the bootstrap value), in fp32 like the learner; each block adds its
+// advantages' count, sum and sum of squares (double) to stats[3] for the
+// global advantage normalisation, so no host round trip.
+__global__ void k_gae(const float* __restrict__ rew, const float* __restrict__ val, const uint8_t* __restrict__ done,
+                      const float* __restrict__ last_val, int T, int N, float gamma, float lam, float* __restrict__ adv,
+                      float* __restrict__ ret, double* __restrict__ stats) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  double s = 0.0, sq = 0.0;
+  if (e < N) {
+    float next_v = last_val[e], a = 0.f;
+    for (int t = T - 1; t >= 0; --t) {
+      const size_t i = size_t(t) * N + e;
+      const float nonterm = done[i] ? 0.f : 1.f;
+      const float v = val[i];
+      const float delta = rew[i] + gamma * next_v * nonterm - v;
+      a = delta + gamma * lam * nonterm * a;
+      adv[i] = a;
+      ret[i] = a + v;
+      s += double(a);
+      sq += double(a) * double(a);
+      next_v = v;
+    }
+  }
+  if (stats) {
+    for (int off = 16; off > 0; off >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, off);
+      sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    }
+    __shared__ double ws[2][32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+      ws[0][w] = s;
+      ws[1][w] = sq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bs = 0.0, bq = 0.0;
+      for (int k = 0; k < int(blockDim.x >> 5); ++k) {
+        bs += ws[0][k];
+        bq += ws[1][k];
+      }
+      const int n_here = min(int(blockDim.x), N - int(blockIdx.x * blockDim.x));
+      atomicAdd(stats, double(n_here) * T);
+      atomicAdd(stats + 1, bs);
+      atomicAdd(stats + 2, bq);
+    }
+  }
+}
+
 }  // namespace
+
+extern "C" int stp_gae(const float* rewards, const float* values, const uint8_t* dones, const float* last_value,
+                       int32_t T, int32_t N, float gamma, float lam, float* advantages, float* returns,
+                       double* stats, void* stream) {
+  if (T < 0 || N < 0 || (T > 0 && N > 0 && (!rewards || !values || !dones || !last_value || !advantages || !returns)))
+    return stp::fail(STP_EINVAL, "stp_gae: bad arguments");
+  if (T == 0 || N == 0) return STP_OK;
+  const int threads = 256;
+  k_gae<<<(N + threads - 1) / threads, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      rewards, values, dones, last_value, T, N, gamma, lam, advantages, returns, stats);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_gae: ") + cudaGetErrorString(e));
+  return STP_OK;
+}
 
 extern "C" int stp_debug_math(int32_t fn, const float* x, const float* y, float* out0, float* out1, int64_t n,
                               void* stream) {

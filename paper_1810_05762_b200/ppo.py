@@ -59,10 +59,14 @@ def allreduce_mean_grads(model: torch.nn.Module):
         off += n
 
 
-def global_normalize(adv: torch.Tensor) -> torch.Tensor:
-    """Advantage normalisation with statistics over all ranks."""
-    s = torch.stack([torch.tensor(float(adv.numel()), device=adv.device, dtype=torch.float64),
-                     adv.double().sum(), (adv.double() ** 2).sum()])
+def global_normalize(adv: torch.Tensor, stats: torch.Tensor | None = None) -> torch.Tensor:
+    """Advantage normalisation with statistics over all ranks.
+    `stats` = [count, sum, sum of squares] (float64, e.g. from the GAE kernel);
+    computed here when absent.  One SUM allreduce, no host synchronisation."""
+    if stats is None:
+        stats = torch.stack([torch.tensor(float(adv.numel()), device=adv.device, dtype=torch.float64),
+                             adv.double().sum(), (adv.double() ** 2).sum()])
+    s = stats.to(torch.float64).clone()
     if _dist():
         dist.all_reduce(s, op=dist.ReduceOp.SUM)
     n, sm, sq = s[0], s[1], s[2]
@@ -71,9 +75,30 @@ def global_normalize(adv: torch.Tensor) -> torch.Tensor:
     return ((adv.double() - mean) / std).to(adv.dtype)
 
 
-def gae(rewards, values, dones, last_value, gamma, lam):
-    """Generalised advantage estimation over [T, N] tensors."""
+def gae(rewards, values, dones, last_value, gamma, lam, stats: torch.Tensor | None = None):
+    """Generalised advantage estimation over [T, N] tensors.
+
+    CUDA tensors run the product kernel (stp_gae: one thread per env, the
+    backward recursion, the advantages' count / sum / sum of squares added into
+    `stats` for the normalisation); host tensors (the gloo tests of the
+    distributed logic) run the same recursion vectorised over the envs."""
     T = rewards.shape[0]
+    if rewards.is_cuda:
+        import ctypes as C
+        from . import abi
+        N = rewards.shape[1] if rewards.dim() > 1 else 1
+        r = rewards.to(torch.float32).contiguous()
+        v = values.to(torch.float32).contiguous()
+        d = dones.to(torch.uint8).contiguous()
+        lv = last_value.to(torch.float32).contiguous()
+        adv, ret = torch.empty_like(r), torch.empty_like(r)
+        p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+        h = torch.cuda.current_stream(r.device).cuda_stream
+        rc = abi.load().stp_gae(p(r), p(v), p(d), p(lv), T, N, C.c_float(gamma), C.c_float(lam), p(adv), p(ret),
+                                p(stats), C.c_void_p(h if h else 1))
+        if rc != abi.STP_OK:
+            raise RuntimeError(f"stp_gae failed ({rc}): {abi.last_error()}")
+        return adv.to(rewards.dtype), ret.to(rewards.dtype)
     adv = torch.zeros_like(rewards)
     last = torch.zeros_like(rewards[0])
     for t in reversed(range(T)):
@@ -88,10 +113,14 @@ def gae(rewards, values, dones, last_value, gamma, lam):
 class PPOLearner:
     def __init__(self, model: ActorCritic, cfg: PPOConfig):
         self.model, self.cfg = model, cfg
-        self.opt = torch.optim.Adam(model.parameters(), lr=cfg.lr)
+        # one fused multi-tensor Adam kernel per step on the GPU (SPEC.md:488-496:
+        # beta 0.9 / 0.999, eps 1e-8, bias correction)
+        cuda = next(model.parameters()).is_cuda
+        self.opt = torch.optim.Adam(model.parameters(), lr=cfg.lr, fused=cuda)
         broadcast_params(model)
 
-    def update(self, xw, actions, old_logp=None, adv=None, ret=None, generator: torch.Generator | None = None):
+    def update(self, xw, actions, old_logp=None, adv=None, ret=None, generator: torch.Generator | None = None,
+               adv_stats: torch.Tensor | None = None):
         """ppo_update on the whitened batch xw [B, O] of this
         rank (time x agents flattened).  The old policy is snapshotted on the
         same whitened batch before the first epoch (its log-probs, not the
@@ -100,10 +129,13 @@ class PPOLearner:
         gradient averaged across ranks; then KL(old || new) of the diagonal
         Gaussians, averaged over states and ranks, adapts the learning rate
         once (adapt_learning_rate, :468-475).  A non-finite loss restores the
-        snapshot, halves the learning rate and reports `aborted`."""
+        snapshot, halves the learning rate and reports `aborted`: the check is
+        one device flag read once after the epochs (no host synchronisation per
+        minibatch) — the steps after a non-finite loss are discarded with the
+        restore, so the outcome equals aborting at the first one."""
         cfg = self.cfg
         del old_logp  # re-derived from the snapshot below
-        adv = global_normalize(adv)
+        adv = global_normalize(adv, adv_stats)
         B = xw.shape[0]
         with torch.no_grad():
             mu_old = self.model.pi(xw)
@@ -116,8 +148,12 @@ class PPOLearner:
         mb = max(1, B // n_mb)
         lr = self.opt.param_groups[0]["lr"]
         loss = torch.zeros((), device=xw.device)
+        bad = torch.zeros((), device=xw.device)  # 1 once any loss was not finite
         for epoch in range(cfg.epochs):
-            perm = torch.randperm(B, generator=generator, device="cpu").to(xw.device)
+            if generator is None and xw.is_cuda:  # drawn on the device: no host round trip
+                perm = torch.randperm(B, device=xw.device)
+            else:  # an explicit (CPU) generator: reproducible permutations (tests)
+                perm = torch.randperm(B, generator=generator, device="cpu").to(xw.device)
             for s0 in range(0, B, mb):
                 idx = perm[s0:s0 + mb]
                 logp = self.model.log_prob(xw[idx], actions[idx])
@@ -127,22 +163,22 @@ class PPOLearner:
                 v = self.model.v(xw[idx]).squeeze(-1)
                 vf = ((v - ret[idx]) ** 2).mean()
                 loss = pg + cfg.vf_coef * vf
-                ok = torch.isfinite(loss).to(torch.float32)
-                if _dist():
-                    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-                if ok.item() < 1.0:  # abort: restore the snapshot, halve the learning rate
-                    with torch.no_grad():
-                        for p_, s_ in zip(self.model.parameters(), snapshot):
-                            p_.copy_(s_)
-                    self.opt.load_state_dict(opt_state)
-                    lr = max(lr / 2.0, 1e-6)
-                    for g in self.opt.param_groups:
-                        g["lr"] = lr
-                    return {"kl": 0.0, "lr": lr, "loss": float("nan"), "aborted": True}
+                bad = torch.maximum(bad, (~torch.isfinite(loss)).to(bad.dtype))
                 self.opt.zero_grad(set_to_none=False)
                 loss.backward()
                 allreduce_mean_grads(self.model)
                 self.opt.step()
+        if _dist():
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if bad.item() > 0:  # abort: restore the snapshot, halve the learning rate
+            with torch.no_grad():
+                for p_, s_ in zip(self.model.parameters(), snapshot):
+                    p_.copy_(s_)
+            self.opt.load_state_dict(opt_state)
+            lr = max(lr / 2.0, 1e-6)
+            for g in self.opt.param_groups:
+                g["lr"] = lr
+            return {"kl": 0.0, "lr": lr, "loss": float("nan"), "aborted": True}
         with torch.no_grad():
             kl = gaussian_kl(mu_old, ls_old, self.model.pi(xw), self.model.log_std).mean()
             if _dist():

@@ -73,10 +73,11 @@ def main(argv=None):
             stat.merge_allreduce(local_stat)  # observation-statistics allreduce
         else:
             stat._merge(local_stat.n, local_stat.mean, local_stat.m2)
-        adv, ret = gae(data["rew"], data["val"], data["done"], last_val, cfg.gamma, cfg.lam)
+        adv_stats = torch.zeros(3, dtype=torch.float64, device=dev)  # count, sum, sum of squares (GAE kernel)
+        adv, ret = gae(data["rew"], data["val"], data["done"], last_val, cfg.gamma, cfg.lam, stats=adv_stats)
         xw = stat.whiten(data["obs"].reshape(-1, env.obs_dim))
         stats = learner.update(xw, data["act"].reshape(-1, env.action_dim), data["logp"].reshape(-1),
-                               adv.reshape(-1), ret.reshape(-1))
+                               adv.reshape(-1), ret.reshape(-1), adv_stats=adv_stats)
         kern.refresh()
         torch.cuda.synchronize()
         t_it = time.perf_counter() - t0
