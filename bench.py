@@ -39,6 +39,34 @@ N_ENVS = 4096
 TASK = "humanoid"
 SEED = 1234
 
+# BASELINE.json configs as workloads (the default is the metric's: Humanoid,
+# 4096 envs per GPU).  flop = algorithmic FLOPs per env-step of the reference
+# algorithm (0.93 M Humanoid-size, 0.37 M Ant-size; terrain
+# contact work on top is not counted).  Terrain: boxes over the env grid.
+WORKLOADS = {
+    "humanoid4096": dict(task="humanoid", n=4096, flop=929_813.0,
+                         name="humanoid_run_flat_4096envs_random_actions", config="metric (configs[2] size)"),
+    "ant64": dict(task="ant", n=64, flop=369_122.0, name="ant_run_flat_64envs_random_actions", config="configs[0]"),
+    "humanoid1024": dict(task="humanoid", n=1024, flop=929_813.0, name="humanoid_run_flat_1024envs_random_actions",
+                         config="configs[1]"),
+    "hfh4096": dict(task="hfh", n=4096, flop=929_813.0,
+                    name="hfh_flagrun_4096envs_random_actions_interagent", config="configs[2]"),
+    "hfh_terrain4096": dict(task="hfh_terrain", n=4096, flop=929_813.0, boxes=2048, extent=131.0,
+                            name="hfh_terrain_4096envs_2048boxes_random_actions", config="configs[3]"),
+}
+
+
+def terrain_boxes(n_boxes, extent, seed=3):
+    """generate_terrain over the env grid: dims U[0.2, 1] m,
+    yaw U[0, pi) (counter-based RNG, fixed seed).  The oracle's restatement
+    (oracle/model_text.py) draws the same boxes as the device library's
+    stp_generate_terrain (tests/test_model_format.py), and keeps the CPU arms
+    off the product library."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import model_text
+    return model_text.generate_terrain(n_boxes, 0.2, 1.0, -3.0, extent, -3.0, extent, 0.0, 3.141592653589793, seed)
+
+
 # Algorithmic work of the reference algorithm per Humanoid env-step (FP32
 # roofline numerator), SURVEY.md §8(d.1): 0.93 MFLOP measured with a
 # counting-scalar build of the unmodified reference on a 22-body / 21-hinge
@@ -150,7 +178,7 @@ def _cpu_info():
 
 
 def cpu_reference_rate(n_envs: int, steps: int, warmup: int, threads: int, budget_s: float = 20.0,
-                       single_thread_s: float = 0.0):
+                       single_thread_s: float = 0.0, workload: str = "humanoid4096"):
     """Reference stampede::physics::step + restated env layer on host cores.
 
     Runs oracle/_ref (the compiled, unmodified reference, its Release flags)
@@ -166,13 +194,17 @@ def cpu_reference_rate(n_envs: int, steps: int, warmup: int, threads: int, budge
     import model_text
     from paper_1810_05762_b200 import abi  # ctypes struct layouts only (no library load)
     kind = "reference_fast" if available("reference_fast") else "restatement"
-    model = model_text.load_model("humanoid")
-    task = model_text.default_task(abi.TASK_HUMANOID)
+    wl = WORKLOADS[workload]
+    kinds = {"ant": abi.TASK_ANT, "humanoid": abi.TASK_HUMANOID, "hfh": abi.TASK_HFH,
+             "hfh_terrain": abi.TASK_HFH_TERRAIN}
+    model = model_text.load_model("ant" if wl["task"] == "ant" else "humanoid")
+    task = model_text.default_task(kinds[wl["task"]])
     cfg = model_text.default_step_config()
+    boxes = terrain_boxes(wl["boxes"], wl["extent"]) if wl.get("boxes") else None
 
     def measure(nthreads, budget, n_steps, n_warm):
         probe_n = min(n_envs, 64 * nthreads)
-        env = OracleEnv(model, task, cfg, probe_n, seed=SEED, nthreads=nthreads, kind=kind)
+        env = OracleEnv(model, task, cfg, probe_n, seed=SEED, nthreads=nthreads, kind=kind, terrain=boxes)
         for s in range(2):
             env.step(env.random_actions(s))
         t0 = time.perf_counter()
@@ -180,7 +212,7 @@ def cpu_reference_rate(n_envs: int, steps: int, warmup: int, threads: int, budge
         rate = probe_n / max(time.perf_counter() - t0, 1e-6)
         env.close()
         n_sample = int(max(16, min(n_envs, rate * budget / max(1, n_steps))))
-        env = OracleEnv(model, task, cfg, n_sample, seed=SEED, nthreads=nthreads, kind=kind)
+        env = OracleEnv(model, task, cfg, n_sample, seed=SEED, nthreads=nthreads, kind=kind, terrain=boxes)
         acts = [env.random_actions(s) for s in range(n_warm + n_steps)]
         for s in range(n_warm):
             env.step(acts[s])
@@ -195,9 +227,9 @@ def cpu_reference_rate(n_envs: int, steps: int, warmup: int, threads: int, budge
     info = _cpu_info()
     out = {"value": value, "unit": "env-steps/s", "cores": threads,
            "kind": "reference" if kind.startswith("reference") else "port",
-           "sample": f"{n_sample} of {n_envs} Humanoid envs x {steps} env_steps (random actions, auto-reset), "
+           "sample": f"{n_sample} of {n_envs} {wl['task']} envs x {steps} env_steps (random actions, auto-reset), "
                      f"{'oracle/_ref/libstampede_ref_fast.so: unmodified stampede::physics::step, -O3 -march=native, util::ThreadPool(' + str(threads) + ')' if kind.startswith('reference') else 'oracle/liboracle.so restatement'}"
-                     f" + restated env layer; model from assets/humanoid.model via oracle/model_text.py",
+                     f" + restated env layer; model from assets/*.model via oracle/model_text.py",
            **info}
     if single_thread_s > 0:
         v1, n1 = measure(1, single_thread_s, 2, 1)
@@ -242,11 +274,20 @@ def dist_setup(args):
     return world, rank, local
 
 
-def bench_config(world: int) -> dict:
+def bench_config(world: int, workload: str = "humanoid4096") -> dict:
     """The workload description, identical in both arms."""
-    return {"workload": "humanoid_run_flat_4096envs_random_actions", "envs_per_gpu": N_ENVS, "task": TASK,
-            "parallelism": f"dp{world} (env shards, no collective)",
-            "l2": "flushed between timed steps (256 MiB write)", "auto_reset": True}
+    wl = WORKLOADS[workload]
+    c = {"workload": wl["name"], "envs_per_gpu": wl["n"], "task": wl["task"], "baseline_config": wl["config"],
+         "parallelism": f"dp{world} (env shards, no collective)",
+         "l2": "flushed between timed steps (256 MiB write)", "auto_reset": True}
+    if wl.get("boxes"):
+        c["terrain"] = f"{wl['boxes']} static yaw boxes over [-3, {wl['extent']:.0f}] m^2 (generate_terrain, seed 3)"
+    return c
+
+
+def metric_name(workload: str) -> str:
+    return ("env-steps/sec (Humanoid, 4096 envs/GPU)" if workload == "humanoid4096"
+            else f"env-steps/sec ({WORKLOADS[workload]['name']})")
 
 
 def run_reference(args, world, rank):
@@ -254,13 +295,14 @@ def run_reference(args, world, rank):
         return
     threads = _cpu_info()["logical_cpus"]
     budget = float(os.environ.get("STP_BENCH_CPU_BUDGET_S", "90"))
-    r = cpu_reference_rate(N_ENVS, max(1, args.steps), max(0, args.warmup), threads, budget_s=budget,
-                           single_thread_s=min(10.0, budget / 6))
-    line = {"metric": "env-steps/sec (Humanoid, 4096 envs/GPU)", "value": r["value"], "unit": "env-steps/s",
+    n_envs = WORKLOADS[args.workload]["n"]
+    r = cpu_reference_rate(n_envs, max(1, args.steps), max(0, args.warmup), threads, budget_s=budget,
+                           single_thread_s=min(10.0, budget / 6), workload=args.workload)
+    line = {"metric": metric_name(args.workload), "value": r["value"], "unit": "env-steps/s",
             "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * N_ENVS / r["value"] if r["value"] else None, "higher_is_better": True,
+            "ms_per_step": 1e3 * n_envs / r["value"] if r["value"] else None, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": bench_config(world),
+            "config": bench_config(world, args.workload),
             "cpu_baseline": r,
             "e2e": {"value": r["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "CPU reference on the host cores of rank 0 only (one sample of the per-GPU workload)",
@@ -280,12 +322,16 @@ def _repo_libraries_loaded():
 
 
 def run_ours(args, world, rank, local):
+    global N_ENVS, TASK
+    wl = WORKLOADS[args.workload]
+    N_ENVS, TASK = wl["n"], wl["task"]
+    boxes = terrain_boxes(wl["boxes"], wl["extent"]) if wl.get("boxes") else None
     import torch
     from paper_1810_05762_b200.sim import VecEnv
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     assert torch.cuda.is_available(), "bench.py --impl ours needs a CUDA device (no CPU fallback)"
-    env = VecEnv(TASK, n_envs=N_ENVS, device=local, seed=SEED, env_offset=rank * N_ENVS)
+    env = VecEnv(TASK, n_envs=N_ENVS, device=local, seed=SEED, env_offset=rank * N_ENVS, terrain=boxes)
     K, Wm = args.steps, args.warmup
     # synthetic inputs resident in HBM before timing: one action batch per step
     acts = [env.random_actions(s) for s in range(Wm + K)]
@@ -332,7 +378,7 @@ def run_ours(args, world, rank, local):
     try:
         from paper_1810_05762_b200.policy import HIDDEN, ActorCritic, PolicyKernel, RunningStat
         torch.manual_seed(0)
-        model = ActorCritic(env.obs_dim, env.action_dim, HIDDEN[TASK]).to(dev)
+        model = ActorCritic(env.obs_dim, env.action_dim, HIDDEN.get(TASK, HIDDEN["hfh"])).to(dev)
         kern = PolicyKernel(model, dev)
         st = RunningStat(env.obs_dim, device=dev)
         st.push(obs)
@@ -369,7 +415,7 @@ def run_ours(args, world, rank, local):
         pol_ms = q0.elapsed_time(q1) / K
         rollout = {"env_steps_per_s": N_ENVS / (roll_ms / 1e3), "ms_per_step": roll_ms,
                    "policy_forward_ms": pol_ms, "policy_forward_timing": "CUDA graph of K forwards, device",
-                   "policy": f"tcgen05 SELU MLP pi+V {HIDDEN[TASK]} bf16",
+                   "policy": f"tcgen05 SELU MLP pi+V {HIDDEN.get(TASK, HIDDEN["hfh"])} bf16",
                    "l2": "not flushed"}
     except Exception as ex:
         rollout = {"error": repr(ex)}
@@ -379,10 +425,12 @@ def run_ours(args, world, rank, local):
     # iteration; informational (the metric above is the env step)
     ppo = None
     try:
+        if args.workload != "humanoid4096":
+            raise RuntimeError("PPO iteration timed for the metric workload only")
         from paper_1810_05762_b200.ppo import PPOConfig, PPOLearner, gae
         from paper_1810_05762_b200.ppo import rollout as ppo_rollout
         torch.manual_seed(0)
-        pmodel = ActorCritic(env.obs_dim, env.action_dim, HIDDEN[TASK]).to(dev)
+        pmodel = ActorCritic(env.obs_dim, env.action_dim, HIDDEN.get(TASK, HIDDEN["hfh"])).to(dev)
         pcfg = PPOConfig()
         learner = PPOLearner(pmodel, pcfg)
         pkern = PolicyKernel(pmodel, dev)
@@ -458,11 +506,12 @@ def run_ours(args, world, rank, local):
     peaks, src = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
-    f_env = F_ENV_STEP - F_PCR_ITER * (64.0 - kry_mean)  # live Krylov count
+    f_pcr_iter = F_PCR_ITER if TASK != "ant" else 71_617.0 / 16.0  # one PCR iteration
+    f_env = wl["flop"] - f_pcr_iter * (64.0 - kry_mean)  # live Krylov count
     achieved = N_ENVS * f_env / (ms_per_step / 1e3) / 1e12
     roof = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
             "frac": achieved / fp32_peak, "traffic": _traffic("k_env_step<float,32,2>"),
-            "kernel": "k_env_step<float,32,2>",
+            "kernel": f"k_env_step<float,32,{4 if wl.get('boxes') else 2}>",
             "flop_per_env_step": f_env, "krylov_iters_per_env_step": kry_mean,
             "peak_source": f"148 SM x 128 FP32 lanes x 2 x sm_max_mhz {sm_max:.0f} ({src})",
             "hbm_gbs_achieved": N_ENVS * 2700 / (ms_per_step / 1e3) / 1e9,
@@ -474,16 +523,16 @@ def run_ours(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cpu = cpu_reference_rate(N_ENVS, 5, 1, _cpu_info()["logical_cpus"], budget_s=20.0,
-                                     single_thread_s=6.0)
+                                     single_thread_s=6.0, workload=args.workload)
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"unavailable: {ex!r}"}
     per_rank = [N_ENVS * K / (ms / 1e3) for ms in per_rank_ms]
     if rank == 0:
-        line = {"metric": "env-steps/sec (Humanoid, 4096 envs/GPU)", "value": value, "unit": "env-steps/s",
+        line = {"metric": metric_name(args.workload), "value": value, "unit": "env-steps/s",
                 "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": bench_config(world),
+                "config": bench_config(world, args.workload),
                 "per_rank_env_steps_per_s": per_rank,
                 "weak_scaling_fraction_of_ideal": value / sum(per_rank),
                 "e2e": {"value": e2e_value, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
@@ -501,6 +550,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="humanoid4096",
+                    help="BASELINE config (default: the metric's Humanoid, 4096 envs per GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     self_launch(args)

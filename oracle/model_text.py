@@ -126,3 +126,37 @@ def default_task(kind: int) -> abi.Task:
     t.height_map = int(kind == abi.TASK_HFH_TERRAIN)
     t.inter_agent_collisions = int(hfh)
     return t
+
+
+# --- generate_terrain, restated for the CPU arms ---------
+M64 = 0xFFFFFFFFFFFFFFFF
+
+
+def _mix64(z):  # splitmix64, rng.hpp:25-31
+    z = (z + 0x9E3779B97F4A7C15) & M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def _uniform(stream, k):  # 24-bit counter-based uniform (DESIGN.md §5 RNG)
+    return (_mix64((stream + k) & M64) >> 40) * (1.0 / 16777216.0)
+
+
+def generate_terrain(count, dim_lo, dim_hi, x_lo, x_hi, y_lo, y_hi, yaw_lo, yaw_hi, seed):
+    """Static yaw boxes resting on z = 0: full edges U[dim_lo, dim_hi], centres
+    uniform over the rectangle, yaw U[yaw_lo, yaw_hi); box i draws from
+    derive_seed(seed, 5, i) (rng.hpp:35-37), the same draws as the device
+    library's stp_generate_terrain."""
+    out = []
+    for i in range(count):
+        s = _mix64(_mix64(_mix64(seed) ^ 5) ^ i)
+        b = abi.StaticBox()
+        for k in range(3):
+            b.half_extents[k] = 0.5 * (dim_lo + (dim_hi - dim_lo) * _uniform(s, k))
+        b.center[0] = x_lo + (x_hi - x_lo) * _uniform(s, 3)
+        b.center[1] = y_lo + (y_hi - y_lo) * _uniform(s, 4)
+        b.center[2] = b.half_extents[2]
+        b.yaw = yaw_lo + (yaw_hi - yaw_lo) * _uniform(s, 5)
+        out.append(b)
+    return out

@@ -106,3 +106,16 @@ def test_oracle_reader_matches_builtin(name):
     for k in (abi.TASK_ANT, abi.TASK_HUMANOID, abi.TASK_HFH, abi.TASK_HFH_TERRAIN):
         assert bytes(model_text.default_task(k)) == bytes(abi.default_task(k))
     assert C.sizeof(a) == C.sizeof(abi.Model)
+
+
+def test_oracle_terrain_generator_matches_device_library():
+    """The CPU arms' terrain restatement draws exactly the boxes of
+    stp_generate_terrain (same counter-based RNG)."""
+    import model_text
+    spec = abi.TerrainSpec(count=200, dim_lo=0.2, dim_hi=1.0, x_lo=-3.0, x_hi=131.0, y_lo=-3.0, y_hi=131.0,
+                           yaw_lo=0.0, yaw_hi=3.141592653589793, seed=3)
+    boxes = (abi.StaticBox * 200)()
+    assert abi.load().stp_generate_terrain(spec, boxes, 200) == 200
+    ours = model_text.generate_terrain(200, 0.2, 1.0, -3.0, 131.0, -3.0, 131.0, 0.0, 3.141592653589793, 3)
+    for a, b in zip(boxes, ours):
+        assert bytes(a) == bytes(b)
