@@ -120,7 +120,7 @@ typedef struct stp_step_config {
   double gravity[3];
   int32_t has_ground_plane;
   /* 1 (default) = reproduce the reference's block-pointer aliasing in
-   * assemble (solver.cpp:350-351 + block_sparse.cpp:218): when creating
+   * assemble (solver.cpp:350-351 + block_sparse.cpp:33-37): when creating
    * block (b,a) reallocates the block pool, the first row's contribution
    * to block (a,b) is lost.  0 = the symmetric system the reference
    * intends.  See DESIGN.md §"Reference quirks". */

@@ -908,7 +908,7 @@ void assemble(const Model<T>& m, const Dyn<T>* dyn, std::vector<Row<T>>& rows, s
     if (sa >= 0 && sb >= 0) {
       T* ab = H.at(sa, sb);
       // Reference quirk (solver.cpp:350-351): `ab` is taken before
-      // h.block(sb, sa) may grow the pool (block_sparse.cpp:218); when that
+      // h.block(sb, sa) may grow the pool (block_sparse.cpp:33-37); when that
       // reallocates, the writes through `ab` land in freed memory and this
       // row's contribution to block (sa, sb) is lost.  Emulated so the
       // oracle reproduces the reference's actual output.

@@ -254,7 +254,7 @@ void build_dev_model(const stp_model& m, const stp_step_config& cfg, stp::DevMod
     d.lim_lo[c] = T(s.limit_lo);
     d.lim_hi[c] = T(s.limit_hi);
     d.tmax[c] = T(s.max_torque);
-    // Reference aliasing quirk (solver.cpp:350-351, block_sparse.cpp:218):
+    // Reference aliasing quirk (solver.cpp:350-351, block_sparse.cpp:33-37):
     // with n_dyn diagonal blocks created first and two blocks per coupled
     // pair in row order, creating (child, parent) reallocates the block pool
     // exactly when the count before it is a power of two.

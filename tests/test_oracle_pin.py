@@ -68,7 +68,7 @@ def test_restatement_bit_exact_vs_compiled_reference(name):
 
 
 def test_assembly_quirk_pattern():
-    """Reference aliasing quirk (solver.cpp:350-351 + block_sparse.cpp:218):
+    """Reference aliasing quirk (solver.cpp:350-351 + block_sparse.cpp:33-37):
     the Humanoid's assembled H is symmetric, the Ant's loses anchor row 0 of
     joint 3 in block (3, 4) only; the restatement reproduces the reference's
     matrix bit-for-bit either way."""
