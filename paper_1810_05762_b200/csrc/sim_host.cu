@@ -60,6 +60,7 @@ struct stp_sim {
   int n_boxes = 0;
   void* d_scratch = nullptr;
   void* d_dbg = nullptr;  // assemble_system hook capture (stp_debug_first_system)
+  stp::IslandStreams isl{};  // inter-agent handles: island launches beside the main launch
   int dbg_env = -1;
   // terrain broadphase grid
   int grid_nx = 0, grid_ny = 0;
@@ -402,7 +403,12 @@ int launch_t(stp_sim* s, int mode, const float* torques, const float* actions, f
     a.big_bar = v.big_bar;
     a.big_xch = reinterpret_cast<T*>(v.big_xch);
   }
-  const cudaError_t e = stp::launch_env_step<T>(a, s->W, s->cpb, st);
+  if (a.merged && !s->isl.side) {
+    CK(cudaStreamCreateWithFlags(&s->isl.side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s->isl.fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s->isl.join, cudaEventDisableTiming));
+  }
+  const cudaError_t e = stp::launch_env_step<T>(a, s->W, s->cpb, st, a.merged ? &s->isl : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "k_env_step launch");
   return STP_OK;
 }
@@ -614,6 +620,12 @@ void stp_destroy(stp_sim* s) {
     if (s->ev_out[c]) cudaEventDestroy(s->ev_out[c]);
   }
   if (s->ev_in) cudaEventDestroy(s->ev_in);
+  if (s->isl.side) {
+    cudaStreamSynchronize(s->isl.side);
+    cudaStreamDestroy(s->isl.side);
+    cudaEventDestroy(s->isl.fork);
+    cudaEventDestroy(s->isl.join);
+  }
   if (s->ev_caller) cudaEventDestroy(s->ev_caller);
   stp::pair_scratch_free(s->pairs);
   for (void* p : s->allocations) cudaFree(p);

@@ -40,8 +40,15 @@ constexpr int kXSlotRows = 19 + 36 + 1;
 constexpr int kScratchRows = 55 + 11 * kSpillSlots + kXSlotRows * kXSlots;
 // lanes = W (8/16/32 lanes per env), cpb = shared-memory contact slots per body
 // (2: plane only; 4 + kSpillSlots overflow rows: terrain boxes, dynamic boxes).
+// side stream + fork / join events of a handle with inter-agent collisions:
+// the island launches run concurrently with the main step launch
+struct IslandStreams {
+  cudaStream_t side;
+  cudaEvent_t fork, join;
+};
 template <class T>
-cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s);
+cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s,
+                            const IslandStreams* isl = nullptr);
 
 // CTAs of the island launch that are co-resident on the current device (the
 // budget of big-island parts per step, sim_step.cuh big_island_ctas).

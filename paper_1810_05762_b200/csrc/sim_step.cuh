@@ -433,67 +433,11 @@ __host__ __device__ constexpr int island_cap() {
 }
 constexpr int kXch = kXchEntries;  // per-lane exchange entries (Mi is the largest)
 
-template <class T, int W, int CPB, bool ISL = false, bool DBG = false>
-__global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
-    k_env_step(const KArgs<T> a) {
-  int e;
-  int isl_m = 1, isl_w = 0;  // island size and this warp's place in it
-  const int* mem = nullptr;  // the island's member envs (unordered)
-  int* bar_ctr = nullptr;    // big islands: global barrier counter
-  T* big_area = nullptr;     // big islands: the island's global exchange area
-  if constexpr (ISL) {
-    static_assert(W == 32, "island mode: one env per warp");
-    constexpr int cap = island_cap<T>();
-    if (a.isl_big_mode) {
-      // this CTA's (big island, part): parts of an island are consecutive CTAs
-      const int nbig = *a.big_count;
-      int acc = 0, bi = -1, part = 0;
-      for (int i = 0; i < nbig; ++i) {
-        const int p = (a.big_size[i] + cap - 1) / cap;
-        if (int(blockIdx.x) < acc + p) {
-          bi = i;
-          part = int(blockIdx.x) - acc;
-          break;
-        }
-        acc += p;
-      }
-      if (bi < 0) return;
-      isl_m = a.big_size[bi];
-      mem = a.big_members + a.big_off[bi];
-      isl_w = part * cap + int(threadIdx.x >> 5);
-      if (isl_w >= isl_m) return;  // never arrives at the island barrier
-      bar_ctr = a.big_bar + bi;
-      big_area = a.big_xch + size_t(a.big_off[bi]) * kBigStride;
-      // env = the member of rank isl_w (index order = the reference's slot order)
-      const int ln = threadIdx.x & 31;
-      int found = -1;
-      for (int k = ln; k < isl_m; k += 32) {
-        const int mk = mem[k];
-        int rank = 0;
-        for (int j = 0; j < isl_m; ++j) rank += mem[j] < mk;
-        if (rank == isl_w) found = mk;
-      }
-      e = __reduce_max_sync(0xffffffffu, found);
-    } else {
-      if (blockIdx.x >= unsigned(*a.isl_count)) return;
-      mem = a.isl_members + blockIdx.x * kIslandMax;
-      isl_m = 0;
-      for (int k = 0; k < kIslandMax; ++k) isl_m += mem[k] >= 0;
-      isl_w = threadIdx.x >> 5;
-      if (isl_w >= isl_m) return;  // before the first island barrier (big islands: isl_m = 0 here)
-      e = -1;
-      for (int k = 0; k < isl_m; ++k) {
-        int rank = 0;
-        for (int j = 0; j < isl_m; ++j) rank += mem[j] < mem[k];
-        if (rank == isl_w) e = mem[k];
-      }
-    }
-  } else {
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    e = a.e_begin + tid / W;
-    if (e >= a.n) return;  // whole segments exit together
-    if (a.merged && a.merged[e] == 1) return;  // stepped by the island launch
-  }
+// The step of one env (one warp segment; island mode: one warp of an island)
+// after the env / island selection of the kernel below.
+template <class T, int W, int CPB, bool ISL, bool DBG>
+__device__ __forceinline__ void env_step_body(const KArgs<T>& a, const int e, const int isl_m, const int isl_w,
+                                              const int* mem, int* bar_ctr, T* big_area) {
   const int lane = threadIdx.x & 31;
   const int b = lane % W;
   const int base = lane - b;
@@ -2203,6 +2147,72 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
   }
 }
 
+template <class T, int W, int CPB, bool ISL = false, bool DBG = false>
+__global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
+    k_env_step(const KArgs<T> a) {
+  if constexpr (ISL) {
+    static_assert(W == 32, "island mode: one env per warp");
+    constexpr int cap = island_cap<T>();
+    if (a.isl_big_mode) {
+      // this CTA's (big island, part): parts of an island are consecutive CTAs
+      const int nbig = *a.big_count;
+      int acc = 0, bi = -1, part = 0;
+      for (int i = 0; i < nbig; ++i) {
+        const int p = (a.big_size[i] + cap - 1) / cap;
+        if (int(blockIdx.x) < acc + p) {
+          bi = i;
+          part = int(blockIdx.x) - acc;
+          break;
+        }
+        acc += p;
+      }
+      if (bi < 0) return;
+      const int isl_m = a.big_size[bi];
+      const int* mem = a.big_members + a.big_off[bi];
+      const int isl_w = part * cap + int(threadIdx.x >> 5);
+      if (isl_w >= isl_m) return;  // never arrives at the island barrier
+      // env = the member of rank isl_w (index order = the reference's slot order)
+      const int ln = threadIdx.x & 31;
+      int found = -1;
+      for (int k = ln; k < isl_m; k += 32) {
+        const int mk = mem[k];
+        int rank = 0;
+        for (int j = 0; j < isl_m; ++j) rank += mem[j] < mk;
+        if (rank == isl_w) found = mk;
+      }
+      const int e = __reduce_max_sync(0xffffffffu, found);
+      env_step_body<T, W, CPB, ISL, DBG>(a, e, isl_m, isl_w, mem, a.big_bar + bi,
+                                         a.big_xch + size_t(a.big_off[bi]) * kBigStride);
+      return;
+    }
+    // islands of <= cap envs: a persistent grid, each CTA takes islands
+    // blockIdx.x, + gridDim.x, ... (the island count is known on the device only)
+    const int n_isl = *a.isl_count;
+    for (int i = blockIdx.x; i < n_isl; i += gridDim.x) {
+      const int* mem = a.isl_members + i * kIslandMax;
+      int isl_m = 0;
+      for (int k = 0; k < kIslandMax; ++k) isl_m += mem[k] >= 0;
+      const int isl_w = threadIdx.x >> 5;
+      if (isl_w < isl_m) {  // the other warps wait at the barrier below
+        int e = -1;
+        for (int k = 0; k < isl_m; ++k) {
+          int rank = 0;
+          for (int j = 0; j < isl_m; ++j) rank += mem[j] < mem[k];
+          if (rank == isl_w) e = mem[k];
+        }
+        env_step_body<T, W, CPB, ISL, DBG>(a, e, isl_m, isl_w, mem, nullptr, nullptr);
+      }
+      __syncthreads();  // exchange area and named barrier free for the next island
+    }
+  } else {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int e = a.e_begin + tid / W;
+    if (e >= a.n) return;  // whole segments exit together
+    if (a.merged && a.merged[e] == 1) return;  // stepped by the island launch
+    env_step_body<T, W, CPB, ISL, DBG>(a, e, 1, 0, nullptr, nullptr, nullptr);
+  }
+}
+
 template <class T, int W, int CPB, bool DBG = false>
 static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
   constexpr int threads = kStepThreads;
@@ -2233,7 +2243,16 @@ static cudaError_t launch_island(const KArgs<T>& a, cudaStream_t s) {
                                            int(smem));
     if (err != cudaSuccess) return err;
   }
-  const int grid = (a.n - a.e_begin) / 2 > 0 ? (a.n - a.e_begin) / 2 : 1;  // at most n/2 merged islands
+  // a persistent grid (islands are taken round-robin): at most n / 2 islands,
+  // at most one CTA per SM
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int half = (a.n - a.e_begin) / 2 > 0 ? (a.n - a.e_begin) / 2 : 1;
+  const int grid = half < sms ? half : sms;
   k_env_step<T, W, CPB, true><<<grid, 32 * cap, smem, s>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !a.big_count) return e;
@@ -2278,18 +2297,33 @@ int island_launch_budget(int cpb) {
 }
 
 template <class T>
-cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s) {
+cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s, const IslandStreams* isl) {
   if (a.dbg) {  // assemble_system hook: its own instantiations (no cost on the hot path)
     if (a.merged) return cudaErrorInvalidValue;
     if (lanes == 32) return cpb <= 2 ? launch_one<T, 32, 2, true>(a, s) : launch_one<T, 32, 4, true>(a, s);
     if (lanes == 16) return cpb <= 2 ? launch_one<T, 16, 2, true>(a, s) : launch_one<T, 16, 4, true>(a, s);
     return cpb <= 2 ? launch_one<T, 8, 2, true>(a, s) : launch_one<T, 8, 4, true>(a, s);
   }
-  if (a.merged) {  // inter-agent collisions: independent envs, then the merged islands
+  if (a.merged) {  // inter-agent collisions: the merged islands and the independent envs
     if (lanes != 32) return cudaErrorInvalidValue;
-    cudaError_t e = cpb <= 2 ? launch_one<T, 32, 2>(a, s) : launch_one<T, 32, 4>(a, s);
+    // The island launches touch only merged envs and the main launch skips
+    // them, so they run concurrently: islands first on the side stream (an
+    // island CTA is one latency-bound chain of a few warps), the main launch
+    // on `s` filling the rest of the machine, then `s` joins the side stream.
+    cudaStream_t is = isl && isl->side ? isl->side : s;
+    cudaError_t e = cudaSuccess;
+    if (is != s) {
+      e = cudaEventRecord(isl->fork, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(is, isl->fork, 0);
+      if (e != cudaSuccess) return e;
+    }
+    e = cpb <= 2 ? launch_island<T, 32, 2>(a, is) : launch_island<T, 32, 4>(a, is);
     if (e != cudaSuccess) return e;
-    return cpb <= 2 ? launch_island<T, 32, 2>(a, s) : launch_island<T, 32, 4>(a, s);
+    e = cpb <= 2 ? launch_one<T, 32, 2>(a, s) : launch_one<T, 32, 4>(a, s);
+    if (e != cudaSuccess || is == s) return e;
+    e = cudaEventRecord(isl->join, is);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, isl->join, 0);
+    return e;
   }
   if (lanes == 32) {
     if (cpb <= 2) return launch_one<T, 32, 2>(a, s);

@@ -1,0 +1,8 @@
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import torch
+from paper_1810_05762_b200.sim import VecEnv
+env = VecEnv("hfh", n_envs=4096, seed=1234)
+for t in range(int(os.environ.get("STEPS", "130"))):
+    env.step(env.random_actions(t))
+torch.cuda.synchronize()
