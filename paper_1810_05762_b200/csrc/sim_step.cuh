@@ -1562,8 +1562,8 @@ __device__ __forceinline__ void env_step_body(const KArgs<T>& a, const int e, co
           constexpr int GR = decltype(gr_c)::value;
           // y = Ahat v: the env's own blocks, plus in island mode the
           // inter-agent coupling blocks against the partners' v (exchange area)
-          auto apply_x = [&](const T (&v)[6], T (&y)[6]) {
-            L.template apply_hat<RARE, GR>(v, y);
+          // island mode: += the inter-agent coupling blocks against the partners' v
+          auto couple = [&](const T (&v)[6], T (&y)[6]) {
             if constexpr (ISL) {
               T* my = xch + (isl_w * 32 + lane) * kXch;
 #pragma unroll
@@ -1583,23 +1583,43 @@ __device__ __forceinline__ void env_step_body(const KArgs<T>& a, const int e, co
               isl_bar();
             }
           };
-          if constexpr (sizeof(T) == 4 && kPackedPCR && !ISL) {
-            // fp32: the loop on packed pairs (see Lane::apply_hat_p)
+          auto apply_x = [&](const T (&v)[6], T (&y)[6]) {
+            L.template apply_hat<RARE, GR>(v, y);
+            couple(v, y);
+          };
+          if constexpr (sizeof(T) == 4 && kPackedPCR) {
+            // fp32: the loop on packed pairs (see Lane::apply_hat_p); island
+            // mode adds the coupling blocks and takes its sums / votes over the
+            // island (apply_p, sum3 / sum4, all_of)
             float2 Hp[18];
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
 #pragma unroll
               for (int rp = 0; rp < 3; ++rp) Hp[3 * c + rp] = make_float2(L.Hh[(2 * rp) * 6 + c], L.Hh[(2 * rp + 1) * 6 + c]);
             }
+            auto apply_p = [&](const float2 (&v)[3], float2 (&y)[3]) {
+              L.template apply_hat_p<RARE, GR>(v, y, Hp);
+              if constexpr (ISL) {
+                const T vs[6] = {v[0].x, v[0].y, v[1].x, v[1].y, v[2].x, v[2].y};
+                T ys[6] = {y[0].x, y[0].y, y[1].x, y[1].y, y[2].x, y[2].y};
+                couple(vs, ys);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) y[k] = make_float2(ys[2 * k], ys[2 * k + 1]);
+              }
+            };
+            auto all_of = [&](bool p) -> bool {
+              if constexpr (ISL) return isl_all(p);
+              else return __all_sync(mask, p);
+            };
             float2 x2[3], rh[3], ar[3], ph[3], ap[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) x2[k] = make_float2(xh[2 * k], xh[2 * k + 1]);
-            L.template apply_hat_p<RARE, GR>(x2, ar, Hp);
+            apply_p(x2, ar);
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
               rh[k] = dyn ? make_float2(bh[2 * k] - ar[k].x, bh[2 * k + 1] - ar[k].y) : make_float2(0.f, 0.f);
             }
-            L.template apply_hat_p<RARE, GR>(rh, ar, Hp);
+            apply_p(rh, ar);
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
               ph[k] = rh[k];
@@ -1610,7 +1630,12 @@ __device__ __forceinline__ void env_step_body(const KArgs<T>& a, const int e, co
               return res_exact(r6);
             };
             T zaz = dot6p(rh, ar), lb = lbw * dot6p(rh, rh), denom = dot6p(ar, ar);
-            seg_sum3<W>(zaz, lb, denom, mask);
+            if constexpr (ISL) {
+              T dummy = T(0);
+              isl_sum4(zaz, lb, denom, dummy);
+            } else {
+              seg_sum3<W>(zaz, lb, denom, mask);
+            }
             int kk = 0;
             // Exit tests of krylov.cpp: ||r|| <= tol ||b|| (:141, :154) and the
             // breakdown test (:144) of the next trip are decided together at
@@ -1618,8 +1643,8 @@ __device__ __forceinline__ void env_step_body(const KArgs<T>& a, const int e, co
             // segment-uniform, so every test is one vote.
             auto go_on = [&](float lbv, float zv, float dv) {
               bool above = lbv > tol2_safe;
-              if (!__all_sync(mask, above)) above = res_exact_p() > tol2;  // near convergence only
-              return __all_sync(mask, above && dv > 0.f && zv > 0.f);
+              if (!all_of(above)) above = res_exact_p() > tol2;  // near convergence only
+              return all_of(above && dv > 0.f && zv > 0.f);
             };
             if (kk < cf.kmax && go_on(lb, zaz, denom)) {
               for (;;) {
@@ -1630,11 +1655,12 @@ __device__ __forceinline__ void env_step_body(const KArgs<T>& a, const int e, co
                   rh[k] = __ffma2_rn(ap[k], make_float2(-alpha, -alpha), rh[k]);
                 }
                 if (++kk >= cf.kmax) break;  // exit certain: the rest cannot change xhat
-                L.template apply_hat_p<RARE, GR>(rh, ar, Hp);
+                apply_p(rh, ar);
                 // one reduction per trip: (lb, zn) and (aa, ax) as two pairs
                 float2 q0 = make_float2(lbw * dot6p(rh, rh), dot6p(rh, ar));
                 float2 q1 = make_float2(dot6p(ar, ar), dot6p(ar, ap));
-                seg_sum2x2<W>(q0, q1, mask);
+                if constexpr (ISL) isl_sum4(q0.x, q0.y, q1.x, q1.y);
+                else seg_sum2x2<W>(q0, q1, mask);
                 const float zn = q0.y, aa = q1.x, ax = q1.y;
                 const float beta = fdiv(zn, zaz);
                 denom = aa + beta * (2.f * ax + beta * denom);
