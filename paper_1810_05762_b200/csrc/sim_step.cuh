@@ -433,11 +433,77 @@ __host__ __device__ constexpr int island_cap() {
 }
 constexpr int kXch = kXchEntries;  // per-lane exchange entries (Mi is the largest)
 
-// The step of one env (one warp segment; island mode: one warp of an island)
-// after the env / island selection of the kernel below.
-template <class T, int W, int CPB, bool ISL, bool DBG>
-__device__ __forceinline__ void env_step_body(const KArgs<T>& a, const int e, const int isl_m, const int isl_w,
-                                              const int* mem, int* bar_ctr, T* big_area) {
+template <class T, int W, int CPB, bool ISL = false, bool DBG = false>
+__global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
+    k_env_step(const KArgs<T> a) {
+  // env / island selection.  Island mode: big islands (isl_big_mode) are
+  // consecutive CTAs of a cooperative launch; islands of <= cap envs are taken
+  // round-robin by a persistent grid (isl_next), each CTA looping over them.
+  int e = -1, isl_m = 1, isl_w = 0;
+  const int* mem = nullptr;  // the island's member envs (unordered)
+  int* bar_ctr = nullptr;    // big islands: global barrier counter
+  T* big_area = nullptr;     // big islands: the island's global exchange area
+  int isl_next = 0, n_isl = 0;
+  if constexpr (ISL) {
+    static_assert(W == 32, "island mode: one env per warp");
+    constexpr int cap = island_cap<T>();
+    if (a.isl_big_mode) {
+      // this CTA's (big island, part): parts of an island are consecutive CTAs
+      const int nbig = *a.big_count;
+      int acc = 0, bi = -1, part = 0;
+      for (int i = 0; i < nbig; ++i) {
+        const int p = (a.big_size[i] + cap - 1) / cap;
+        if (int(blockIdx.x) < acc + p) {
+          bi = i;
+          part = int(blockIdx.x) - acc;
+          break;
+        }
+        acc += p;
+      }
+      if (bi < 0) return;
+      isl_m = a.big_size[bi];
+      mem = a.big_members + a.big_off[bi];
+      isl_w = part * cap + int(threadIdx.x >> 5);
+      if (isl_w >= isl_m) return;  // never arrives at the island barrier
+      bar_ctr = a.big_bar + bi;
+      big_area = a.big_xch + size_t(a.big_off[bi]) * kBigStride;
+      // env = the member of rank isl_w (index order = the reference's slot order)
+      const int ln = threadIdx.x & 31;
+      int found = -1;
+      for (int k = ln; k < isl_m; k += 32) {
+        const int mk = mem[k];
+        int rank = 0;
+        for (int j = 0; j < isl_m; ++j) rank += mem[j] < mk;
+        if (rank == isl_w) found = mk;
+      }
+      e = __reduce_max_sync(0xffffffffu, found);
+    } else {
+      n_isl = *a.isl_count;
+      isl_next = blockIdx.x;
+    }
+  } else {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    e = a.e_begin + tid / W;
+    if (e >= a.n) return;  // whole segments exit together
+    if (a.merged && a.merged[e] == 1) return;  // stepped by the island launch
+  }
+  for (;;) {
+    if constexpr (ISL) {
+      if (!a.isl_big_mode) {  // the next island of this CTA
+        if (isl_next >= n_isl) return;
+        mem = a.isl_members + isl_next * kIslandMax;
+        isl_m = 0;
+        for (int k = 0; k < kIslandMax; ++k) isl_m += mem[k] >= 0;
+        isl_w = threadIdx.x >> 5;
+        e = -1;
+        for (int k = 0; k < isl_m; ++k) {
+          int rank = 0;
+          for (int j = 0; j < isl_m; ++j) rank += mem[j] < mem[k];
+          if (rank == isl_w) e = mem[k];
+        }
+      }
+    }
+    if (!ISL || a.isl_big_mode || isl_w < isl_m) {  // the step of env e
   const int lane = threadIdx.x & 31;
   const int b = lane % W;
   const int base = lane - b;
@@ -2171,71 +2237,11 @@ __device__ __forceinline__ void env_step_body(const KArgs<T>& a, const int e, co
     else if (a.merged) ov = ov || a.merged[e] == 2 || (*a.isl_err & 8) != 0;
     if (b == 0) a.overflow_out[e] = ov ? 1 : 0;
   }
-}
-
-template <class T, int W, int CPB, bool ISL = false, bool DBG = false>
-__global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
-    k_env_step(const KArgs<T> a) {
-  if constexpr (ISL) {
-    static_assert(W == 32, "island mode: one env per warp");
-    constexpr int cap = island_cap<T>();
-    if (a.isl_big_mode) {
-      // this CTA's (big island, part): parts of an island are consecutive CTAs
-      const int nbig = *a.big_count;
-      int acc = 0, bi = -1, part = 0;
-      for (int i = 0; i < nbig; ++i) {
-        const int p = (a.big_size[i] + cap - 1) / cap;
-        if (int(blockIdx.x) < acc + p) {
-          bi = i;
-          part = int(blockIdx.x) - acc;
-          break;
-        }
-        acc += p;
-      }
-      if (bi < 0) return;
-      const int isl_m = a.big_size[bi];
-      const int* mem = a.big_members + a.big_off[bi];
-      const int isl_w = part * cap + int(threadIdx.x >> 5);
-      if (isl_w >= isl_m) return;  // never arrives at the island barrier
-      // env = the member of rank isl_w (index order = the reference's slot order)
-      const int ln = threadIdx.x & 31;
-      int found = -1;
-      for (int k = ln; k < isl_m; k += 32) {
-        const int mk = mem[k];
-        int rank = 0;
-        for (int j = 0; j < isl_m; ++j) rank += mem[j] < mk;
-        if (rank == isl_w) found = mk;
-      }
-      const int e = __reduce_max_sync(0xffffffffu, found);
-      env_step_body<T, W, CPB, ISL, DBG>(a, e, isl_m, isl_w, mem, a.big_bar + bi,
-                                         a.big_xch + size_t(a.big_off[bi]) * kBigStride);
-      return;
     }
-    // islands of <= cap envs: a persistent grid, each CTA takes islands
-    // blockIdx.x, + gridDim.x, ... (the island count is known on the device only)
-    const int n_isl = *a.isl_count;
-    for (int i = blockIdx.x; i < n_isl; i += gridDim.x) {
-      const int* mem = a.isl_members + i * kIslandMax;
-      int isl_m = 0;
-      for (int k = 0; k < kIslandMax; ++k) isl_m += mem[k] >= 0;
-      const int isl_w = threadIdx.x >> 5;
-      if (isl_w < isl_m) {  // the other warps wait at the barrier below
-        int e = -1;
-        for (int k = 0; k < isl_m; ++k) {
-          int rank = 0;
-          for (int j = 0; j < isl_m; ++j) rank += mem[j] < mem[k];
-          if (rank == isl_w) e = mem[k];
-        }
-        env_step_body<T, W, CPB, ISL, DBG>(a, e, isl_m, isl_w, mem, nullptr, nullptr);
-      }
-      __syncthreads();  // exchange area and named barrier free for the next island
-    }
-  } else {
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int e = a.e_begin + tid / W;
-    if (e >= a.n) return;  // whole segments exit together
-    if (a.merged && a.merged[e] == 1) return;  // stepped by the island launch
-    env_step_body<T, W, CPB, ISL, DBG>(a, e, 1, 0, nullptr, nullptr, nullptr);
+    if constexpr (!ISL) return;
+    if (a.isl_big_mode) return;
+    __syncthreads();  // exchange area and named barrier free for the next island
+    isl_next += gridDim.x;
   }
 }
 

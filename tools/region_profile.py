@@ -32,7 +32,7 @@ for ln in fn.splitlines():
     if m:
         f, l, fi, li = m.group(1), int(m.group(2)), m.group(3), m.group(4)
         if f.endswith("sim_step.cuh"):
-            cur = l if not (fi and fi.endswith("sim_step.cuh")) else int(li)
+            cur = l  # the step body is one inlined function: its own line is the useful one
         elif fi and fi.endswith("sim_step.cuh"):
             cur = int(li)
         else:
@@ -106,3 +106,16 @@ if "--stalls" in sys.argv:
             byop[op.split(".")[0]] += int(r[ist])
     print("  stall samples by opcode (of the stalled instruction):",
           ", ".join(f"{k} {100 * v / max(1, sum(byop.values())):.0f}%" for k, v in byop.most_common(10)))
+
+if "--spills" in sys.argv:
+    # executed local-memory instructions (LDL / STL) per source line
+    byl = Counter()
+    for i, r in enumerate(R):
+        op = ins[i][1]
+        if "LDL" in op or "STL" in op:
+            byl[ins[i][0]] += int(r[ia])
+    tot_sp = sum(byl.values())
+    print(f"spill instructions executed per warp: {tot_sp / nw:.0f}")
+    for l, n in byl.most_common(25):
+        txt = src[l - 1].strip()[:80] if l and l > 0 else ""
+        print(f"{n / nw:8.1f}  {l}: {txt}  [{region(l)}]")
