@@ -24,8 +24,10 @@
 // chunks through one buffer, every chunk accumulating into the same TMEM
 // accumulator.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "stampede_sim.h"
 #include "stp_error.h"
@@ -113,6 +115,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// programmatic dependent launch (griddepcontrol): wait for the preceding
+// grid's completion and memory; let the next grid launch
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+// one lane of a converged warp (elect.sync): the MMA issue region, so that
+// ptxas knows a single thread issues and keeps the descriptors in uniform
+// registers (a `tid == 0` region makes it wrap every tcgen05.mma in an
+// ELECT / R2UR.BROADCAST loop over the possibly active threads)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n"
+      : "+r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];\n" ::"l"(
                    reinterpret_cast<uint64_t>(__cvta_generic_to_shared(bar)))
@@ -142,11 +161,38 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 // __expf(y) is ex2.approx(y * log2 e); the flush-to-zero form skips the
 // denormal-range fixups, which only differ for y < -87 where SELU's negative
 // branch rounds to -lambda*alpha either way.
+#ifndef STP_K4_SELU
+#define STP_K4_SELU 0
+#endif
 __device__ __forceinline__ float selu(float x) {
+#if STP_K4_SELU == 2  // timing experiment only: identity
+  return x;
+#else
   float e;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fminf(x, 0.f) * 1.4426950408889634f));
   const float neg = kSeluL * kSeluA * (e - 1.f);
   return x > 0.f ? kSeluL * x : neg;
+#endif
+}
+
+// bias + SELU on a thread's 16 accumulator columns.  STP_K4_SELU == 1
+// (experiment): the exponentials as ex2.approx.f16x2, two per MUFU op.
+__device__ __forceinline__ void selu16(float (&v)[16], float bias) {
+#if STP_K4_SELU == 1
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float a = v[2 * i] + bias, b = v[2 * i + 1] + bias;
+    const __half2 t = __floats2half2_rn(fminf(a, 0.f) * 1.4426950408889634f, fminf(b, 0.f) * 1.4426950408889634f);
+    uint32_t e2;
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(e2) : "r"(*reinterpret_cast<const uint32_t*>(&t)));
+    const float2 e = __half22float2(*reinterpret_cast<const __half2*>(&e2));
+    v[2 * i] = a > 0.f ? kSeluL * a : kSeluL * kSeluA * (e.x - 1.f);
+    v[2 * i + 1] = b > 0.f ? kSeluL * b : kSeluL * kSeluA * (e.y - 1.f);
+  }
+#else
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = selu(v[i] + bias);
+#endif
 }
 
 
@@ -160,14 +206,19 @@ __device__ __forceinline__ void st_xt(__nv_bfloat16* buf, int kpad, int k, int n
 }
 
 // Experiment-only phase timestamps (tools/exp/k4_phases.py builds with
-// -DSTP_K4_PHASES): thread 0 of each CTA records %globaltimer at phase ends.
+// -DSTP_K4_PHASES): thread 0 of each CTA records %globaltimer (phase 0) and
+// the SM clock (every phase) at phase ends.
 #ifdef STP_K4_PHASES
-constexpr int kPhases = 16;
+constexpr int kPhases = 32;
 __device__ unsigned long long g_k4_phase[1024 * kPhases];
 __device__ __forceinline__ void phase(int i) {
   if (threadIdx.x == 0) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (i == 0) {
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      g_k4_phase[(blockIdx.y * gridDim.x + blockIdx.x) * kPhases + 31] = t;
+    }
+    t = clock64();
     g_k4_phase[(blockIdx.y * gridDim.x + blockIdx.x) * kPhases + i] = t;
   }
 }
@@ -185,9 +236,10 @@ struct Smem {
   alignas(16) float winv[256];
   uint64_t streams[kMaxNT];  // policy noise stream per environment of the tile
   float sdv[256];            // exp(log_std) per action
+  float lsd[256];            // log_std per action
   alignas(16) float bias[4][256];  // the net's biases (TMA bulk copies, padded widths)
 };
-constexpr int kHeader = 8192;  // Smem, rounded to the operand alignment
+constexpr int kHeader = 9216;  // Smem, rounded to the operand alignment
 static_assert(sizeof(Smem) <= kHeader, "Smem header");
 constexpr int kTmemCols = 2 * kMaxNT;  // two M blocks x NT accumulator columns
 
@@ -215,7 +267,8 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
     const int mblocks = (D.n[l] + kM - 1) / kM;
     fence_async_smem();  // generic-proxy operand writes -> visible to the tensor core
     __syncthreads();
-    if (tid == 0) {
+    phase(13 + l);
+    if (warp == 0 && elect_one()) {
       tc_after_sync();
       const uint32_t xa = smem_u32(x_in);
       const uint32_t xsbo = uint32_t(D.k[l]) * 16;  // 8-environment group stride of X^T
@@ -256,8 +309,10 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
         }
       }
       umma_commit(&sh->bar_mma);
+      phase(17 + l);
     }
     bg(l);
+    phase(21 + l);
     mbar_wait(&sh->bar_mma, mphase);
     mphase ^= 1;
     tc_after_sync();
@@ -274,8 +329,7 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
       const float bias = h < D.n[l] ? sh->bias[l][h] : 0.f;
       float v[16];
       tmem_ld16(sh->tmem + (uint32_t(sp * 32) << 16) + uint32_t(mb * NT + ch * 16), v);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = selu(v[i] + bias);
+      selu16(v, bias);
       if (h < kout) {
         st_xt(x_out, kout, h, ch * 16, v);
         st_xt(x_out, kout, h, ch * 16 + 8, v + 8);
@@ -334,28 +388,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool tma_stat = tma_obs && (stat_bytes & 15) == 0 &&
                         ((reinterpret_cast<uintptr_t>(mean) | reinterpret_cast<uintptr_t>(stdv)) & 15) == 0;
   const bool stream = wbuf_elems > 0;
-  if (tid == 0) {
+  // Programmatic dependent launch: everything up to griddep_wait() reads only
+  // the network parameters (never written by a kernel that triggers early: the
+  // step kernel and K4 itself), so it overlaps the tail of the preceding grid;
+  // the observations, the whitening statistics and every output come after it.
+  if (warp == 1 && elect_one()) {  // barriers + weight TMA (warp 0 allocates TMEM meanwhile)
     mbar_init(&sh->bar_obs, 1);
     mbar_init(&sh->bar_w, 1);
     mbar_init(&sh->bar_mma, 1);
     mbar_init(&sh->bar_chunk, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    // biases (16-byte multiples: padded to 16 outputs) always by TMA on bar_obs
-    uint32_t bias_bytes = 0;
-    for (int l = 0; l < 4; ++l) bias_bytes += uint32_t(D.n[l]) * 4;
-    mbar_expect_tx(&sh->bar_obs, bias_bytes + (tma_obs ? tile_bytes : 0) + (tma_stat ? 2 * stat_bytes : 0));
-    for (int l = 0; l < 4; ++l) bulk_g2s(sh->bias[l], P.bias[l], uint32_t(D.n[l]) * 4, &sh->bar_obs);
-    if (tma_obs) {
-      bulk_g2s(stage, src, tile_bytes, &sh->bar_obs);
-      if (tma_stat) {
-        bulk_g2s(sh->wmean, mean, stat_bytes, &sh->bar_obs);
-        bulk_g2s(sh->winv, stdv, stat_bytes, &sh->bar_obs);  // the standard deviations themselves
-      }
-    }
-    if (!stream) {
+    if (!stream) {  // weights + biases (16-byte multiples: padded to 16 outputs) on bar_w
       uint32_t bytes = 0;
-      for (int l = 0; l < 4; ++l) bytes += uint32_t(D.k[l]) * D.n[l] * 2;
+      for (int l = 0; l < 4; ++l) bytes += uint32_t(D.k[l]) * D.n[l] * 2 + uint32_t(D.n[l]) * 4;
       mbar_expect_tx(&sh->bar_w, bytes);
+      for (int l = 0; l < 4; ++l) bulk_g2s(sh->bias[l], P.bias[l], uint32_t(D.n[l]) * 4, &sh->bar_w);
       for (int l = 0; l < 4; ++l) bulk_g2s(wsm[l], P.w[l], uint32_t(D.k[l]) * D.n[l] * 2, &sh->bar_w);
     }
   }
@@ -364,16 +411,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
-  if (!tma_stat)
-    for (int c = tid; c < obs_dim; c += kThreads) {
-      sh->wmean[c] = __ldg(mean + c);
-      sh->winv[c] = __ldg(stdv + c);
-    }
   if (!value_net && act_out) {
     for (int r = tid; r < rows; r += kThreads)
       sh->streams[r] = stp_derive_seed(seed, 6 /* policy noise */, (uint64_t(env_offset + tile0 + r) << 32) |
                                                                        uint32_t(step));
   }
+  griddep_wait();
+  griddep_launch_dependents();
+  if (warp == 1 && elect_one()) {  // observation tile + statistics (+ streaming mode: biases) on bar_obs
+    uint32_t bias_bytes = 0;
+    if (stream)
+      for (int l = 0; l < 4; ++l) bias_bytes += uint32_t(D.n[l]) * 4;
+    mbar_expect_tx(&sh->bar_obs, bias_bytes + (tma_obs ? tile_bytes : 0) + (tma_stat ? 2 * stat_bytes : 0));
+    if (stream)
+      for (int l = 0; l < 4; ++l) bulk_g2s(sh->bias[l], P.bias[l], uint32_t(D.n[l]) * 4, &sh->bar_obs);
+    if (tma_obs) {
+      bulk_g2s(stage, src, tile_bytes, &sh->bar_obs);
+      if (tma_stat) {
+        bulk_g2s(sh->wmean, mean, stat_bytes, &sh->bar_obs);
+        bulk_g2s(sh->winv, stdv, stat_bytes, &sh->bar_obs);  // the standard deviations themselves
+      }
+    }
+  }
+  if (!tma_stat)
+    for (int c = tid; c < obs_dim; c += kThreads) {
+      sh->wmean[c] = __ldg(mean + c);
+      sh->winv[c] = __ldg(stdv + c);
+    }
   if (!tma_obs) {
     const int nf = rows * obs_dim;
     for (int i = tid; i < nf; i += kThreads) stage[i] = __ldg(src + i);
@@ -392,38 +456,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kpad = D.k[0], ngr = NT / 8;
     for (int u = tid; u < kpad * ngr; u += kThreads) {
       const int k = u % kpad, g = u / kpad;
+      // branch-free: padded columns / rows read a clamped in-tile address and
+      // are zeroed by the select, so the 8 loads issue back to back
+      const bool kin = k < obs_dim;
+      const int kc = kin ? k : 0;
+      const float mk = sh->wmean[kc], ik = sh->winv[kc];
       float x8[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = g * 8 + i;
-        float x = 0.f;
-        if (r < rows && k < obs_dim) {
-          x = (stage[r * obs_dim + k] - sh->wmean[k]) * sh->winv[k];
-          x = fminf(fmaxf(x, -10.f), 10.f);
-        }
-        x8[i] = x;
+        const bool in = kin && r < rows;
+        const float x = (stage[(in ? r : 0) * obs_dim + kc] - mk) * ik;
+        x8[i] = in ? fminf(fmaxf(x, -10.f), 10.f) : 0.f;
       }
       st_xt(xb0, kpad, k, g * 8, x8);
     }
   }
   phase(2);
   uint32_t wphase = 0, mphase = 0;
-  // policy noise (Box-Muller on two 24-bit counter-based uniforms per element,
-  // fast log / cos: |err| ~1e-6) in four slices, drawn while the four layers'
-  // MMAs run
+  // policy noise: Box-Muller pairs (both the cosine and the sine branch) on
+  // two 24-bit counter-based uniforms of one 64-bit hash per pair of
+  // actions, fast log / sincos on [-pi, pi) (|err| ~1e-6), in four slices
+  // drawn while the four layers' MMAs run
   const bool draw = !value_net && act_out;
-  const int n_eps = draw ? rows * D.out : 0;
+  const int npair = (D.out + 1) / 2;
+  const int n_pairs = draw ? rows * npair : 0;
   auto noise = [&](int l) {
     if (l == 0 && draw)  // exp(log_std) (a global load: off the prologue's critical path)
-      for (int c = tid; c < D.out; c += kThreads) sh->sdv[c] = expf(log_std[c]);
-    const int e0 = n_eps * l / 4, e1 = n_eps * (l + 1) / 4;
-    for (int i = e0 + tid; i < e1; i += kThreads) {
-      const int r = i / D.out, c = i - r * D.out;
-      // one 64-bit hash per element: two 24-bit uniforms (bits 40-63, 16-39)
-      const uint64_t z = stp_mix64(sh->streams[r] + uint64_t(c));
+      for (int c = tid; c < D.out; c += kThreads) {
+        const float ls = log_std[c];
+        sh->lsd[c] = ls;
+        sh->sdv[c] = expf(ls);
+      }
+    const int p0 = n_pairs * l / 4, p1 = n_pairs * (l + 1) / 4;
+    for (int i = p0 + tid; i < p1; i += kThreads) {
+      const int r = i / npair, q = i - r * npair;
+      const uint64_t z = stp_mix64(sh->streams[r] + uint64_t(q));  // bits 40-63: u1, 16-39: u2
       const float u1 = fmaxf(float(z >> 40) * (1.f / 16777216.f), 1e-7f);
       const float u2 = float((z >> 16) & 0xffffffu) * (1.f / 16777216.f);
-      eps[i] = sqrtf(-2.f * __logf(u1)) * __cosf(6.2831853071795865f * u2);
+      const float rad = sqrtf(-2.f * __logf(u1));
+      float sn, cs;
+      __sincosf(6.2831853071795865f * u2 - 3.14159265358979323f, &sn, &cs);
+      float* e = eps + r * D.out + 2 * q;
+      e[0] = rad * cs;
+      if (2 * q + 1 < D.out) e[1] = rad * sn;
     }
   };
   run_net(D, P, wsm, xb0, xb1, sh, wphase, mphase, tid, stream, NT, noise);
@@ -434,7 +510,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // memory (the operand buffers are free once the last MMA completed), then
     // every thread takes consecutive tile elements, so the mean / action
     // stores are coalesced; the log-prob terms replace the means in place and
-    // each environment's row is summed in column order by one thread
+    // each environment's row is summed by 8 threads (columns j, j+8, ..., then
+    // a fixed shuffle tree: deterministic)
     const int out = D.out;
     float* tile = reinterpret_cast<float*>(base);
     for (int u = wq; u < nch * ((out + 31) / 32); u += 4) {
@@ -458,15 +535,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (act_out) {
         const float ep = eps[i];  // drawn during the MMAs (same [env][out] indexing)
         act_out[g0 + i] = m + sh->sdv[c] * ep;
-        tile[i] = -0.5f * ep * ep - log_std[c] - 0.91893853320467274f;
+        tile[i] = -0.5f * ep * ep - sh->lsd[c] - 0.91893853320467274f;
       }
     }
     __syncthreads();
-    if (logp_out && tid < rows) {
+    if (logp_out) {
+      static_assert(kThreads >= 8 * kMaxNT, "8 threads per environment");
+      const int r = tid >> 3, j = tid & 7;
       float lp = 0.f;
-      if (act_out)
-        for (int c = 0; c < out; ++c) lp += tile[tid * out + c];
-      logp_out[tile0 + tid] = lp;
+      if (act_out && r < rows)
+        for (int c = j; c < out; c += 8) lp += tile[r * out + c];
+      lp += __shfl_xor_sync(0xffffffffu, lp, 4);
+      lp += __shfl_xor_sync(0xffffffffu, lp, 2);
+      lp += __shfl_xor_sync(0xffffffffu, lp, 1);
+      if (j == 0 && r < rows) logp_out[tile0 + r] = lp;
     }
   } else if (sp == 0 && wq < nch) {
     float v[16];
@@ -591,11 +673,27 @@ extern "C" int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_
     if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_policy_mlp attr: ") + cudaGetErrorString(e));
     if (dev >= 0 && dev < 64) configured[dev] = smem;
   }
-  const dim3 grid((n_envs + NT - 1) / NT, nets);
-  k_policy_mlp<<<grid, kThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
-      obs, n_envs, obs_dim, obs_mean, obs_std, Dpi, Ppi, Dv, Pv, log_std, seed, step, env_offset, mean_out,
-      action_out, logp_out, value_out, x0, x1, wbuf, NT, eps_elems);
-  const cudaError_t e = cudaGetLastError();
+  // programmatic dependent launch: the prologue (barriers, TMEM, weight TMA)
+  // overlaps the tail of the preceding grid when that grid triggers early
+  // (the step kernel, K4); STP_PDL=0 launches plainly (A/B timing)
+  static const bool pdl = [] {
+    const char* v = getenv("STP_PDL");
+    return !(v && v[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((n_envs + NT - 1) / NT, nets);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_policy_mlp, obs, n_envs, obs_dim, obs_mean, obs_std, Dpi, Ppi, Dv, Pv,
+                                     log_std, seed, step, (long long)env_offset, mean_out, action_out, logp_out,
+                                     value_out, x0, x1, wbuf, NT, eps_elems);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_policy_mlp: ") + cudaGetErrorString(e));
   return STP_OK;
 }

@@ -436,6 +436,10 @@ constexpr int kXch = kXchEntries;  // per-lane exchange entries (Mi is the large
 template <class T, int W, int CPB, bool ISL = false, bool DBG = false>
 __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
     k_env_step(const KArgs<T> a) {
+  // a grid launched after this one with programmatic stream serialization (the
+  // policy forward K4) may start its parameter-only prologue on SMs this grid
+  // frees; it waits for this grid's completion before touching its outputs
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   // env / island selection.  Island mode: big islands (isl_big_mode) are
   // consecutive CTAs of a cooperative launch; islands of <= cap envs are taken
   // round-robin by a persistent grid (isl_next), each CTA looping over them.

@@ -178,12 +178,20 @@ def _mix64(z):
 
 
 def kernel_noise(seed: int, env: int, step: int, act_dim: int) -> np.ndarray:
+    """The policy noise of K4 (policy_mlp.cu, noise lambda): Box-Muller pairs,
+    one splitmix64 hash per pair of actions q = 0, 1, ...: u1 = bits 40-63,
+    u2 = bits 16-39 (24-bit uniforms), r = sqrt(-2 ln max(u1, 1e-7)),
+    theta = 2 pi u2 - pi; eps[2q] = r cos(theta), eps[2q + 1] = r sin(theta)."""
     s = _mix64(_mix64(_mix64(seed) ^ 6) ^ ((env << 32) | (step & 0xFFFFFFFF)))
     out = np.zeros(act_dim, np.float32)
-    for c in range(act_dim):
-        z = _mix64((s + c) & 0xFFFFFFFFFFFFFFFF)  # one hash per element: bits 40-63 and 16-39
+    for q in range((act_dim + 1) // 2):
+        z = _mix64((s + q) & 0xFFFFFFFFFFFFFFFF)
         u1 = np.float32((z >> 40) * (1.0 / 16777216.0))
         u2 = np.float32(((z >> 16) & 0xFFFFFF) * (1.0 / 16777216.0))
         u1 = max(u1, np.float32(1e-7))
-        out[c] = math.sqrt(-2.0 * math.log(u1)) * math.cos(2 * math.pi * u2)
+        rad = math.sqrt(-2.0 * math.log(u1))
+        th = 2 * math.pi * float(u2) - math.pi
+        out[2 * q] = rad * math.cos(th)
+        if 2 * q + 1 < act_dim:
+            out[2 * q + 1] = rad * math.sin(th)
     return out

@@ -11,10 +11,17 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-SO = os.path.join(ROOT, "tools", "exp", "_k4phase.so")
+SO = os.environ.get("K4SO", os.path.join(ROOT, "tools", "exp", "_k4phase.so"))
 OLD = os.path.join(ROOT, "tools", "exp", "_k4old.so")
-NAMES = {0: "start", 1: "tmem alloc", 11: "obs landed", 2: "obs prologue", 3: "weights landed", 4: "mma L0", 5: "epi L0",
-         6: "mma L1", 7: "epi L1", 8: "mma L2", 9: "epi L2", 10: "mma L3", 12: "head + end"}
+NAMES = {0: "start", 1: "prologue sync", 11: "obs landed", 2: "obs prologue", 3: "weights landed", 4: "mma L0",
+         5: "epi L0", 6: "mma L1", 7: "epi L1", 8: "mma L2", 9: "epi L2", 10: "mma L3", 12: "head + end"}
+for _l in range(4):
+    NAMES[13 + _l] = f"sync L{_l}"
+    NAMES[17 + _l] = f"issued L{_l}"
+    NAMES[21 + _l] = f"noise L{_l}"
+ORDER = [1, 11, 2, 3, 13, 17, 21, 4, 5, 14, 18, 22, 6, 7, 15, 19, 23, 8, 9, 16, 20, 24, 10, 12]
+KP = 32
+CLK_GHZ = float(os.environ.get("CLK_GHZ", "1.965"))
 
 
 def build():
@@ -64,15 +71,19 @@ def run():
     torch.cuda.synchronize()
     nt = 64 if (n + 63) // 64 * 2 >= 120 else 32 if (n + 31) // 32 * 2 >= 120 else 16  # stp_policy_forward's NT
     ctas = 2 * ((n + nt - 1) // nt)
-    buf = np.zeros(ctas * 16, dtype=np.uint64)
+    buf = np.zeros(ctas * KP, dtype=np.uint64)
     lib.stp_k4_phases(buf.ctypes.data, buf.size)
-    t = buf.reshape(ctas, 16).astype(np.int64)
-    t0 = t[:, 0].min()
-    print(f"{ctas} CTAs; launch spread {(t[:, 0].max() - t0) / 1e3:.2f} us; "
-          f"kernel span {(t[:, 12].max() - t0) / 1e3:.2f} us")
+    t = buf.reshape(ctas, KP).astype(np.int64)
+    g0 = t[:, 31].min()
+    span = (t[:, 12] - t[:, 0]) / CLK_GHZ / 1e3 + (t[:, 31] - g0) / 1e3
+    print(f"{ctas} CTAs; launch spread {(t[:, 31].max() - g0) / 1e3:.2f} us; "
+          f"kernel span {span.max():.2f} us (SM clock at {CLK_GHZ} GHz; CTA body median "
+          f"{np.median((t[:, 12] - t[:, 0]) / CLK_GHZ / 1e3):.2f} us)")
     prev = 0
-    for i in [1, 11, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12]:
-        d = (t[:, i] - t[:, prev]) / 1e3
+    for i in ORDER:
+        if i in (17, 18, 19, 20):  # thread 0 only; others wait at the mma barrier
+            pass
+        d = (t[:, i] - t[:, prev]) / CLK_GHZ / 1e3
         print(f"  {NAMES[prev]:>15} -> {NAMES[i]:<15} median {np.median(d):7.2f} us  max {d.max():7.2f} us"
               f"   (policy {np.median(d[: ctas // 2]):6.2f}, value {np.median(d[ctas // 2:]):6.2f})")
         prev = i
