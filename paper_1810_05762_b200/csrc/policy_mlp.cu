@@ -245,12 +245,9 @@ constexpr int kTmemCols = 2 * kMaxNT;  // two M blocks x NT accumulator columns
 
 // One 4-layer net over the CTA's NT environments; B operand of layer 0 already
 // in xb0.  Returns with the last layer's accumulator (rows = outputs) in TMEM.
-// bg(l) runs on every thread while layer l's MMAs execute (work that does
-// not depend on the net: the policy noise).
-template <class BG>
-__device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4], __nv_bfloat16* xb0,
+__device__ __forceinline__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4], __nv_bfloat16* xb0,
                         __nv_bfloat16* xb1, Smem* sh, uint32_t& wphase, uint32_t& mphase, int tid, bool stream,
-                        int NT, BG&& bg) {
+                        int NT) {
   const int warp = tid >> 5, lane = tid & 31;
   const int sp = warp & 3;   // TMEM subpartition: lanes 32 sp ..
   const int wq = warp >> 2;  // 0..3: unit phase within the subpartition
@@ -311,7 +308,6 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
       umma_commit(&sh->bar_mma);
       phase(17 + l);
     }
-    bg(l);
     phase(21 + l);
     mbar_wait(&sh->bar_mma, mphase);
     mphase ^= 1;
@@ -329,6 +325,7 @@ __device__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4
       const float bias = h < D.n[l] ? sh->bias[l][h] : 0.f;
       float v[16];
       tmem_ld16(sh->tmem + (uint32_t(sp * 32) << 16) + uint32_t(mb * NT + ch * 16), v);
+      if (l == 0 && u == wq) phase(28);
       selu16(v, bias);
       if (h < kout) {
         st_xt(x_out, kout, h, ch * 16, v);
@@ -416,6 +413,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       sh->streams[r] = stp_derive_seed(seed, 6 /* policy noise */, (uint64_t(env_offset + tile0 + r) << 32) |
                                                                        uint32_t(step));
   }
+  // policy noise [env][out] into shared memory, before the dependency wait
+  // (it reads only the seed / step / env ids and log_std): Box-Muller pairs
+  // (both the cosine and the sine branch) on two 24-bit counter-based
+  // uniforms of one 64-bit hash per pair of actions, fast log / sincos on
+  // [-pi, pi) (|err| ~1e-6)
+  if (!value_net && act_out) {
+    __syncthreads();  // streams
+    for (int c = tid; c < D.out; c += kThreads) {
+      const float ls = log_std[c];
+      sh->lsd[c] = ls;
+      sh->sdv[c] = expf(ls);
+    }
+    const int npair = (D.out + 1) / 2;
+    for (int i = tid; i < rows * npair; i += kThreads) {
+      const int r = i / npair, q = i - r * npair;
+      const uint64_t z = stp_mix64(sh->streams[r] + uint64_t(q));  // bits 40-63: u1, 16-39: u2
+      const float u1 = fmaxf(float(z >> 40) * (1.f / 16777216.f), 1e-7f);
+      const float u2 = float((z >> 16) & 0xffffffu) * (1.f / 16777216.f);
+      const float rad = sqrtf(-2.f * __logf(u1));
+      float sn, cs;
+      __sincosf(6.2831853071795865f * u2 - 3.14159265358979323f, &sn, &cs);
+      float* e = eps + r * D.out + 2 * q;
+      e[0] = rad * cs;
+      if (2 * q + 1 < D.out) e[1] = rad * sn;
+    }
+  }
   griddep_wait();
   griddep_launch_dependents();
   if (warp == 1 && elect_one()) {  // observation tile + statistics (+ streaming mode: biases) on bar_obs
@@ -474,44 +497,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   phase(2);
   uint32_t wphase = 0, mphase = 0;
-  // policy noise: Box-Muller pairs (both the cosine and the sine branch) on
-  // two 24-bit counter-based uniforms of one 64-bit hash per pair of
-  // actions, fast log / sincos on [-pi, pi) (|err| ~1e-6), in four slices
-  // drawn while the four layers' MMAs run
-  const bool draw = !value_net && act_out;
-  const int npair = (D.out + 1) / 2;
-  const int n_pairs = draw ? rows * npair : 0;
-  auto noise = [&](int l) {
-    if (l == 0 && draw)  // exp(log_std) (a global load: off the prologue's critical path)
-      for (int c = tid; c < D.out; c += kThreads) {
-        const float ls = log_std[c];
-        sh->lsd[c] = ls;
-        sh->sdv[c] = expf(ls);
-      }
-    const int p0 = n_pairs * l / 4, p1 = n_pairs * (l + 1) / 4;
-    for (int i = p0 + tid; i < p1; i += kThreads) {
-      const int r = i / npair, q = i - r * npair;
-      const uint64_t z = stp_mix64(sh->streams[r] + uint64_t(q));  // bits 40-63: u1, 16-39: u2
-      const float u1 = fmaxf(float(z >> 40) * (1.f / 16777216.f), 1e-7f);
-      const float u2 = float((z >> 16) & 0xffffffu) * (1.f / 16777216.f);
-      const float rad = sqrtf(-2.f * __logf(u1));
-      float sn, cs;
-      __sincosf(6.2831853071795865f * u2 - 3.14159265358979323f, &sn, &cs);
-      float* e = eps + r * D.out + 2 * q;
-      e[0] = rad * cs;
-      if (2 * q + 1 < D.out) e[1] = rad * sn;
-    }
-  };
-  run_net(D, P, wsm, xb0, xb1, sh, wphase, mphase, tid, stream, NT, noise);
+  run_net(D, P, wsm, xb0, xb1, sh, wphase, mphase, tid, stream, NT);
   // last layer: TMEM lane = output, columns = environments
   const int sp = warp & 3, wq = warp >> 2, nch = NT / 16;
   if (!value_net) {
     // policy head: the mean tile [env][out] through shared
     // memory (the operand buffers are free once the last MMA completed), then
-    // every thread takes consecutive tile elements, so the mean / action
-    // stores are coalesced; the log-prob terms replace the means in place and
-    // each environment's row is summed by 8 threads (columns j, j+8, ..., then
-    // a fixed shuffle tree: deterministic)
+    // 8 threads per environment write its mean / action row (8 consecutive
+    // columns per pass) and sum its log-prob terms
     const int out = D.out;
     float* tile = reinterpret_cast<float*>(base);
     for (int u = wq; u < nch * ((out + 31) / 32); u += 4) {
@@ -526,25 +519,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 16; ++i) tile[(ch * 16 + i) * out + c] = v[i] + bias;
       }
     }
+    phase(25);
     __syncthreads();
-    const size_t g0 = size_t(tile0) * out;
-    for (int i = tid; i < rows * out; i += kThreads) {
-      const int r = i / out, c = i - r * out;
-      const float m = tile[i];
-      mu_out[g0 + i] = m;
-      if (act_out) {
-        const float ep = eps[i];  // drawn during the MMAs (same [env][out] indexing)
-        act_out[g0 + i] = m + sh->sdv[c] * ep;
-        tile[i] = -0.5f * ep * ep - sh->lsd[c] - 0.91893853320467274f;
+    phase(26);
+    // 8 threads per environment: columns j, j + 8, ...; the log-prob terms
+    // summed in that order, then a fixed shuffle tree (deterministic)
+    static_assert(kThreads >= 8 * kMaxNT, "8 threads per environment");
+    const int r = tid >> 3, j = tid & 7;
+    float lp = 0.f;
+    if (r < rows)
+      for (int c = j; c < out; c += 8) {
+        const float m = tile[r * out + c];
+        const size_t g = (size_t(tile0) + r) * out + c;
+        mu_out[g] = m;
+        if (act_out) {
+          const float ep = eps[r * out + c];  // drawn in the prologue (same [env][out] indexing)
+          act_out[g] = m + sh->sdv[c] * ep;
+          lp += -0.5f * ep * ep - sh->lsd[c] - 0.91893853320467274f;
+        }
       }
-    }
-    __syncthreads();
+    phase(27);
     if (logp_out) {
-      static_assert(kThreads >= 8 * kMaxNT, "8 threads per environment");
-      const int r = tid >> 3, j = tid & 7;
-      float lp = 0.f;
-      if (act_out && r < rows)
-        for (int c = j; c < out; c += 8) lp += tile[r * out + c];
       lp += __shfl_xor_sync(0xffffffffu, lp, 4);
       lp += __shfl_xor_sync(0xffffffffu, lp, 2);
       lp += __shfl_xor_sync(0xffffffffu, lp, 1);

@@ -19,7 +19,8 @@ for _l in range(4):
     NAMES[13 + _l] = f"sync L{_l}"
     NAMES[17 + _l] = f"issued L{_l}"
     NAMES[21 + _l] = f"noise L{_l}"
-ORDER = [1, 11, 2, 3, 13, 17, 21, 4, 5, 14, 18, 22, 6, 7, 15, 19, 23, 8, 9, 16, 20, 24, 10, 12]
+NAMES.update({25: "head tile", 26: "head sync", 27: "head rows", 28: "L0 first tmem ld"})
+ORDER = [1, 11, 2, 3, 13, 17, 21, 4, 28, 5, 14, 18, 22, 6, 7, 15, 19, 23, 8, 9, 16, 20, 24, 10, 25, 26, 27, 12]
 KP = 32
 CLK_GHZ = float(os.environ.get("CLK_GHZ", "1.965"))
 
