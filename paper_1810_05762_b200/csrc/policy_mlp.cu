@@ -245,7 +245,7 @@ constexpr int kTmemCols = 2 * kMaxNT;  // two M blocks x NT accumulator columns
 
 // One 4-layer net over the CTA's NT environments; B operand of layer 0 already
 // in xb0.  Returns with the last layer's accumulator (rows = outputs) in TMEM.
-__device__ __forceinline__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wsm[4], __nv_bfloat16* xb0,
+__device__ __forceinline__ void run_net(const MlpDims& D, const NetPtrs& P, __nv_bfloat16* wbase, __nv_bfloat16* xb0,
                         __nv_bfloat16* xb1, Smem* sh, uint32_t& wphase, uint32_t& mphase, int tid, bool stream,
                         int NT) {
   const int warp = tid >> 5, lane = tid & 31;
@@ -260,6 +260,7 @@ __device__ __forceinline__ void run_net(const MlpDims& D, const NetPtrs& P, __nv
   __nv_bfloat16* x_in = xb0;
   __nv_bfloat16* x_out = xb1;
   const uint32_t idesc = umma_idesc(kM, NT);
+  uint32_t woff = 0;  // byte offset of layer l's resident weights
   for (int l = 0; l < 4; ++l) {
     const int mblocks = (D.n[l] + kM - 1) / kM;
     fence_async_smem();  // generic-proxy operand writes -> visible to the tensor core
@@ -285,7 +286,7 @@ __device__ __forceinline__ void run_net(const MlpDims& D, const NetPtrs& P, __nv
         }
       };
       if (!stream) {
-        issue(smem_u32(wsm[l]), 0, D.k[l] / 16, 0);
+        issue(smem_u32(wbase) + woff, 0, D.k[l] / 16, 0);
       } else {
         // K blocks [kb0, kb0 + nb) of the packed [k/8][n][8] weight are one
         // contiguous range: stage it, accumulate its MMAs, free the buffer
@@ -294,10 +295,10 @@ __device__ __forceinline__ void run_net(const MlpDims& D, const NetPtrs& P, __nv
           const int nb = min(kbc, kbt - kb0);
           const uint32_t bytes = uint32_t(nb) * 8 * D.n[l] * 2;
           mbar_expect_tx(&sh->bar_w, bytes);
-          bulk_g2s(wsm[0], P.w[l] + size_t(kb0) * 8 * D.n[l], bytes, &sh->bar_w);
+          bulk_g2s(wbase, P.w[l] + size_t(kb0) * 8 * D.n[l], bytes, &sh->bar_w);
           mbar_wait(&sh->bar_w, wphase);
           wphase ^= 1;
-          issue(smem_u32(wsm[0]), 0, nb / 2, kb0 / 2);
+          issue(smem_u32(wbase), 0, nb / 2, kb0 / 2);
           if (kb0 + nb < kbt) {
             umma_commit(&sh->bar_chunk);
             mbar_wait(&sh->bar_chunk, cphase);
@@ -308,6 +309,7 @@ __device__ __forceinline__ void run_net(const MlpDims& D, const NetPtrs& P, __nv
       umma_commit(&sh->bar_mma);
       phase(17 + l);
     }
+    woff += uint32_t(D.k[l]) * D.n[l] * 2;
     phase(21 + l);
     mbar_wait(&sh->bar_mma, mphase);
     mphase ^= 1;
@@ -364,12 +366,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const MlpDims& D = value_net ? Dv : Dpi;
   const NetPtrs& P = value_net ? Pv : Ppi;
 
-  __nv_bfloat16* wsm[4];
-  int off = 0;
-  for (int l = 0; l < 4; ++l) {
-    wsm[l] = wbase + off;
-    off += D.k[l] * D.n[l];
-  }
   // The tile's observation rows are one contiguous block of global memory,
   // staged into the (still unused) layer-1 operand buffer by one TMA bulk copy
   // when its size and address allow (issued first, then the 4 weight blobs, all
@@ -400,7 +396,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int l = 0; l < 4; ++l) bytes += uint32_t(D.k[l]) * D.n[l] * 2 + uint32_t(D.n[l]) * 4;
       mbar_expect_tx(&sh->bar_w, bytes);
       for (int l = 0; l < 4; ++l) bulk_g2s(sh->bias[l], P.bias[l], uint32_t(D.n[l]) * 4, &sh->bar_w);
-      for (int l = 0; l < 4; ++l) bulk_g2s(wsm[l], P.w[l], uint32_t(D.k[l]) * D.n[l] * 2, &sh->bar_w);
+      for (int l = 0, off = 0; l < 4; off += D.k[l] * D.n[l], ++l)
+        bulk_g2s(wbase + off, P.w[l], uint32_t(D.k[l]) * D.n[l] * 2, &sh->bar_w);
     }
   }
   if (warp == 0) {  // TMEM: two M blocks x NT columns
@@ -497,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   phase(2);
   uint32_t wphase = 0, mphase = 0;
-  run_net(D, P, wsm, xb0, xb1, sh, wphase, mphase, tid, stream, NT);
+  run_net(D, P, wbase, xb0, xb1, sh, wphase, mphase, tid, stream, NT);
   // last layer: TMEM lane = output, columns = environments
   const int sp = warp & 3, wq = warp >> 2, nch = NT / 16;
   if (!value_net) {
