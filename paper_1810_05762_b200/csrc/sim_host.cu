@@ -408,7 +408,11 @@ int launch_t(stp_sim* s, int mode, const float* torques, const float* actions, f
     CK(cudaEventCreateWithFlags(&s->isl.fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&s->isl.join, cudaEventDisableTiming));
   }
-  const cudaError_t e = stp::launch_env_step<T>(a, s->W, s->cpb, st, a.merged ? &s->isl : nullptr);
+  static const bool side = [] {  // STP_ISL_SIDE=0: island launches in order on the caller's stream (A/B)
+    const char* v = getenv("STP_ISL_SIDE");
+    return !(v && v[0] == '0');
+  }();
+  const cudaError_t e = stp::launch_env_step<T>(a, s->W, s->cpb, st, a.merged && side ? &s->isl : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "k_env_step launch");
   return STP_OK;
 }

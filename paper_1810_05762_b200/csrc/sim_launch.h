@@ -2,6 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 #include "sim_kernels.cuh"
 
 namespace stp {
@@ -28,6 +31,39 @@ inline bool first_on_device(bool (&done)[64]) {
   done[d] = true;
   return true;
 }
+
+// Programmatic dependent launch along a stream's chain of dependent kernels
+// (the inter-agent pre-step kernels, the step kernel, K4): a kernel launched
+// with launch_pdl may be scheduled while its predecessor drains; it runs
+// pdl_wait() before touching anything the predecessor writes, and
+// pdl_trigger() so its own successor can be scheduled early.  Both are no-ops
+// for a plain launch.  STP_PDL=0 launches plainly (A/B timing).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("STP_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+#endif
 
 // Global scratch rows per lane of every env (sim_step.cuh: G_QH, G_HD, G_LC,
 // then 12 overflow contact slots of 11 rows for the terrain instantiation,

@@ -138,12 +138,29 @@ __device__ __forceinline__ void shapes_of_env(const DevModel<T>* __restrict__ Mp
   }
 }
 
+// one launch zeroing the step's counters and the hash-bin counts (was four
+// cudaMemsetAsync operations, each a separate ~2-3 us item on the stream)
+__global__ void k_pairs_reset(int* __restrict__ bin_count, int nbins, int* __restrict__ gcnt,
+                              int* __restrict__ counters, int* __restrict__ icnt) {
+  pdl_wait();  // programmatic dependent launch (sim_launch.h)
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nbins) bin_count[i] = 0;
+  if (i < 2) {
+    gcnt[i] = 0;
+    counters[i] = 0;
+  }
+  if (icnt && i < 3) icnt[i] = 0;
+}
+
 template <class T>
 __global__ void k_shapes_warp(const DevModel<T>* __restrict__ Mp, const T* __restrict__ state,
                               const double* __restrict__ origin, int n, int W, WShape* __restrict__ ws,
                               double* __restrict__ env_box, int2* __restrict__ env_cell, int* __restrict__ bin_count,
                               int* __restrict__ bins, unsigned hmask, int* __restrict__ ovf, int* __restrict__ n_ovf,
                               int* __restrict__ max_ext_bits, int* __restrict__ xcount) {
+  pdl_wait();  // programmatic dependent launch (sim_launch.h)
+  pdl_trigger();
   // the warp's shapes are staged in shared memory and written out as
   // coalesced 8-byte words (one 136-byte struct per lane would scatter)
   __shared__ WShape stage[4][32];  // launched with 128 threads
@@ -164,6 +181,8 @@ __global__ void k_env_query(int n, const double* __restrict__ env_box, const int
                             const int* __restrict__ ovf, const int* __restrict__ n_ovf,
                             const int* __restrict__ max_ext_bits, double margin, int2* __restrict__ pairs, int cap,
                             int* __restrict__ n_pairs) {
+  pdl_wait();  // programmatic dependent launch (sim_launch.h)
+  pdl_trigger();
   // one warp per env; lanes over (cell, bin slot) candidates
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= n) return;
@@ -309,6 +328,8 @@ __global__ void k_narrow_slots(const int2* __restrict__ pairs, const int* __rest
                                int B, long long NB, const WShape* __restrict__ ws, double margin,
                                XSlot* __restrict__ xslots, int* __restrict__ xcount, int2* __restrict__ edges,
                                int edge_cap, int* __restrict__ n_edges, int* __restrict__ err) {
+  pdl_wait();  // programmatic dependent launch (sim_launch.h)
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int np = min(*n_pairs_p, pair_cap);
@@ -380,6 +401,8 @@ __global__ void k_islands(int n, const int2* __restrict__ edges, const int* __re
                           int labels_in_smem, int cap, int max_parts, int* __restrict__ big_count,
                           int* __restrict__ big_off, int* __restrict__ big_size, int* __restrict__ big_fill,
                           int* __restrict__ big_members, int* __restrict__ big_bar) {
+  pdl_wait();  // programmatic dependent launch (sim_launch.h)
+  pdl_trigger();
   extern __shared__ int slab[];
   __shared__ int changed, any_big;
   int* L = labels_in_smem ? slab : label;
@@ -539,19 +562,18 @@ void pair_scratch_free(PairScratch* p) {
 // current state into P->pairs / P->counters[0]; world shapes into P->ws
 template <class T>
 static cudaError_t broadphase(PairScratch* P, const DevModel<T>* model, const T* state, const double* origin, int n,
-                              int W, double margin, cudaStream_t st, int* xcount = nullptr) {
-  cudaError_t e = cudaMemsetAsync(P->bin_count, 0, sizeof(int) * (P->hmask + 1), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(P->gcnt, 0, sizeof(int) * 2, st);
+                              int W, double margin, cudaStream_t st, int* xcount = nullptr, int* icnt = nullptr) {
+  const int nbins = int(P->hmask + 1);
+  cudaError_t e = launch_pdl(k_pairs_reset, dim3((nbins + 255) / 256), dim3(256), 0, st, P->bin_count, nbins, P->gcnt,
+                             P->counters, icnt);
   if (e != cudaSuccess) return e;
-  k_shapes_warp<T><<<(n * 32 + 127) / 128, 128, 0, st>>>(model, state, origin, n, W, P->ws, P->env_box, P->env_cell,
-                                                         P->bin_count, P->bins, P->hmask, P->ovf, P->gcnt,
-                                                         P->gcnt + 1, xcount);
-  e = cudaGetLastError();
+  e = launch_pdl(k_shapes_warp<T>, dim3((n * 32 + 127) / 128), dim3(128), 0, st, model, state, origin, n, W, P->ws,
+                 P->env_box, P->env_cell, P->bin_count, P->bins, P->hmask, P->ovf, P->gcnt, P->gcnt + 1, xcount);
   if (e != cudaSuccess) return e;
-  k_env_query<<<(n * 32 + 127) / 128, 128, 0, st>>>(n, P->env_box, P->env_cell, P->bin_count, P->bins, P->hmask, P->ovf,
-                                               P->gcnt, P->gcnt + 1, margin, P->pairs, int(P->pair_cap),
-                                               P->counters);
-  return cudaGetLastError();
+  return launch_pdl(k_env_query, dim3((n * 32 + 127) / 128), dim3(128), 0, st, n, (const double*)P->env_box,
+                    (const int2*)P->env_cell, (const int*)P->bin_count, (const int*)P->bins, P->hmask,
+                    (const int*)P->ovf, (const int*)P->gcnt, (const int*)(P->gcnt + 1), margin, P->pairs,
+                    int(P->pair_cap), P->counters);
 }
 
 template <class T>
@@ -595,7 +617,6 @@ cudaError_t detect_pairs(PairScratch*& P, const DevModel<T>* model, int B, const
     STP_CK(cudaMalloc(&P->ovf, sizeof(int) * n));
     STP_CK(cudaMalloc(&P->gcnt, sizeof(int) * 2));
   }
-  STP_CK(cudaMemsetAsync(P->counters, 0, sizeof(int) * 2, st));
   STP_CK(broadphase<T>(P, model, state, origin, n, W, margin, st));
   int h_cnt[2] = {0, 0};
   STP_CK(cudaMemcpyAsync(h_cnt, P->counters, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -681,12 +702,9 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
     STP_CK(cudaMalloc(&P->big_xch, sizeof(double) * kBigStride * size_t(n)));
   }
   const int edge_cap = n * B * kXSlots;
-  STP_CK(cudaMemsetAsync(P->counters, 0, sizeof(int) * 2, st));
-  STP_CK(cudaMemsetAsync(P->icnt, 0, sizeof(int) * 3, st));
-  STP_CK(broadphase<T>(P, model, state, origin, n, W, margin, st, P->xcount));
-  k_narrow_slots<<<148 * 2, 256, 0, st>>>(P->pairs, P->counters, int(P->pair_cap), B, (long long)n * B, P->ws, margin,
-                                          P->xslots, P->xcount, P->edges, edge_cap, P->icnt, P->icnt + 2);
-  STP_CK(cudaGetLastError());
+  STP_CK(broadphase<T>(P, model, state, origin, n, W, margin, st, P->xcount, P->icnt));
+  STP_CK(launch_pdl(k_narrow_slots, dim3(148 * 2), dim3(256), 0, st, P->pairs, P->counters, int(P->pair_cap), B,
+                    (long long)n * B, P->ws, margin, P->xslots, P->xcount, P->edges, edge_cap, P->icnt, P->icnt + 2));
   // labels in shared memory up to 48K envs (192 KB), else in global scratch
   const size_t lab_bytes = size_t(n) * sizeof(int);
   const bool lab_smem = lab_bytes <= 192 * 1024;
@@ -694,11 +712,10 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
   if (lab_smem && lab_bytes > 48 * 1024 && first_on_device(lab_attr))
     STP_CK(cudaFuncSetAttribute(k_islands, cudaFuncAttributeMaxDynamicSharedMemorySize, int(192 * 1024)));
   int* bg = P->big;
-  k_islands<<<1, 1024, lab_smem ? lab_bytes : 0, st>>>(
-      n, P->edges, P->icnt, edge_cap, P->label, P->merged, P->isl_of, P->isl_size, P->isl_fill, P->isl_big,
-      P->isl_members, P->icnt + 1, P->icnt + 2, int(lab_smem), cap, max_parts, bg, bg + 1, bg + 1 + kBigIslands,
-      bg + 1 + 2 * kBigIslands, P->big_members, bg + 1 + 3 * kBigIslands);
-  STP_CK(cudaGetLastError());
+  STP_CK(launch_pdl(k_islands, dim3(1), dim3(1024), lab_smem ? lab_bytes : 0, st, n, P->edges, P->icnt, edge_cap,
+                    P->label, P->merged, P->isl_of, P->isl_size, P->isl_fill, P->isl_big, P->isl_members,
+                    P->icnt + 1, P->icnt + 2, int(lab_smem), cap, max_parts, bg, bg + 1, bg + 1 + kBigIslands,
+                    bg + 1 + 2 * kBigIslands, P->big_members, bg + 1 + 3 * kBigIslands));
   view->merged = P->merged;
   view->isl_members = P->isl_members;
   view->isl_count = P->icnt + 1;

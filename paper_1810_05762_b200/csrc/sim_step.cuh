@@ -436,10 +436,12 @@ constexpr int kXch = kXchEntries;  // per-lane exchange entries (Mi is the large
 template <class T, int W, int CPB, bool ISL = false, bool DBG = false>
 __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
     k_env_step(const KArgs<T> a) {
-  // a grid launched after this one with programmatic stream serialization (the
-  // policy forward K4) may start its parameter-only prologue on SMs this grid
-  // frees; it waits for this grid's completion before touching its outputs
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  // programmatic dependent launch (sim_launch.h): when launched early behind
+  // the inter-agent pre-step kernels (or K4), wait for them first; a grid
+  // launched after this one (K4, the next step's pre-step kernels) may start
+  // its own prologue on the SMs this grid frees
+  pdl_wait();
+  pdl_trigger();
   // env / island selection.  Island mode: big islands (isl_big_mode) are
   // consecutive CTAs of a cooperative launch; islands of <= cap envs are taken
   // round-robin by a persistent grid (isl_next), each CTA looping over them.
@@ -2261,8 +2263,7 @@ static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
   }
   const long long total = (long long)(a.n - a.e_begin) * W;
   const int blocks = int((total + threads - 1) / threads);
-  k_env_step<T, W, CPB, false, DBG><<<blocks, threads, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_env_step<T, W, CPB, false, DBG>, dim3(blocks), dim3(threads), smem, s, a);
 }
 
 template <class T, int CPB>
