@@ -26,8 +26,8 @@ def main():
     args = ap.parse_args()
     steps = 60 if args.quick else 500
     t0 = time.time()
-    rep = {"kernel_build": subprocess.run(["git", "rev-parse", "--short", "HEAD"], cwd=ROOT, capture_output=True,
-                                          text=True).stdout.strip() or None,
+    rep = {"kernel_build": os.environ.get("STP_BUILD") or subprocess.run(
+               ["git", "rev-parse", "--short", "HEAD"], cwd=ROOT, capture_output=True, text=True).stdout.strip() or None,
            "protocols": {}}
     P = rep["protocols"]
     P["reward_independent_oracle_humanoid"] = parity.reward_vs_independent_oracle("humanoid")
