@@ -404,7 +404,15 @@ int launch_t(stp_sim* s, int mode, const float* torques, const float* actions, f
     a.big_xch = reinterpret_cast<T*>(v.big_xch);
   }
   if (a.merged && !s->isl.side) {
-    CK(cudaStreamCreateWithFlags(&s->isl.side, cudaStreamNonBlocking));
+    // the highest stream priority: island CTAs (long, latency-bound chains of a
+    // few warps) get SMs before the main launch fills the machine instead of
+    // waiting for its last wave to drain (crowded HFH rollout: 0.380 -> 0.361
+    // ms per step; uncrowded steps unchanged)
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&s->isl.side, cudaStreamNonBlocking, hi));
+    CK(cudaMallocHost(&s->isl.h_count, sizeof(int)));
+    s->isl.h_count[0] = a.n;  // first step: no hint (grid min(n / 2, SMs))
     CK(cudaEventCreateWithFlags(&s->isl.fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&s->isl.join, cudaEventDisableTiming));
   }
@@ -626,6 +634,7 @@ void stp_destroy(stp_sim* s) {
   if (s->ev_in) cudaEventDestroy(s->ev_in);
   if (s->isl.side) {
     cudaStreamSynchronize(s->isl.side);
+    if (s->isl.h_count) cudaFreeHost(s->isl.h_count);
     cudaStreamDestroy(s->isl.side);
     cudaEventDestroy(s->isl.fork);
     cudaEventDestroy(s->isl.join);

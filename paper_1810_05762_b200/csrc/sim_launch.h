@@ -79,8 +79,12 @@ constexpr int kScratchRows = 55 + 11 * kSpillSlots + kXSlotRows * kXSlots;
 // side stream + fork / join events of a handle with inter-agent collisions:
 // the island launches run concurrently with the main step launch
 struct IslandStreams {
-  cudaStream_t side;
+  cudaStream_t side;  // highest stream priority: island CTAs get SMs before the main launch
   cudaEvent_t fork, join;
+  // pinned host copy of the previous step's island count (written by an async
+  // copy on `side`, read without a sync): sizes the persistent island grid.
+  // Only a hint: the grid loops over however many islands there are.
+  int* h_count;
 };
 template <class T>
 cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t s,

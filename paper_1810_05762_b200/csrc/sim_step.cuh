@@ -2252,7 +2252,7 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
 }
 
 template <class T, int W, int CPB, bool DBG = false>
-static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
+static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s, bool pdl = true) {
   constexpr int threads = kStepThreads;
   const size_t smem = size_t(threads / 32) * smem_rows<CPB>() * 32 * sizeof(T);
   static bool configured[64] = {};
@@ -2263,6 +2263,10 @@ static cudaError_t launch_one(const KArgs<T>& a, cudaStream_t s) {
   }
   const long long total = (long long)(a.n - a.e_begin) * W;
   const int blocks = int((total + threads - 1) / threads);
+  if (!pdl) {
+    k_env_step<T, W, CPB, false, DBG><<<blocks, threads, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   return launch_pdl(k_env_step<T, W, CPB, false, DBG>, dim3(blocks), dim3(threads), smem, s, a);
 }
 
@@ -2270,7 +2274,7 @@ template <class T, int CPB>
 int big_island_ctas();
 
 template <class T, int W, int CPB>
-static cudaError_t launch_island(const KArgs<T>& a, cudaStream_t s) {
+static cudaError_t launch_island(const KArgs<T>& a, cudaStream_t s, const volatile int* count_hint) {
   constexpr int cap = island_cap<T>();
   const size_t smem = size_t(cap) * smem_rows<CPB>() * 32 * sizeof(T) + size_t(cap) * 32 * kXch * sizeof(T) +
                       size_t(4 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
@@ -2288,14 +2292,36 @@ static cudaError_t launch_island(const KArgs<T>& a, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  // An island CTA holds an SM's whole register file (8 warps x 254
+  // registers), so a CTA without an island still keeps the main launch off its
+  // SM until it exits: with the previous step's island count as a hint the
+  // grid is 2x that + 8 (the round-robin loop covers any count)
   const int half = (a.n - a.e_begin) / 2 > 0 ? (a.n - a.e_begin) / 2 : 1;
-  const int grid = half < sms ? half : sms;
+  int grid = half < sms ? half : sms;
+  if (count_hint) {
+    const int h = 2 * *count_hint + 8;
+    if (h < grid) grid = h;
+  }
   k_env_step<T, W, CPB, true><<<grid, 32 * cap, smem, s>>>(a);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || !a.big_count) return e;
-  // islands with more envs than one CTA holds: consecutive CTAs per island,
-  // all co-resident (cooperative launch) so the island's global barrier
-  // cannot wait on an unscheduled CTA; CTAs without a part exit at once
+  if (e != cudaSuccess) return e;
+  if (count_hint)  // this step's count for the next step's grid (async, pinned)
+    e = cudaMemcpyAsync(const_cast<int*>(count_hint), a.isl_count, sizeof(int), cudaMemcpyDeviceToHost, s);
+  return e;
+}
+
+// islands with more envs than one CTA holds: consecutive CTAs per island, all
+// co-resident (cooperative launch) so the island's global barrier cannot wait
+// on an unscheduled CTA; CTAs without a part exit at once.  Launched on the
+// caller's stream after the main launch: a cooperative grid on the
+// high-priority side stream would hold back the main launch's remaining blocks
+// until the whole grid fits (~22 us per step even with no big island)
+template <class T, int W, int CPB>
+static cudaError_t launch_island_big(const KArgs<T>& a, cudaStream_t s) {
+  if (!a.big_count) return cudaSuccess;
+  constexpr int cap = island_cap<T>();
+  const size_t smem = size_t(cap) * smem_rows<CPB>() * 32 * sizeof(T) + size_t(cap) * 32 * kXch * sizeof(T) +
+                      size_t(4 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
   KArgs<T> b = a;
   b.isl_big_mode = 1;
   void* args[] = {&b};
@@ -2354,9 +2380,17 @@ cudaError_t launch_env_step(const KArgs<T>& a, int lanes, int cpb, cudaStream_t 
       if (e == cudaSuccess) e = cudaStreamWaitEvent(is, isl->fork, 0);
       if (e != cudaSuccess) return e;
     }
-    e = cpb <= 2 ? launch_island<T, 32, 2>(a, is) : launch_island<T, 32, 4>(a, is);
+    const volatile int* hint = isl ? isl->h_count : nullptr;
+    e = cpb <= 2 ? launch_island<T, 32, 2>(a, is, hint) : launch_island<T, 32, 4>(a, is, hint);
     if (e != cudaSuccess) return e;
-    e = cpb <= 2 ? launch_one<T, 32, 2>(a, s) : launch_one<T, 32, 4>(a, s);
+    // with islands last step, a plain launch: an early (PDL) main launch would
+    // take every SM before the island CTAs, which need a whole SM's register
+    // file each, are released by the fork; launched together, the side
+    // stream's priority places them first.  Without islands, PDL.
+    const bool pdl = is == s || (hint && *hint == 0);
+    e = cpb <= 2 ? launch_one<T, 32, 2>(a, s, pdl) : launch_one<T, 32, 4>(a, s, pdl);
+    if (e != cudaSuccess) return e;
+    e = cpb <= 2 ? launch_island_big<T, 32, 2>(a, s) : launch_island_big<T, 32, 4>(a, s);
     if (e != cudaSuccess || is == s) return e;
     e = cudaEventRecord(isl->join, is);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, isl->join, 0);

@@ -18,12 +18,13 @@ if wl.get("boxes"):
     kw["terrain"] = bench.terrain_boxes(wl["boxes"], wl["extent"])
 env = VecEnv(wl["task"], n_envs=wl["n"], seed=1234, **kw)
 env.reset()
-acts = [env.random_actions(s) for s in range(30)]
-for s in range(20):
+WARM = int(os.environ.get("WARM", "20"))  # WARM=160: a crowded scene (2-env islands)
+acts = [env.random_actions(s) for s in range(WARM + 10)]
+for s in range(WARM):
     env.step(acts[s])
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-    for s in range(20, 25):
+    for s in range(WARM, WARM + 5):
         env.step(acts[s])
     torch.cuda.synchronize()
 prof.export_chrome_trace("/tmp/hfh_trace.json")
@@ -51,7 +52,7 @@ import time  # noqa: E402
 torch.cuda.synchronize()
 t = time.perf_counter()
 for s in range(50):
-    env.step(acts[s % 30])
+    env.step(acts[s % len(acts)])
 t_host = (time.perf_counter() - t) / 50
 torch.cuda.synchronize()
 t_all = (time.perf_counter() - t) / 50

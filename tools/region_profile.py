@@ -8,6 +8,7 @@ usage: python tools/region_profile.py REPORT.ncu-rep [--sass /tmp/step_gi.sass]
 (build the sass: nvcc ... -cubin sim_step_f32.cu -o step.cubin; nvdisasm -gi step.cubin)"""
 import csv
 import io
+import os
 import re
 import subprocess
 import sys
@@ -15,10 +16,11 @@ from collections import Counter
 
 rep = sys.argv[1]
 sass = sys.argv[sys.argv.index("--sass") + 1] if "--sass" in sys.argv else "/tmp/step_gi.sass"
-KERNEL = "_ZN3stp10k_env_stepIfLi32ELi2ELb0ELb0E"
+KERNEL = os.environ.get("KERNEL", "_ZN3stp10k_env_stepIfLi32ELi2ELb0ELb0E")  # Lb1: the island instantiation
 SRC = "/root/repo/paper_1810_05762_b200/csrc/sim_step.cuh"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
-                      "regex:k_env_step"], capture_output=True, text=True).stdout
+                      "regex:k_env_step"] + (["--launch-skip", os.environ["NCU_SKIP"]] if "NCU_SKIP" in os.environ else []),
+                     capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[1]
 R = rows[2:]
