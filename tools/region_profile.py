@@ -19,11 +19,13 @@ sass = sys.argv[sys.argv.index("--sass") + 1] if "--sass" in sys.argv else "/tmp
 KERNEL = os.environ.get("KERNEL", "_ZN3stp10k_env_stepIfLi32ELi2ELb0ELb0E")  # Lb1: the island instantiation
 SRC = "/root/repo/paper_1810_05762_b200/csrc/sim_step.cuh"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
-                      "regex:k_env_step"] + (["--launch-skip", os.environ["NCU_SKIP"]] if "NCU_SKIP" in os.environ else []),
-                     capture_output=True, text=True).stdout
+                      "regex:k_env_step"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-h = rows[1]
-R = rows[2:]
+# one section per captured launch ("Kernel Name" row, header row, SASS rows): NCU_SECTION picks one
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+sec = int(os.environ.get("NCU_SECTION", "0"))
+h = rows[starts[sec] + 1]
+R = [r for r in rows[starts[sec] + 2:starts[sec + 1]] if r]
 ia = h.index("Instructions Executed")
 ist = h.index("Warp Stall Sampling (All Samples)")
 txt = open(sass).read()
