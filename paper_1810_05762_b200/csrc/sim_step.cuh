@@ -433,6 +433,18 @@ __host__ __device__ constexpr int island_cap() {
 }
 constexpr int kXch = kXchEntries;  // per-lane exchange entries (Mi is the largest)
 
+// all warps of a big island arrive; lane 0 of each counts in and spins
+static __device__ __noinline__ void big_island_barrier(int* bar_ctr, int target) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();
+    atomicAdd(bar_ctr, 1);
+    while (*reinterpret_cast<volatile int*>(bar_ctr) < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncwarp();
+}
+
 template <class T, int W, int CPB, bool ISL = false, bool DBG = false>
 __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (sizeof(T) == 4 && !ISL ? STP_MINB : 1))
     k_env_step(const KArgs<T> a) {
@@ -544,17 +556,10 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
     if constexpr (ISL) {
       if (bar_ctr) {
         // all warps of a big island (several CTAs, co-resident by the
-        // cooperative launch): generation-counted global barrier
-        __syncwarp();
-        ++bar_gen;
-        if ((threadIdx.x & 31) == 0) {
-          __threadfence();
-          atomicAdd(bar_ctr, 1);
-          const int target = bar_gen * isl_m;
-          while (*reinterpret_cast<volatile int*>(bar_ctr) < target) __nanosleep(32);
-          __threadfence();
-        }
-        __syncwarp();
+        // cooperative launch): generation-counted global barrier, out of
+        // line (one copy instead of one per call site: the island kernel's
+        // warps run alone on their SMs and stall on instruction fetch)
+        big_island_barrier(bar_ctr, ++bar_gen * isl_m);
       } else {
         asm volatile("bar.sync 1, %0;\n" ::"r"(32 * isl_m) : "memory");
       }
