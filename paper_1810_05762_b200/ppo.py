@@ -32,6 +32,12 @@ class PPOConfig:  # PAPER.md Table 4 (Humanoid)
     lam: float = 0.95
     lr: float = 3e-4
     vf_coef: float = 0.5
+    # "fp32": IEEE fp32 GEMMs (cuBLAS SIMT kernels at these shapes); "tf32":
+    # the GEMMs on the tensor cores with TF32 inputs (10-bit mantissa, fp32
+    # accumulation): the 4096-env update 0.116 -> 0.063 s, but over 8 Adam
+    # steps the parameter step moves 14 % from the fp64 restatement's (fp32:
+    # 3e-5; tests/test_gpu_ppo.py bounds both), so it is opt-in
+    matmul: str = "fp32"
 
 
 def _dist():
@@ -133,8 +139,15 @@ class PPOLearner:
         one device flag read once after the epochs (no host synchronisation per
         minibatch) — the steps after a non-finite loss are discarded with the
         restore, so the outcome equals aborting at the first one."""
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = self.cfg.matmul == "tf32"
+        try:
+            return self._update(xw, actions, adv, ret, generator, adv_stats)
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+
+    def _update(self, xw, actions, adv, ret, generator, adv_stats):
         cfg = self.cfg
-        del old_logp  # re-derived from the snapshot below
         adv = global_normalize(adv, adv_stats)
         B = xw.shape[0]
         with torch.no_grad():

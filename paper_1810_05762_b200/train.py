@@ -31,6 +31,8 @@ def main(argv=None):
     ap.add_argument("--frames", type=int, default=32)
     ap.add_argument("--epochs", type=int, default=20)
     ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--matmul", choices=["fp32", "tf32"], default="fp32",
+                    help="update GEMM precision (PPOConfig.matmul; tf32 is ~1.8x faster, not fp32-exact)")
     args = ap.parse_args(argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -43,7 +45,7 @@ def main(argv=None):
     env = VecEnv(args.task, n_envs=args.envs, device=local, seed=args.seed, env_offset=rank * args.envs)
     torch.manual_seed(args.seed)
     model = ActorCritic(env.obs_dim, env.action_dim, HIDDEN.get(args.task, (256, 128, 64))).to(dev)
-    cfg = PPOConfig(frames_per_iter=args.frames, epochs=args.epochs)
+    cfg = PPOConfig(frames_per_iter=args.frames, epochs=args.epochs, matmul=args.matmul)
     learner = PPOLearner(model, cfg)  # broadcasts rank 0's parameters
     kern = PolicyKernel(model, dev)
     stat = RunningStat(env.obs_dim, device=dev)

@@ -126,12 +126,21 @@ def _update_fp64(params, xw, act, adv, ret, cfg, perms):
     return P, float(kl), float(loss), adapt_learning_rate(lr, float(kl), cfg.desired_kl)
 
 
-def test_ppo_update_matches_fp64_restatement():
+# worst relative parameter-step error, relative KL / loss error vs the fp64
+# restatement: IEEE fp32 GEMMs (the default; measured 2.7e-5 / 3e-7 / 1e-7)
+# and the opt-in TF32 tensor-core GEMMs (measured 0.137 / 1.4e-2 / 7.4e-4:
+# Adam's normalisation amplifies the TF32 rounding of small gradients)
+UPDATE_BOUNDS = {"fp32": (1e-3, 1e-3, 1e-3), "tf32": (0.3, 5e-2, 5e-3)}
+
+
+@pytest.mark.parametrize("matmul", ["fp32", "tf32"])
+def test_ppo_update_matches_fp64_restatement(matmul):
     torch.manual_seed(0)
     O, A, B = 76, 21, 512
     model = ActorCritic(O, A).cuda()
     params0 = {k: v.detach().cpu().double() for k, v in model.named_parameters()}
-    cfg = PPOConfig(frames_per_iter=32, epochs=4, minibatch_per_agent=16, lr=3e-4)  # 2 minibatches per epoch
+    cfg = PPOConfig(frames_per_iter=32, epochs=4, minibatch_per_agent=16, lr=3e-4,  # 2 minibatches per epoch
+                    matmul=matmul)
     g = torch.Generator().manual_seed(5)
     xw = torch.randn(B, O, generator=g).clamp(-10, 10)
     with torch.no_grad():
@@ -153,10 +162,11 @@ def test_ppo_update_matches_fp64_restatement():
         worst = max(worst, rel)
     print(f"update: KL {st['kl']:.6e} vs {kl64:.6e}, loss {st['loss']:.6e} vs {loss64:.6e}, "
           f"worst relative parameter-step error {worst:.2e}")
+    b_step, b_kl, b_loss = UPDATE_BOUNDS[matmul]
     assert not st["aborted"]
-    assert worst <= 1e-3
-    assert abs(st["kl"] - kl64) <= 1e-3 * max(abs(kl64), 1e-6)
-    assert abs(st["loss"] - loss64) <= 1e-3 * max(abs(loss64), 1e-6)
+    assert worst <= b_step
+    assert abs(st["kl"] - kl64) <= b_kl * max(abs(kl64), 1e-6)
+    assert abs(st["loss"] - loss64) <= b_loss * max(abs(loss64), 1e-6)
     assert st["lr"] == lr64
 
 
