@@ -253,3 +253,39 @@ print("ok")
     env = dict(os.environ, STP_ISLAND_BUDGET="1")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_island_grid_hint_does_not_change_results(precision):
+    """The persistent island grid is sized from the previous step's island
+    count (a pinned host hint, sim_step.cuh launch_island).  A handle whose
+    last step had no islands launches 8 island CTAs for 12 two-agent islands
+    (some CTAs loop over two); a fresh handle launches 12.  Both must give
+    bit-identical states, contact counts and reports, with no env flagged."""
+    n = 24
+    chains = [(2 * k, 2) for k in range(12)]
+    g0 = VecEnv("hfh", n_envs=n, precision=precision, seed=41)
+    o = oracle.OracleEnv(g0.model, g0.task, g0.cfg, n, seed=41)
+    calm = o.get_state()
+    crowded = S.chain_state(calm.copy(), g0.model, chains)
+    tm = np.array([g0.model.joints[j].max_torque for j in range(g0.action_dim)])
+    tq = o.random_actions(0) * tm
+    fresh = VecEnv("hfh", n_envs=n, precision=precision, seed=41)
+    stale = VecEnv("hfh", n_envs=n, precision=precision, seed=41)
+    stale.set_state(calm)
+    stale.physics_step(np.zeros_like(tq))  # no islands: the next grid is 2 * 0 + 8 CTAs
+    assert stale.report()["overflow"].sum() == 0
+    for h in (fresh, stale):
+        h.set_state(crowded)
+    dd = fresh.detect_inter_agent()
+    nb = fresh.n_bodies
+    links = {(a // nb, b // nb) for a, b in zip(dd["body_a"].tolist(), dd["body_b"].tolist())}
+    assert all((s0, s0 + 1) in links for s0, _ in chains), "every pair must touch (12 islands)"
+    for t in range(3):
+        fresh.physics_step(tq * (0.5 + 0.25 * t))
+        stale.physics_step(tq * (0.5 + 0.25 * t))
+        np.testing.assert_array_equal(fresh.get_state(), stale.get_state())
+        np.testing.assert_array_equal(fresh.contact_arrays()["count"], stale.contact_arrays()["count"])
+        rf, rs = fresh.report(), stale.report()
+        assert rf["overflow"].sum() == 0 and rs["overflow"].sum() == 0
+        np.testing.assert_array_equal(rf["failed"], rs["failed"])
