@@ -443,7 +443,7 @@ def run_ours(args, world, rank, local):
         else:
             pst._merge(first.n, first.mean, first.m2)
         times = []
-        for it in range(3):
+        for it in range(5):
             if world > 1:
                 torch.distributed.barrier()
             torch.cuda.synchronize()
@@ -467,7 +467,8 @@ def run_ours(args, world, rank, local):
         it_s = statistics.median(times[1:])
         frames = pcfg.frames_per_iter * N_ENVS * world
         ppo = {"iteration_s": it_s, "frames_per_iteration": frames, "env_steps_per_s_with_update": frames / it_s,
-               "epochs": pcfg.epochs, "kl": stats["kl"], "aborted": stats["aborted"], "clock": "host, median of 2"}
+               "epochs": pcfg.epochs, "kl": stats["kl"], "aborted": stats["aborted"], "clock": "host, median of 4",
+               "update_gemms": pcfg.matmul}
     except Exception as ex:
         ppo = {"error": repr(ex)}
 
