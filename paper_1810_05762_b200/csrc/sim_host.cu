@@ -81,6 +81,10 @@ struct stp_sim {
   static constexpr int kChunks = STP_HOST_CHUNKS;
   cudaStream_t cs[kChunks] = {};
   cudaEvent_t ev_in = nullptr, ev_out[kChunks] = {};
+  // stp_step_host, inter-agent handles: the actions' upload runs on cs[0]
+  // beside the pre-step chain (which reads only the state); the step launch
+  // waits for it (act_wait, consumed by launch())
+  cudaEvent_t ev_act = nullptr, act_wait = nullptr;
   stp::PairScratch* pairs = nullptr;  // inter-agent detection scratch (created on first use)
   std::vector<void*> allocations;
 };
@@ -403,6 +407,10 @@ int launch_t(stp_sim* s, int mode, const float* torques, const float* actions, f
     a.big_bar = v.big_bar;
     a.big_xch = reinterpret_cast<T*>(v.big_xch);
   }
+  if (s->act_wait) {  // the actions' upload (stp_step_host) overlapped the pre-step chain
+    CK(cudaStreamWaitEvent(st, s->act_wait, 0));
+    s->act_wait = nullptr;
+  }
   if (a.merged && !s->isl.side) {
     // the highest stream priority: island CTAs (long, latency-bound chains of a
     // few warps) get SMs before the main launch fills the machine instead of
@@ -632,6 +640,7 @@ void stp_destroy(stp_sim* s) {
     if (s->ev_out[c]) cudaEventDestroy(s->ev_out[c]);
   }
   if (s->ev_in) cudaEventDestroy(s->ev_in);
+  if (s->ev_act) cudaEventDestroy(s->ev_act);
   if (s->isl.side) {
     cudaStreamSynchronize(s->isl.side);
     if (s->isl.h_count) cudaFreeHost(s->isl.h_count);
@@ -868,8 +877,26 @@ int stp_step_host(stp_sim* s, const float* actions, float* obs, float* reward, u
                     ? 1
                     : int(std::min<size_t>(stp_sim::kChunks, std::max<size_t>(1, N / kMinChunk)));
   if (C == 1) {
-    CK(cudaMemcpyAsync(s->d_act, actions, N * s->J * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+    if (s->task.inter_agent_collisions && s->J) {
+      // upload beside the pre-step chain (detection reads the state only)
+      if (!s->ev_in) {
+        CK(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
+        for (int c = 0; c < stp_sim::kChunks; ++c) {
+          CK(cudaStreamCreateWithFlags(&s->cs[c], cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&s->ev_out[c], cudaEventDisableTiming));
+        }
+      }
+      if (!s->ev_act) CK(cudaEventCreateWithFlags(&s->ev_act, cudaEventDisableTiming));
+      CK(cudaEventRecord(s->ev_in, s->stream));  // after the work already queued (readers of d_act)
+      CK(cudaStreamWaitEvent(s->cs[0], s->ev_in, 0));
+      CK(cudaMemcpyAsync(s->d_act, actions, N * s->J * sizeof(float), cudaMemcpyHostToDevice, s->cs[0]));
+      CK(cudaEventRecord(s->ev_act, s->cs[0]));
+      s->act_wait = s->ev_act;
+    } else {
+      CK(cudaMemcpyAsync(s->d_act, actions, N * s->J * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+    }
     int rc = launch(s, 1, nullptr, s->d_act, obs ? s->d_obs : nullptr, rew_k, done_k, nullptr, s->stream);
+    s->act_wait = nullptr;
     if (rc) return rc;
     if (obs) CK(cudaMemcpyAsync(obs, s->d_obs, N * s->obs_dim * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
     if (reward && !rew_z) CK(cudaMemcpyAsync(reward, s->d_rew, N * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
