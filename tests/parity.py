@@ -60,6 +60,12 @@ def obs_groups(J, n_feet, height_map):
     return g
 
 
+# height-map samples: a difference above HM_JUMP (m) is a jump across a box
+# edge; it is an explained edge flip when the GPU's sample is within HM_OWN of
+# the double height map of the GPU's own state (counted, excluded from the
+# height_map statistics, bounded by the tests)
+HM_JUMP, HM_OWN = 0.05, 1e-3
+
 # groups compared relative to max(1, |value|) (velocities: heavy-tailed)
 RELATIVE = {"v_root", "w_root", "theta_dot"}
 
@@ -144,18 +150,26 @@ def _feet_cols(J, nf):
 
 
 def teacher_forced_env(name="humanoid", n=32, steps=500, seed=7, scale=1.0, precision="f32", source="oracle",
-                       envelope=True, oracle_kind="restatement", threads=None, warm=0, device=0):
+                       envelope=True, oracle_kind="restatement", threads=None, warm=0, device=0, terrain=None):
     """Teacher-forced env_step protocol (see module docstring).  Returns a
     dict of statistics (percentiles + max) for the GPU and, with
     ``envelope``, for the fp32 restatement of the reference physics."""
-    g = VecEnv(name, n_envs=n, precision=precision, seed=seed, device=device)
+    g = VecEnv(name, n_envs=n, precision=precision, seed=seed, device=device, terrain=terrain)
     m, cfg = g.model, g.cfg
     J, nf = g.action_dim, m.n_feet
     otask = _task(name, auto_reset=0)
     threads = threads or min(16, os.cpu_count() or 1)
-    o = oracle.OracleEnv(m, otask, cfg, n, seed=seed, kind=oracle_kind, nthreads=threads)
-    o32 = oracle.OracleEnv(m, otask, cfg, n, seed=seed, precision="f32", nthreads=threads) if envelope else None
+    o = oracle.OracleEnv(m, otask, cfg, n, seed=seed, kind=oracle_kind, nthreads=threads, terrain=terrain)
+    o32 = oracle.OracleEnv(m, otask, cfg, n, seed=seed, precision="f32", nthreads=threads,
+                           terrain=terrain) if envelope else None
     groups = obs_groups(J, nf, bool(g.task.height_map))
+    # height map: the terrain height is discontinuous at box edges, so a sample
+    # within fp32 rounding of an edge can jump by a box height between the two
+    # sides; a jump (> HM_JUMP) is counted as an edge flip when the GPU's value
+    # equals the double height map of the GPU's own state (o_hm observes it)
+    o_hm = oracle.OracleEnv(m, otask, cfg, n, seed=seed, nthreads=threads, terrain=terrain) \
+        if "height_map" in groups else None
+    hm_flips = 0
     thr = m.fall_height
     acc = {k: {"gpu": [], "f32": []} for k in ["dx", "dv", "reward"] + list(groups)}
     reset_err = []
@@ -231,6 +245,12 @@ def teacher_forced_env(name="humanoid", n=32, steps=500, seed=7, scale=1.0, prec
                 d = np.abs(ob[:, cols].astype(np.float64) - oo[:, cols])
                 if gname in RELATIVE:
                     d = d / np.maximum(1, np.abs(oo[:, cols]))
+                if gname == "height_map" and key == "gpu" and (d > HM_JUMP).any():
+                    o_hm.set_state(st)
+                    own = np.abs(ob[:, cols].astype(np.float64) - o_hm.observe()[:, cols])
+                    edge = (d > HM_JUMP) & (own <= HM_OWN)
+                    hm_flips += int((edge & fine[:, None]).sum())
+                    d = np.where(edge, 0.0, d)
                 acc[gname][key].append(d.max(axis=1)[fine])
             if key == "gpu" and do.any():
                 rs = do.astype(bool) & (dn == 1)
@@ -242,10 +262,12 @@ def teacher_forced_env(name="humanoid", n=32, steps=500, seed=7, scale=1.0, prec
     o.close()
     if o32 is not None:
         o32.close()
+    if o_hm is not None:
+        o_hm.close()
     out = {"task": name, "precision": precision, "n_envs": n, "steps": n_steps, "torque_scale": scale,
            "source": source, "oracle": oracle_kind, "done_events": n_done, "failed": n_failed,
            "done_mismatch": done_mism, "done_boundary": done_boundary, "feet_flag_mismatch": feet_mism,
-           "reward_discrete_flips": flips,
+           "reward_discrete_flips": flips, "height_map_edge_flips": hm_flips,
            "reset_state_obs_err": summarize(np.concatenate(reset_err)) if reset_err else {"n": 0}}
     for k, v in acc.items():
         out[k] = {key: summarize(np.concatenate(v[key])) if v[key] else {"n": 0} for key in v}

@@ -67,6 +67,30 @@ def test_teacher_forced_hfh_with_interagent_against_reference():
     _check(rep, absolute=True)
 
 
+def _terrain(n_boxes=160, seed=3):
+    from paper_1810_05762_b200 import abi
+    spec = abi.TerrainSpec(count=n_boxes, dim_lo=0.2, dim_hi=1.0, x_lo=-3.0, x_hi=66.0, y_lo=-3.0, y_hi=3.0,
+                           yaw_lo=0.0, yaw_hi=3.141592653589793, seed=seed)
+    boxes = (abi.StaticBox * n_boxes)()
+    assert abi.load().stp_generate_terrain(spec, boxes, n_boxes) == n_boxes
+    return list(boxes)
+
+
+def test_teacher_forced_hfh_terrain_fp32():
+    """HFH on complex terrain (config C4 shape: 160 yaw boxes over the 32 envs'
+    strip): teacher-forced env_step over 200 steps against the compiled
+    reference physics (inter-agent islands on, as for flat HFH): box contacts,
+    the 15 x 11 height-map observation, flagrun and falls."""
+    rep = P.teacher_forced_env("hfh_terrain", n=32, steps=200, seed=7, terrain=_terrain(), envelope=False,
+                               oracle_kind="reference")
+    _show("hfh terrain", rep)
+    assert "height_map" in rep
+    # samples at box edges may jump between the sides (explained by each side's
+    # own state; tests/parity.py HM_JUMP / HM_OWN): at most 0.1 % of them
+    assert rep["height_map_edge_flips"] <= 1e-3 * 165 * rep["height_map"]["gpu"]["n"]
+    _check(rep, absolute=True)
+
+
 def test_bench_config_teacher_forced():
     """The bench workload itself: 4096 Humanoids, seed 1234, auto-reset, after
     64 free-running GPU steps; 3 steps with the oracle teacher-forced from the

@@ -37,6 +37,10 @@ def main():
     P["teacher_forced_ant_saturating"] = parity.teacher_forced_env("ant", steps=steps, scale=1.0)
     P["teacher_forced_hfh_reference"] = parity.teacher_forced_env("hfh", steps=steps, envelope=False,
                                                                   oracle_kind="reference")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_gpu_envparity import _terrain  # noqa: E402
+    P["teacher_forced_hfh_terrain_reference"] = parity.teacher_forced_env(
+        "hfh_terrain", steps=min(steps, 200), terrain=_terrain(), envelope=False, oracle_kind="reference")
     P["bench_config_4096_seed1234"] = parity.teacher_forced_env("humanoid", n=4096, steps=3, seed=1234,
                                                                source="gpu", warm=64, envelope=True)
     rep["seconds"] = time.time() - t0
