@@ -397,6 +397,8 @@ int launch_t(stp_sim* s, int mode, const float* torques, const float* actions, f
     a.merged = v.merged;
     a.isl_members = v.isl_members;
     a.isl_count = v.isl_count;
+    a.isl_order = v.isl_order;
+    a.isl_npair = v.isl_npair;
     a.isl_err = v.err;
     a.xslots = v.xslots;
     a.xcount = v.xcount;

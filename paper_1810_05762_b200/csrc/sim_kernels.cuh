@@ -87,6 +87,8 @@ struct KArgs {
   const uint8_t* merged;      // [n] 1: env belongs to a contact-merged island
   const int* isl_members;     // [n / 2][kIslandMax] member envs (unordered; -1 unused)
   const int* isl_count;       // number of merged islands
+  const int* isl_order;       // island indices: the two-env islands first ([0, *isl_npair)), then the rest
+  const int* isl_npair;       // number of two-env islands (packed four per island CTA)
   const XSlot* xslots;        // [n * B][kXSlots] cross contacts of each body
   const int* xcount;          // [n * B]
   const int* isl_err;         // preparation overflow bits (see IslandView)

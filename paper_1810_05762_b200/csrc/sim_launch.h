@@ -101,6 +101,8 @@ struct IslandView {
   const uint8_t* merged;  // 1: stepped by an island launch, 2: island over budget (stepped alone, flagged)
   const int* isl_members;
   const int* isl_count;
+  const int* isl_order;  // two-env islands first, then the rest
+  const int* isl_npair;
   int* err;  // bit 1: more than kXSlots cross contacts on a body, 4: contact edges dropped,
              // 8: candidate env pairs dropped (pair capacity)
   const XSlot* xslots;

@@ -150,7 +150,7 @@ __global__ void k_pairs_reset(int* __restrict__ bin_count, int nbins, int* __res
     gcnt[i] = 0;
     counters[i] = 0;
   }
-  if (icnt && i < 3) icnt[i] = 0;
+  if (icnt && i < 5) icnt[i] = 0;
 }
 
 template <class T>
@@ -400,7 +400,8 @@ __global__ void k_islands(int n, const int2* __restrict__ edges, const int* __re
                           int* __restrict__ isl_members, int* __restrict__ isl_count, int* __restrict__ err,
                           int labels_in_smem, int cap, int max_parts, int* __restrict__ big_count,
                           int* __restrict__ big_off, int* __restrict__ big_size, int* __restrict__ big_fill,
-                          int* __restrict__ big_members, int* __restrict__ big_bar) {
+                          int* __restrict__ big_members, int* __restrict__ big_bar, int* __restrict__ isl_order,
+                          int* __restrict__ npair, int* __restrict__ nrest) {
   pdl_wait();  // programmatic dependent launch (sim_launch.h)
   pdl_trigger();
   extern __shared__ int slab[];
@@ -503,6 +504,16 @@ __global__ void k_islands(int n, const int2* __restrict__ edges, const int* __re
       isl_members[i * kIslandMax + atomicAdd(&isl_fill[i], 1)] = e;
     }
   }
+  // island order for the one-CTA launch: two-env islands first (four share
+  // an island CTA), then the rest (big islands there have no members here)
+  __syncthreads();
+  const int nisl = *isl_count;
+  for (int i = threadIdx.x; i < nisl; i += blockDim.x)
+    if (isl_size[i] == 2 && isl_big[i] == -1) isl_order[atomicAdd(npair, 1)] = i;
+  __syncthreads();
+  const int np = *npair;
+  for (int i = threadIdx.x; i < nisl; i += blockDim.x)
+    if (!(isl_size[i] == 2 && isl_big[i] == -1)) isl_order[np + atomicAdd(nrest, 1)] = i;
 }
 
 __global__ void k_keys(const PairContact* __restrict__ c, const int* __restrict__ n_p, int cap,
@@ -536,9 +547,9 @@ struct PairScratch {
   XSlot* xslots = nullptr;
   int* xcount = nullptr;
   int2* edges = nullptr;
-  int* icnt = nullptr;  // [0] edges, [1] islands, [2] error bits
+  int* icnt = nullptr;  // [0] edges, [1] islands, [2] error bits, [3] two-env islands, [4] the rest placed
   int *label = nullptr, *isl_of = nullptr, *isl_size = nullptr, *isl_members = nullptr;
-  int *isl_fill = nullptr, *isl_big = nullptr;
+  int *isl_fill = nullptr, *isl_big = nullptr, *isl_order = nullptr;
   uint8_t* merged = nullptr;
   // big islands: [0] count, then off / size / fill / barrier [kBigIslands] each
   int* big = nullptr;
@@ -552,8 +563,8 @@ void pair_scratch_free(PairScratch* p) {
                   (void*)p->cidx, (void*)p->scidx, p->tmp, (void*)p->xslots, (void*)p->xcount, (void*)p->edges,
                   (void*)p->icnt, (void*)p->label, (void*)p->isl_of, (void*)p->isl_size, (void*)p->isl_members,
                   (void*)p->merged, (void*)p->env_cell, (void*)p->bin_count, (void*)p->bins, (void*)p->ovf,
-                  (void*)p->gcnt, (void*)p->isl_fill, (void*)p->isl_big, (void*)p->big, (void*)p->big_members,
-                  p->big_xch})
+                  (void*)p->gcnt, (void*)p->isl_fill, (void*)p->isl_big, (void*)p->isl_order, (void*)p->big,
+                  (void*)p->big_members, p->big_xch})
     if (q) cudaFree(q);
   delete p;
 }
@@ -683,13 +694,14 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
   if (P->isl_n < size_t(n)) {
     for (void* q : {(void*)P->xslots, (void*)P->xcount, (void*)P->edges, (void*)P->icnt, (void*)P->label,
                     (void*)P->isl_of, (void*)P->isl_size, (void*)P->isl_members, (void*)P->merged,
-                    (void*)P->isl_fill, (void*)P->isl_big, (void*)P->big, (void*)P->big_members, P->big_xch})
+                    (void*)P->isl_fill, (void*)P->isl_big, (void*)P->isl_order, (void*)P->big, (void*)P->big_members,
+                    P->big_xch})
       if (q) cudaFree(q);
     P->isl_n = n;
     STP_CK(cudaMalloc(&P->xslots, sizeof(XSlot) * size_t(n) * B * kXSlots));
     STP_CK(cudaMalloc(&P->xcount, sizeof(int) * size_t(n) * B));
     STP_CK(cudaMalloc(&P->edges, sizeof(int2) * size_t(n) * B * kXSlots));
-    STP_CK(cudaMalloc(&P->icnt, sizeof(int) * 3));
+    STP_CK(cudaMalloc(&P->icnt, sizeof(int) * 5));
     STP_CK(cudaMalloc(&P->label, sizeof(int) * n));
     STP_CK(cudaMalloc(&P->isl_of, sizeof(int) * n));
     STP_CK(cudaMalloc(&P->isl_size, sizeof(int) * (n / 2 + 1)));
@@ -697,6 +709,7 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
     STP_CK(cudaMalloc(&P->merged, n));
     STP_CK(cudaMalloc(&P->isl_fill, sizeof(int) * (n / 2 + 1)));
     STP_CK(cudaMalloc(&P->isl_big, sizeof(int) * (n / 2 + 1)));
+    STP_CK(cudaMalloc(&P->isl_order, sizeof(int) * (n / 2 + 1)));
     STP_CK(cudaMalloc(&P->big, sizeof(int) * (1 + 4 * kBigIslands)));
     STP_CK(cudaMalloc(&P->big_members, sizeof(int) * n));
     STP_CK(cudaMalloc(&P->big_xch, sizeof(double) * kBigStride * size_t(n)));
@@ -715,10 +728,13 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
   STP_CK(launch_pdl(k_islands, dim3(1), dim3(1024), lab_smem ? lab_bytes : 0, st, n, P->edges, P->icnt, edge_cap,
                     P->label, P->merged, P->isl_of, P->isl_size, P->isl_fill, P->isl_big, P->isl_members,
                     P->icnt + 1, P->icnt + 2, int(lab_smem), cap, max_parts, bg, bg + 1, bg + 1 + kBigIslands,
-                    bg + 1 + 2 * kBigIslands, P->big_members, bg + 1 + 3 * kBigIslands));
+                    bg + 1 + 2 * kBigIslands, P->big_members, bg + 1 + 3 * kBigIslands, P->isl_order, P->icnt + 3,
+                    P->icnt + 4));
   view->merged = P->merged;
   view->isl_members = P->isl_members;
   view->isl_count = P->icnt + 1;
+  view->isl_order = P->isl_order;
+  view->isl_npair = P->icnt + 3;
   view->err = P->icnt + 2;
   view->xslots = P->xslots;
   view->xcount = P->xcount;

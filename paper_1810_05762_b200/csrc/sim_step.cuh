@@ -462,6 +462,9 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
   int* bar_ctr = nullptr;    // big islands: global barrier counter
   T* big_area = nullptr;     // big islands: the island's global exchange area
   int isl_next = 0, n_isl = 0;
+  int isl_base_w = 0;  // one-CTA islands: the island's first warp in the CTA (cap / 2 two-env islands share a CTA)
+  int isl_bar_id = 1;  // its named barrier
+  int n_pair = 0, n_pair_items = 0;
   if constexpr (ISL) {
     static_assert(W == 32, "island mode: one env per warp");
     constexpr int cap = island_cap<T>();
@@ -497,7 +500,9 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
       e = __reduce_max_sync(0xffffffffu, found);
     } else {
       n_isl = *a.isl_count;
-      isl_next = blockIdx.x;
+      n_pair = *a.isl_npair;
+      n_pair_items = (n_pair + int(blockDim.x >> 6) - 1) / int(blockDim.x >> 6);  // cap / 2 pairs per item
+      isl_next = blockIdx.x;  // work item: a group of four two-env islands, or one other island
     }
   } else {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -507,12 +512,26 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
   }
   for (;;) {
     if constexpr (ISL) {
-      if (!a.isl_big_mode) {  // the next island of this CTA
-        if (isl_next >= n_isl) return;
-        mem = a.isl_members + isl_next * kIslandMax;
+      if (!a.isl_big_mode) {  // the next work item of this CTA
+        if (isl_next >= n_pair_items + (n_isl - n_pair)) return;
+        const int cw = threadIdx.x >> 5;
+        int island = -1;
+        if (isl_next < n_pair_items) {  // warps 2j, 2j + 1: two-env island (cap / 2) item + j
+          const int slot = int(blockDim.x >> 6) * isl_next + (cw >> 1);
+          if (slot < n_pair) island = a.isl_order[slot];
+          isl_base_w = cw & ~1;
+          isl_bar_id = 1 + (cw >> 1);
+          isl_w = cw & 1;
+        } else {  // one island in the whole CTA
+          island = a.isl_order[n_pair + isl_next - n_pair_items];
+          isl_base_w = 0;
+          isl_bar_id = 1;
+          isl_w = cw;
+        }
+        mem = a.isl_members + (island >= 0 ? island : 0) * kIslandMax;
         isl_m = 0;
-        for (int k = 0; k < kIslandMax; ++k) isl_m += mem[k] >= 0;
-        isl_w = threadIdx.x >> 5;
+        if (island >= 0)
+          for (int k = 0; k < kIslandMax; ++k) isl_m += mem[k] >= 0;
         e = -1;
         for (int k = 0; k < isl_m; ++k) {
           int rank = 0;
@@ -550,6 +569,10 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
     xch = big_area;
     red = xch + size_t(isl_m) * 32 * kXch;
     vote = reinterpret_cast<int*>(red + 4 * isl_m);
+  } else if (ISL) {  // this island's slices (indexed by rank within the island)
+    xch += isl_base_w * 32 * kXch;
+    red += 4 * isl_base_w;
+    vote += isl_base_w;
   }
   int bar_gen = 0;
   auto isl_bar = [&]() {
@@ -561,7 +584,7 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
         // warps run alone on their SMs and stall on instruction fetch)
         big_island_barrier(bar_ctr, ++bar_gen * isl_m);
       } else {
-        asm volatile("bar.sync 1, %0;\n" ::"r"(32 * isl_m) : "memory");
+        asm volatile("bar.sync %0, %1;\n" ::"r"(isl_bar_id), "r"(32 * isl_m) : "memory");
       }
     }
   };
