@@ -564,7 +564,9 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
   // shared memory for one-CTA islands, a global area for big islands
   T* xch = reinterpret_cast<T*>(smem_raw) + (ISL ? island_cap<T>() : 0) * smem_rows<CPB>() * 32;
   T* red = xch + (ISL ? island_cap<T>() * 32 * kXch : 0);
-  int* vote = reinterpret_cast<int*>(red + 4 * island_cap<T>());
+  // one-CTA islands: two halves of 4 * cap partials (isl_sum / isl_sum4 alternate
+  // between them, so the barrier that protected the reuse is not needed)
+  int* vote = reinterpret_cast<int*>(red + 8 * island_cap<T>());
   if (ISL && big_area) {
     xch = big_area;
     red = xch + size_t(isl_m) * 32 * kXch;
@@ -589,14 +591,24 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
     }
   };
   // segment sums / votes over the whole island (the warp forms without ISL)
+  int red_par = 0;  // one-CTA islands: the half of `red` the next island sum uses
+  // The half used by one sum is reused two sums later; the barrier of the sum
+  // in between orders every warp's reads before any warp's next writes.
+  auto red_buf = [&]() -> T* {
+    if (bar_ctr) return red;  // big islands: one buffer, a trailing barrier
+    T* rb = red + red_par * 4 * island_cap<T>();
+    red_par ^= 1;
+    return rb;
+  };
   auto isl_sum = [&](T v) -> T {
     v = seg_sum<W>(v, mask);
     if constexpr (ISL) {
-      if (lane == 0) red[isl_w] = v;
+      T* rb = red_buf();
+      if (lane == 0) rb[isl_w] = v;
       isl_bar();
       T s = T(0);
-      for (int k = 0; k < isl_m; ++k) s += red[k];
-      isl_bar();
+      for (int k = 0; k < isl_m; ++k) s += rb[k];
+      if (bar_ctr) isl_bar();
       v = s;
     }
     return v;
@@ -604,21 +616,22 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
   auto isl_sum4 = [&](T& v0, T& v1, T& v2, T& v3) {
     seg_sum4<W>(v0, v1, v2, v3, mask);
     if constexpr (ISL) {
+      T* rb = red_buf();
       if (lane == 0) {
-        red[4 * isl_w] = v0;
-        red[4 * isl_w + 1] = v1;
-        red[4 * isl_w + 2] = v2;
-        red[4 * isl_w + 3] = v3;
+        rb[4 * isl_w] = v0;
+        rb[4 * isl_w + 1] = v1;
+        rb[4 * isl_w + 2] = v2;
+        rb[4 * isl_w + 3] = v3;
       }
       isl_bar();
       T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
       for (int k = 0; k < isl_m; ++k) {
-        s0 += red[4 * k];
-        s1 += red[4 * k + 1];
-        s2 += red[4 * k + 2];
-        s3 += red[4 * k + 3];
+        s0 += rb[4 * k];
+        s1 += rb[4 * k + 1];
+        s2 += rb[4 * k + 2];
+        s3 += rb[4 * k + 3];
       }
-      isl_bar();
+      if (bar_ctr) isl_bar();
       v0 = s0;
       v1 = s1;
       v2 = s2;
@@ -628,6 +641,18 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
   auto isl_all = [&](bool p) -> bool {
     bool r = __all_sync(mask, p);
     if constexpr (ISL) {
+      if (!bar_ctr) {
+        // one-CTA island: the vote is the named barrier's own AND reduction
+        // (one instruction instead of a shared-memory vote between two barriers)
+        int v;
+        asm volatile(
+            "{\n\t.reg .pred pi, po;\n\tsetp.ne.b32 pi, %1, 0;\n\t"
+            "bar.red.and.pred po, %2, %3, pi;\n\tselp.b32 %0, 1, 0, po;\n\t}\n"
+            : "=r"(v)
+            : "r"(int(r)), "r"(isl_bar_id), "r"(32 * isl_m)
+            : "memory");
+        return v != 0;
+      }
       if (lane == 0) vote[isl_w] = r ? 1 : 0;
       isl_bar();
       r = true;
@@ -2305,7 +2330,7 @@ template <class T, int W, int CPB>
 static cudaError_t launch_island(const KArgs<T>& a, cudaStream_t s, const volatile int* count_hint) {
   constexpr int cap = island_cap<T>();
   const size_t smem = size_t(cap) * smem_rows<CPB>() * 32 * sizeof(T) + size_t(cap) * 32 * kXch * sizeof(T) +
-                      size_t(4 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
+                      size_t(8 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
   static bool configured[64] = {};
   if (first_on_device(configured)) {
     cudaError_t err = cudaFuncSetAttribute(k_env_step<T, W, CPB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2349,7 +2374,7 @@ static cudaError_t launch_island_big(const KArgs<T>& a, cudaStream_t s) {
   if (!a.big_count) return cudaSuccess;
   constexpr int cap = island_cap<T>();
   const size_t smem = size_t(cap) * smem_rows<CPB>() * 32 * sizeof(T) + size_t(cap) * 32 * kXch * sizeof(T) +
-                      size_t(4 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
+                      size_t(8 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
   KArgs<T> b = a;
   b.isl_big_mode = 1;
   void* args[] = {&b};
@@ -2368,7 +2393,7 @@ int big_island_ctas() {
   if (!per_dev[dev]) {
     constexpr int cap = island_cap<T>();
     const size_t smem = size_t(cap) * smem_rows<CPB>() * 32 * sizeof(T) + size_t(cap) * 32 * kXch * sizeof(T) +
-                        size_t(4 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
+                        size_t(8 * cap) * sizeof(T) + size_t(cap) * sizeof(int);
     cudaFuncSetAttribute(k_env_step<T, 32, CPB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_env_step<T, 32, CPB, true>, 32 * cap, smem);

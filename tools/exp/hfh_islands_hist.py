@@ -14,8 +14,8 @@ from paper_1810_05762_b200.sim import VecEnv  # noqa: E402
 task = os.environ.get("TASK", "hfh")
 env = VecEnv(task, n_envs=4096, seed=1234)
 env.reset()
-ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(400)]
-for t in range(400):
+ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(int(os.environ.get("STEPS", "400")))]
+for t in range(int(os.environ.get("STEPS", "400"))):
     a = env.random_actions(t)
     ev[t][0].record()
     env.step(a)

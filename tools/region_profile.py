@@ -30,11 +30,15 @@ ia = h.index("Instructions Executed")
 ist = h.index("Warp Stall Sampling (All Samples)")
 txt = open(sass).read()
 fn = [p for p in re.split(r"//-+ \.text\.", txt) if p.startswith(KERNEL)][0]
-ins, cur = [], None
+INNER = "--inner" in sys.argv  # the innermost sim_step.cuh line of the inline chain (lambdas), not the outermost
+ins, cur, fresh = [], None, True
 for ln in fn.splitlines():
     m = re.search(r'//## File "([^"]+)", line (\d+)(?: inlined at "([^"]+)", line (\d+))?', ln)
     if m:
         f, l, fi, li = m.group(1), int(m.group(2)), m.group(3), m.group(4)
+        if INNER and not fresh:
+            continue
+        fresh = False
         if f.endswith("sim_step.cuh"):
             cur = l  # the step body is one inlined function: its own line is the useful one
         elif fi and fi.endswith("sim_step.cuh"):
@@ -42,6 +46,7 @@ for ln in fn.splitlines():
         else:
             cur = -1
         continue
+    fresh = True
     m = re.search(r"/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
     if m:
         ins.append((cur, m.group(2).strip()))
