@@ -68,6 +68,10 @@ struct Lane {
   __device__ __forceinline__ T& at(int row) const { return sm[row * 32 + lane]; }
   __device__ __forceinline__ T at_kid(int row, int k) const { return sm[row * 32 + base + k]; }
   __device__ __forceinline__ T& g(int row) const { return gs[row * W + b]; }
+  // rows [row, row + 2k) read as k float2 rows (fp32 packed coupling blocks)
+  __device__ __forceinline__ float2& g2(int row, int k) const {
+    return reinterpret_cast<float2*>(gs + row * W)[k * W + b];
+  }
 
   // contact slot k of this lane: 11 rows n(3) r(3) t1(3) d b, in shared memory
   // for k < CPB, in the global overflow rows (G_CT) beyond (terrain only)
@@ -1653,8 +1657,16 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
 #pragma unroll
                   for (int j = 0; j < 6; ++j) hx[i * 6 + j] += al[i] * be[j];
               }
+              if constexpr (sizeof(T) == 4) {  // row pairs (2 rp, 2 rp + 1) as float2 rows rp * 6 + c
 #pragma unroll
-              for (int k = 0; k < 36; ++k) L.g(G + 19 + k) = hx[k];
+                for (int rp = 0; rp < 3; ++rp)
+#pragma unroll
+                  for (int c = 0; c < 6; ++c)
+                    L.g2(G + 19, rp * 6 + c) = make_float2(hx[(2 * rp) * 6 + c], hx[(2 * rp + 1) * 6 + c]);
+              } else {
+#pragma unroll
+                for (int k = 0; k < 36; ++k) L.g(G + 19 + k) = hx[k];
+              }
             }
             isl_bar();
           }
@@ -1688,24 +1700,44 @@ __global__ void __launch_bounds__(ISL ? 32 * island_cap<T>() : kStepThreads, (si
           // y = Ahat v: the env's own blocks, plus in island mode the
           // inter-agent coupling blocks against the partners' v (exchange area)
           // island mode: += the inter-agent coupling blocks against the partners' v
+          // One-CTA islands alternate between two 6-entry halves of the
+          // exchange slots, so the barrier that protected their reuse is not
+          // needed (the island sum after every product orders it)
+          int xpar = 0;
           auto couple = [&](const T (&v)[6], T (&y)[6]) {
             if constexpr (ISL) {
-              T* my = xch + (isl_w * 32 + lane) * kXch;
+              const int h = bar_ctr ? 0 : 6 * xpar;
+              xpar ^= 1;
+              T* my = xch + (isl_w * 32 + lane) * kXch + h;
 #pragma unroll
               for (int k = 0; k < 6; ++k) my[k] = v[k];
               isl_bar();
               for (int s2 = 0; s2 < xc; ++s2) {
                 const int G = G_XS + kXSlotRows * s2;
-                const T* vp = xch + (int(L.g(G)) * 32 + int(L.g(G + 1))) * kXch;
+                const T* vp = xch + (int(L.g(G)) * 32 + int(L.g(G + 1))) * kXch + h;
+                if constexpr (sizeof(T) == 4) {  // packed row pairs: same products and order per row
+                  float2 acc[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-                for (int r = 0; r < 6; ++r) {
-                  T acc = T(0);
+                  for (int c = 0; c < 6; ++c)
 #pragma unroll
-                  for (int c = 0; c < 6; ++c) acc += L.g(G + 19 + r * 6 + c) * vp[c];
-                  y[r] += acc;
+                    for (int rp = 0; rp < 3; ++rp)
+                      acc[rp] = __ffma2_rn(L.g2(G + 19, rp * 6 + c), make_float2(vp[c], vp[c]), acc[rp]);
+#pragma unroll
+                  for (int rp = 0; rp < 3; ++rp) {
+                    y[2 * rp] += acc[rp].x;
+                    y[2 * rp + 1] += acc[rp].y;
+                  }
+                } else {
+#pragma unroll
+                  for (int r = 0; r < 6; ++r) {
+                    T acc = T(0);
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) acc += L.g(G + 19 + r * 6 + c) * vp[c];
+                    y[r] += acc;
+                  }
                 }
               }
-              isl_bar();
+              if (bar_ctr) isl_bar();
             }
           };
           auto apply_x = [&](const T (&v)[6], T (&y)[6]) {
