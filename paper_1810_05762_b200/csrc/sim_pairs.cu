@@ -325,7 +325,8 @@ __global__ void k_narrow(const int2* __restrict__ pairs, const int* __restrict__
 // contact slots (both sides) plus the env edge of every contact; persistent
 // warps loop over the device-counted candidate pairs (no host round trip).
 __global__ void k_narrow_slots(const int2* __restrict__ pairs, const int* __restrict__ n_pairs_p, int pair_cap,
-                               int B, long long NB, const WShape* __restrict__ ws, double margin,
+                               int B, long long NB, const WShape* __restrict__ ws, const double* __restrict__ env_box,
+                               double margin,
                                XSlot* __restrict__ xslots, int* __restrict__ xcount, int2* __restrict__ edges,
                                int edge_cap, int* __restrict__ n_edges, int* __restrict__ err) {
   pdl_wait();  // programmatic dependent launch (sim_launch.h)
@@ -336,11 +337,25 @@ __global__ void k_narrow_slots(const int2* __restrict__ pairs, const int* __rest
   if (blockIdx.x == 0 && threadIdx.x == 0 && *n_pairs_p > pair_cap) atomicOr(err, 8);  // candidates dropped
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < np; w += nwarps) {
     const int2 pr = pairs[w];
-    for (int u = lane; u < B * B; u += 32) {
-      const int ba = u / B, bb = u % B;
+    // exact pruning: a body pair can only overlap (AABBs within the margin) if
+    // each body's AABB overlaps the other env's AABB (the union of its bodies'),
+    // so only those bodies of either env are paired (crowded HFH: a few bodies
+    // near the other agent instead of all B x B)
+    bool ta = false, tb = false;
+    if (lane < B) {
+      const WShape& A = ws[size_t(pr.x) * B + lane];
+      const WShape& Bs = ws[size_t(pr.y) * B + lane];
+      const double la[6] = {A.lo[0], A.lo[1], A.lo[2], A.hi[0], A.hi[1], A.hi[2]};
+      const double lb[6] = {Bs.lo[0], Bs.lo[1], Bs.lo[2], Bs.hi[0], Bs.hi[1], Bs.hi[2]};
+      ta = A.ok && box_overlap(la, env_box + 6 * size_t(pr.y), margin);
+      tb = Bs.ok && box_overlap(lb, env_box + 6 * size_t(pr.x), margin);
+    }
+    const unsigned ma = __ballot_sync(0xffffffffu, ta), mb = __ballot_sync(0xffffffffu, tb);
+    const int na = __popc(ma), nb = __popc(mb);
+    for (int u = lane; u < na * nb; u += 32) {
+      const int ba = __fns(ma, 0, u / nb + 1), bb = __fns(mb, 0, u % nb + 1);
       const WShape& A = ws[size_t(pr.x) * B + ba];
       const WShape& Bs = ws[size_t(pr.y) * B + bb];
-      if (!A.ok || !Bs.ok) continue;
       const double la[6] = {A.lo[0], A.lo[1], A.lo[2], A.hi[0], A.hi[1], A.hi[2]};
       const double lb[6] = {Bs.lo[0], Bs.lo[1], Bs.lo[2], Bs.hi[0], Bs.hi[1], Bs.hi[2]};
       if (!box_overlap(la, lb, margin)) continue;
@@ -717,7 +732,8 @@ cudaError_t prepare_islands(PairScratch*& P, const DevModel<T>* model, int B, co
   const int edge_cap = n * B * kXSlots;
   STP_CK(broadphase<T>(P, model, state, origin, n, W, margin, st, P->xcount, P->icnt));
   STP_CK(launch_pdl(k_narrow_slots, dim3(148 * 2), dim3(256), 0, st, P->pairs, P->counters, int(P->pair_cap), B,
-                    (long long)n * B, P->ws, margin, P->xslots, P->xcount, P->edges, edge_cap, P->icnt, P->icnt + 2));
+                    (long long)n * B, P->ws, (const double*)P->env_box, margin, P->xslots, P->xcount, P->edges,
+                    edge_cap, P->icnt, P->icnt + 2));
   // labels in shared memory up to 48K envs (192 KB), else in global scratch
   const size_t lab_bytes = size_t(n) * sizeof(int);
   const bool lab_smem = lab_bytes <= 192 * 1024;
