@@ -282,18 +282,39 @@ struct PairContact {
 };
 
 // one warp per candidate env pair (A < B): every body pair, aabb test, narrow phase
+// a warp's candidate bodies of env pair pr: those whose AABB overlaps the
+// other env's AABB within the margin (exact pruning of the B x B body pairs,
+// see k_narrow_slots); bit b of the first / second mask: body b of pr.x / pr.y
+__device__ __forceinline__ void candidate_bodies(const int2 pr, int B, const WShape* __restrict__ ws,
+                                                 const double* __restrict__ env_box, double margin, int lane,
+                                                 unsigned& ma, unsigned& mb) {
+  bool ta = false, tb = false;
+  if (lane < B) {
+    const WShape& A = ws[size_t(pr.x) * B + lane];
+    const WShape& Bs = ws[size_t(pr.y) * B + lane];
+    const double la[6] = {A.lo[0], A.lo[1], A.lo[2], A.hi[0], A.hi[1], A.hi[2]};
+    const double lb[6] = {Bs.lo[0], Bs.lo[1], Bs.lo[2], Bs.hi[0], Bs.hi[1], Bs.hi[2]};
+    ta = A.ok && box_overlap(la, env_box + 6 * size_t(pr.y), margin);
+    tb = Bs.ok && box_overlap(lb, env_box + 6 * size_t(pr.x), margin);
+  }
+  ma = __ballot_sync(0xffffffffu, ta);
+  mb = __ballot_sync(0xffffffffu, tb);
+}
+
 __global__ void k_narrow(const int2* __restrict__ pairs, const int* __restrict__ n_pairs_p, int pair_cap, int B,
-                         long long NB, const WShape* __restrict__ ws, double margin, PairContact* __restrict__ out,
-                         int cap, int* __restrict__ n_out) {
+                         long long NB, const WShape* __restrict__ ws, const double* __restrict__ env_box,
+                         double margin, PairContact* __restrict__ out, int cap, int* __restrict__ n_out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int np = min(*n_pairs_p, pair_cap);
   if (warp >= np) return;
   const int2 pr = pairs[warp];
-  for (int u = lane; u < B * B; u += 32) {
-    const int ba = u / B, bb = u % B;
+  unsigned ma, mb;
+  candidate_bodies(pr, B, ws, env_box, margin, lane, ma, mb);
+  const int na = __popc(ma), nb = __popc(mb);
+  for (int u = lane; u < na * nb; u += 32) {
+    const int ba = __fns(ma, 0, u / nb + 1), bb = __fns(mb, 0, u % nb + 1);
     const WShape& A = ws[size_t(pr.x) * B + ba];
     const WShape& Bs = ws[size_t(pr.y) * B + bb];
-    if (!A.ok || !Bs.ok) continue;
     const double la[6] = {A.lo[0], A.lo[1], A.lo[2], A.hi[0], A.hi[1], A.hi[2]};
     const double lb[6] = {Bs.lo[0], Bs.lo[1], Bs.lo[2], Bs.hi[0], Bs.hi[1], Bs.hi[2]};
     if (!box_overlap(la, lb, margin)) continue;
@@ -341,16 +362,8 @@ __global__ void k_narrow_slots(const int2* __restrict__ pairs, const int* __rest
     // each body's AABB overlaps the other env's AABB (the union of its bodies'),
     // so only those bodies of either env are paired (crowded HFH: a few bodies
     // near the other agent instead of all B x B)
-    bool ta = false, tb = false;
-    if (lane < B) {
-      const WShape& A = ws[size_t(pr.x) * B + lane];
-      const WShape& Bs = ws[size_t(pr.y) * B + lane];
-      const double la[6] = {A.lo[0], A.lo[1], A.lo[2], A.hi[0], A.hi[1], A.hi[2]};
-      const double lb[6] = {Bs.lo[0], Bs.lo[1], Bs.lo[2], Bs.hi[0], Bs.hi[1], Bs.hi[2]};
-      ta = A.ok && box_overlap(la, env_box + 6 * size_t(pr.y), margin);
-      tb = Bs.ok && box_overlap(lb, env_box + 6 * size_t(pr.x), margin);
-    }
-    const unsigned ma = __ballot_sync(0xffffffffu, ta), mb = __ballot_sync(0xffffffffu, tb);
+    unsigned ma, mb;
+    candidate_bodies(pr, B, ws, env_box, margin, lane, ma, mb);
     const int na = __popc(ma), nb = __popc(mb);
     for (int u = lane; u < na * nb; u += 32) {
       const int ba = __fns(ma, 0, u / nb + 1), bb = __fns(mb, 0, u % nb + 1);
@@ -651,7 +664,8 @@ cudaError_t detect_pairs(PairScratch*& P, const DevModel<T>* model, int B, const
   *overflow = h_cnt[0] > int(pair_cap);
   if (np > 0) {
     k_narrow<<<(np * 32 + 127) / 128, 128, 0, st>>>(P->pairs, P->counters, int(pair_cap), B, (long long)n * B, P->ws,
-                                                    margin, P->cont, int(c_cap), P->counters + 1);
+                                                    (const double*)P->env_box, margin, P->cont, int(c_cap),
+                                                    P->counters + 1);
     STP_CK(cudaGetLastError());
   }
   STP_CK(cudaMemcpyAsync(h_cnt + 1, P->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
