@@ -897,10 +897,16 @@ int stp_step_host(stp_sim* s, const float* actions, float* obs, float* reward, u
     } else {
       CK(cudaMemcpyAsync(s->d_act, actions, N * s->J * sizeof(float), cudaMemcpyHostToDevice, s->stream));
     }
-    int rc = launch(s, 1, nullptr, s->d_act, obs ? s->d_obs : nullptr, rew_k, done_k, nullptr, s->stream);
+    // one launch: nothing overlaps a download at the end, so page-locked obs
+    // buffers are written by the kernels directly (the PCIe stores spread over
+    // the step) instead of one exposed copy
+    float* obs_z = obs ? static_cast<float*>(pinned_view(obs)) : nullptr;
+    int rc = launch(s, 1, nullptr, s->d_act, obs ? (obs_z ? obs_z : s->d_obs) : nullptr, rew_k, done_k, nullptr,
+                    s->stream);
     s->act_wait = nullptr;
     if (rc) return rc;
-    if (obs) CK(cudaMemcpyAsync(obs, s->d_obs, N * s->obs_dim * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+    if (obs && !obs_z)
+      CK(cudaMemcpyAsync(obs, s->d_obs, N * s->obs_dim * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
     if (reward && !rew_z) CK(cudaMemcpyAsync(reward, s->d_rew, N * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
     if (done && !done_z) CK(cudaMemcpyAsync(done, s->d_done, N, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
