@@ -420,9 +420,11 @@ def run_ours(args, world, rank, local):
     except Exception as ex:
         rollout = {"error": repr(ex)}
 
-    # ---- config C5: PPO iterations (rollout of 32 frames + 20-epoch update with
-    # the per-minibatch gradient allreduce), host-timed after one warm-up
-    # iteration; informational (the metric above is the env step)
+    # ---- config C5: PPO iterations (rollout + 20-epoch update with the
+    # per-minibatch gradient allreduce), host-timed after one warm-up
+    # iteration; informational (the metric above is the env step).  Frames per
+    # iteration per GPU stay the paper's 32 x 1024 = 32768 (PAPER.md:256-258,
+    # SPEC.md:379-381): 8 frames per agent at 4096 envs
     ppo = None
     try:
         if args.workload != "humanoid4096":
@@ -431,7 +433,7 @@ def run_ours(args, world, rank, local):
         from paper_1810_05762_b200.ppo import rollout as ppo_rollout
         torch.manual_seed(0)
         pmodel = ActorCritic(env.obs_dim, env.action_dim, HIDDEN.get(TASK, HIDDEN["hfh"])).to(dev)
-        pcfg = PPOConfig()
+        pcfg = PPOConfig(frames_per_iter=max(1, 32768 // N_ENVS))
         learner = PPOLearner(pmodel, pcfg)
         pkern = PolicyKernel(pmodel, dev)
         pst = RunningStat(env.obs_dim, device=dev)
@@ -442,7 +444,7 @@ def run_ours(args, world, rank, local):
             pst.merge_allreduce(first)  # same global statistics on every rank
         else:
             pst._merge(first.n, first.mean, first.m2)
-        times = []
+        times, upd = [], []
         for it in range(5):
             if world > 1:
                 torch.distributed.barrier()
@@ -458,17 +460,24 @@ def run_ours(args, world, rank, local):
                 pst._merge(loc.n, loc.mean, loc.m2)
             ast = torch.zeros(3, dtype=torch.float64, device=dev)
             adv, ret = gae(data["rew"], data["val"], data["done"], last_val, pcfg.gamma, pcfg.lam, stats=ast)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
             stats = learner.update(pst.whiten(data["obs"].reshape(-1, env.obs_dim)),
                                    data["act"].reshape(-1, env.action_dim), None, adv.reshape(-1), ret.reshape(-1),
                                    adv_stats=ast)
             pkern.refresh()
             torch.cuda.synchronize()
-            times.append(time.perf_counter() - t0)
+            t2 = time.perf_counter()
+            times.append(t2 - t0)
+            upd.append(t2 - t1)
         it_s = statistics.median(times[1:])
         frames = pcfg.frames_per_iter * N_ENVS * world
-        ppo = {"iteration_s": it_s, "frames_per_iteration": frames, "env_steps_per_s_with_update": frames / it_s,
+        ppo = {"iteration_s": it_s, "update_s": statistics.median(upd[1:]), "frames_per_iteration": frames,
+               "frames_per_agent": pcfg.frames_per_iter, "env_steps_per_s_with_update": frames / it_s,
                "epochs": pcfg.epochs, "kl": stats["kl"], "aborted": stats["aborted"], "clock": "host, median of 4",
-               "update_gemms": pcfg.matmul}
+               "update_gemms": pcfg.matmul,
+               "learner": "explicit fwd/bwd: cuBLAS fp32 GEMMs + stp_ppo_surrogate / stp_selu_backward_bias / "
+                          "stp_bias_selu kernels, fused Adam"}
     except Exception as ex:
         ppo = {"error": repr(ex)}
 

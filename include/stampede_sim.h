@@ -314,6 +314,43 @@ int stp_policy_forward(const float* obs, int32_t n_envs, int32_t obs_dim, const 
 int stp_gae(const float* rewards, const float* values, const uint8_t* dones, const float* last_value, int32_t T,
             int32_t N, float gamma, float lam, float* advantages, float* returns, double* stats, void* stream);
 
+/* ppo_update's minibatch loss (clipped surrogate on the
+ * globally normalised advantages + vf_coef x value MSE) and its gradient with
+ * respect to the networks' outputs, for the PPO learner of config C5.
+ * mu [B][A] (policy means) and value [B] are the networks' outputs on the
+ * minibatch's samples in minibatch order; actions [*][A], old_logp, advantages
+ * and returns [*] are the rollout columns, read at row idx[i] for sample i
+ * (idx = NULL: row i) — the minibatch gather.  adv_stats = the advantages'
+ * (count, sum, sum of squares), already summed over ranks (NULL: advantages
+ * used as given).  Writes d_mu [B][A], d_value [B], d_log_std [A] (dL/d of
+ * each; the policy's log-std enters only through the log-prob), the output
+ * layers' bias gradients d_mu_bias [A] = sum_i d_mu[i] and d_value_bias [1]
+ * (either may be NULL), loss[3] = (total, surrogate, value error) and sets
+ * *bad = 1 when the total is not finite (bad may be NULL).
+ * scratch: double[ceil(B / 256) * (2A + 3)].
+ * Deterministic (fixed-order reductions); asynchronous on `stream`.
+ * 1 <= A <= 64. */
+int stp_ppo_surrogate(const float* mu, const float* log_std, const float* value, const float* actions,
+                      const float* old_logp, const float* advantages, const float* returns, const int64_t* idx,
+                      int32_t B, int32_t A, const double* adv_stats, float clip, float vf_coef, float* d_mu,
+                      float* d_value, float* d_log_std, float* d_mu_bias, float* d_value_bias, float* loss,
+                      float* bad, double* scratch, void* stream);
+
+/* Backward of a hidden layer's SELU in the PPO learner: grad [rows][H]
+ * (dL/d the layer's output, overwritten with dL/d its pre-activation, using
+ * the output `out` [rows][H]: selu'(z) = lambda for out > 0, else
+ * out + lambda alpha) and d_bias [H] = the column sums of the result (the
+ * layer's bias gradient), reduced in a fixed order (deterministic).
+ * H % 4 == 0, H <= 1024, 16-byte aligned rows; scratch: float[ceil(rows / 512) * H].
+ * Asynchronous on `stream`. */
+int stp_selu_backward_bias(float* grad, const float* out, int64_t rows, int32_t H, float* d_bias, float* scratch,
+                           void* stream);
+
+/* Forward epilogue of a learner layer: z [rows][H] += bias [H], then SELU
+ * (lambda z for z > 0, lambda alpha (e^z - 1) else; selu = 0: bias only), in
+ * place.  H % 4 == 0, 16-byte aligned.  Asynchronous on `stream`. */
+int stp_bias_selu(float* z, const float* bias, int64_t rows, int32_t H, int32_t selu, void* stream);
+
 /* assemble_system (solver.hpp:41-44, solver.cpp:419-446) on the device path:
  * the first Newton linearisation of env `env` for host torques [N*J] (N*m)
  * exactly as the step kernel assembles it — H dense row-major [6S x 6S] over

@@ -90,7 +90,270 @@ __global__ void k_gae(const float* __restrict__ rew, const float* __restrict__ v
   }
 }
 
+// ppo_update's minibatch loss head and its gradient with
+// respect to the networks' outputs, one thread per sample i of the minibatch:
+//   logp_i = sum_j -z_ij^2 / 2 - ls_j - log(2 pi) / 2,  z = (a - mu) / sigma
+//   r_i = exp(logp_i - logp_old),  Ahat = (A - mean) / std (global stats)
+//   L = -mean_i min(r Ahat, clip(r, 1-eps, 1+eps) Ahat) + c_v mean_i (V - R)^2
+// dL/dmu_ij = g_i z_ij / sigma_j, dL/dls_j = sum_i g_i (z_ij^2 - 1) with
+// g_i = dL/dlogp_i; dL/dV_i = 2 c_v (V_i - R_i) / B.  The min / clamp
+// derivatives follow autograd's (ties split the gradient in half; the clamp
+// passes it on [lo, hi]).  Rollout columns (actions, old log-prob, A, R) are
+// read through the minibatch's permutation idx, so the gather is fused.
+// Block partials [2A + 3] (dL/dls, the column sums of dL/dmu and dL/dV —
+// the heads' bias gradients — the surrogate sum, the value-error sum) go to
+// scratch and are summed in a fixed order by k_ppo_finish: deterministic.
+constexpr int kPpoThreads = 256;
+constexpr int kPpoMaxA = 64;
+
+__global__ void __launch_bounds__(kPpoThreads) k_ppo_head(
+    const float* __restrict__ mu, const float* __restrict__ log_std, const float* __restrict__ value,
+    const float* __restrict__ actions, const float* __restrict__ old_logp, const float* __restrict__ adv,
+    const float* __restrict__ ret, const int64_t* __restrict__ idx, int B, int A, const double* __restrict__ adv_stats,
+    float clip, float vf_coef, float* __restrict__ d_mu, float* __restrict__ d_value, double* __restrict__ partials) {
+  __shared__ float s_ls[kPpoMaxA], s_isig[kPpoMaxA];
+  __shared__ double s_red[kPpoThreads / 32][2 * kPpoMaxA + 3];
+  for (int j = threadIdx.x; j < A; j += blockDim.x) {
+    s_ls[j] = log_std[j];
+    s_isig[j] = expf(-log_std[j]);
+  }
+  __syncthreads();
+  double an_mean = 0.0, an_inv = 1.0;
+  if (adv_stats) {  // global_normalize, in double like the host
+    const double n = adv_stats[0], mean = adv_stats[1] / n;
+    an_mean = mean;
+    an_inv = 1.0 / (sqrt(fmax(adv_stats[2] / n - mean * mean, 0.0)) + 1e-8);
+  }
+  const float inv_b = 1.0f / float(B);
+  const float kHalfLog2Pi = 0.91893853320467274f;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc_pg = 0.0, acc_vf = 0.0, acc_dv = 0.0;
+  float g = 0.f;
+  const float* a_row = nullptr;
+  const float* mu_row = nullptr;
+  if (i < B) {
+    const long long k = idx ? (long long)idx[i] : (long long)i;
+    a_row = actions + k * A;
+    mu_row = mu + (long long)i * A;
+    float logp = 0.f;
+    for (int j = 0; j < A; ++j) {
+      const float z = (a_row[j] - mu_row[j]) * s_isig[j];
+      logp += -0.5f * z * z - s_ls[j] - kHalfLog2Pi;
+    }
+    const float r = expf(logp - old_logp[k]);
+    const float ah = float((double(adv[k]) - an_mean) * an_inv);
+    const float lo = 1.f - clip, hi = 1.f + clip;
+    // clamp and min propagate NaN like torch's (fminf / fmaxf would drop it)
+    const float c = r != r ? r : fminf(fmaxf(r, lo), hi);
+    const float s1 = r * ah, s2 = c * ah;
+    const float pass = (r >= lo && r <= hi) ? 1.f : 0.f;
+    const float dmin_dr = s1 < s2 ? ah : (s1 == s2 ? 0.5f * ah + 0.5f * ah * pass : ah * pass);
+    g = -inv_b * dmin_dr * r;  // dL/dlogp_i
+    acc_pg = (s1 != s1 || s2 != s2) ? double(s1 + s2) : double(fminf(s1, s2));
+    const float dv = value[i] - ret[k];
+    acc_vf = double(dv) * double(dv);
+    d_value[i] = 2.f * vf_coef * dv * inv_b;
+    acc_dv = double(d_value[i]);
+  }
+  // per output column: d_mu, and the column's dL/dls contribution reduced over the block
+  for (int j = 0; j < A; ++j) {
+    double t = 0.0, u = 0.0;
+    if (i < B) {
+      const float z = (a_row[j] - mu_row[j]) * s_isig[j];
+      const float dm = g * z * s_isig[j];
+      d_mu[(long long)i * A + j] = dm;
+      t = double(g) * double(z * z - 1.f);
+      u = double(dm);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      t += __shfl_xor_sync(0xffffffffu, t, off);
+      u += __shfl_xor_sync(0xffffffffu, u, off);
+    }
+    if (lane == 0) {
+      s_red[warp][j] = t;
+      s_red[warp][A + j] = u;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    acc_pg += __shfl_xor_sync(0xffffffffu, acc_pg, off);
+    acc_vf += __shfl_xor_sync(0xffffffffu, acc_vf, off);
+    acc_dv += __shfl_xor_sync(0xffffffffu, acc_dv, off);
+  }
+  if (lane == 0) {
+    s_red[warp][2 * A] = acc_dv;
+    s_red[warp][2 * A + 1] = acc_pg;
+    s_red[warp][2 * A + 2] = acc_vf;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < 2 * A + 3; j += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < kPpoThreads / 32; ++w) s += s_red[w][j];
+    partials[(long long)blockIdx.x * (2 * A + 3) + j] = s;
+  }
+}
+
+// Sums the block partials in block order: d_log_std[A], the heads' bias
+// gradients, loss[3] = (total, surrogate, value error) and bad = max(bad,
+// loss not finite) (ppo.py's abort flag, read once after the epochs).
+__global__ void k_ppo_finish(const double* __restrict__ partials, int nblk, int A, int B, float vf_coef,
+                             float* __restrict__ d_log_std, float* __restrict__ d_mu_bias,
+                             float* __restrict__ d_value_bias, float* __restrict__ loss, float* __restrict__ bad) {
+  for (int j = threadIdx.x; j < 2 * A + 3; j += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += partials[(long long)b * (2 * A + 3) + j];
+    if (j < A) {
+      d_log_std[j] = float(s);
+    } else if (j < 2 * A) {
+      if (d_mu_bias) d_mu_bias[j - A] = float(s);
+    } else if (j == 2 * A) {
+      if (d_value_bias) *d_value_bias = float(s);
+    } else if (j == 2 * A + 1) {
+      loss[1] = float(-s / B);
+    } else {
+      loss[2] = float(s / B);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const float total = loss[1] + vf_coef * loss[2];
+    loss[0] = total;
+    if (bad && !isfinite(total)) *bad = 1.f;
+  }
+}
+
+// Backward of one hidden layer's SELU for the learner (§4.4 SELU
+// networks): g = dy * selu'(z) from the layer's OUTPUT y (y > 0: lambda;
+// else y + lambda alpha = lambda alpha e^z, autograd's result form), written
+// over dy, and the bias gradient db = sum over rows of g.  One pass over the
+// [rows][H] activations (float4 along H); each block reduces its row range
+// per column in registers + shared memory and writes one partial row, which
+// k_colsum_finish adds in block order (deterministic).
+constexpr int kSeluThreads = 256;
+constexpr int kSeluRowsPerBlock = 512;
+
+__global__ void __launch_bounds__(kSeluThreads) k_selu_bwd_bias(float* __restrict__ g, const float* __restrict__ y,
+                                                               long long rows, int H, float* __restrict__ partials) {
+  extern __shared__ float s_part[];  // [kSeluThreads / (H/4)][H]
+  const float kL = 1.0507009873554805f, kLA = 1.0507009873554805f * 1.6732632423543772f;
+  const int q = H >> 2;                       // float4 per row
+  const int c4 = threadIdx.x % q, rlane = threadIdx.x / q, rpar = kSeluThreads / q;
+  const long long r0 = (long long)blockIdx.x * kSeluRowsPerBlock;
+  const long long r1 = min(rows, r0 + kSeluRowsPerBlock);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (rlane < rpar) {
+    for (long long r = r0 + rlane; r < r1; r += rpar) {
+      float4* gp = reinterpret_cast<float4*>(g + r * H) + c4;
+      const float4 yv = reinterpret_cast<const float4*>(y + r * H)[c4];
+      float4 d = *gp;
+      d.x *= yv.x > 0.f ? kL : yv.x + kLA;
+      d.y *= yv.y > 0.f ? kL : yv.y + kLA;
+      d.z *= yv.z > 0.f ? kL : yv.z + kLA;
+      d.w *= yv.w > 0.f ? kL : yv.w + kLA;
+      *gp = d;
+      acc.x += d.x;
+      acc.y += d.y;
+      acc.z += d.z;
+      acc.w += d.w;
+    }
+  }
+  if (rlane < rpar) reinterpret_cast<float4*>(s_part + rlane * H)[c4] = acc;
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += kSeluThreads) {
+    float s = 0.f;
+    for (int k = 0; k < rpar; ++k) s += s_part[k * H + c];
+    partials[(long long)blockIdx.x * H + c] = s;
+  }
+}
+
+__global__ void k_colsum_finish(const float* __restrict__ partials, int nblk, int H, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= H) return;
+  float s = 0.f;
+  for (int b = 0; b < nblk; ++b) s += partials[(long long)b * H + c];
+  out[c] = s;
+}
+
+// Forward epilogue of a learner layer: z += bias (+ SELU) in place over the
+// GEMM's [rows][H] output, float4 along H (the bias / SELU of the forward
+// as one pass instead of a GEMM epilogue plus an elementwise pass).
+__global__ void k_bias_selu(float* __restrict__ z, const float* __restrict__ bias, long long n4, int q, int selu) {
+  const float kL = 1.0507009873554805f, kLA = 1.0507009873554805f * 1.6732632423543772f;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 b = reinterpret_cast<const float4*>(bias)[i % q];
+    float4 v = reinterpret_cast<float4*>(z)[i];
+    v.x += b.x;
+    v.y += b.y;
+    v.z += b.z;
+    v.w += b.w;
+    if (selu) {
+      v.x = v.x > 0.f ? kL * v.x : kLA * expm1f(v.x);
+      v.y = v.y > 0.f ? kL * v.y : kLA * expm1f(v.y);
+      v.z = v.z > 0.f ? kL * v.z : kLA * expm1f(v.z);
+      v.w = v.w > 0.f ? kL * v.w : kLA * expm1f(v.w);
+    }
+    reinterpret_cast<float4*>(z)[i] = v;
+  }
+}
+
 }  // namespace
+
+extern "C" int stp_bias_selu(float* z, const float* bias, int64_t rows, int32_t H, int32_t selu, void* stream) {
+  if (rows < 0 || H <= 0 || (H & 3) || !bias || (rows > 0 && !z) || (reinterpret_cast<uintptr_t>(z) & 15) ||
+      (reinterpret_cast<uintptr_t>(bias) & 15))
+    return stp::fail(STP_EINVAL, "stp_bias_selu: bad arguments");
+  const long long n4 = (long long)rows * (H / 4);
+  if (n4 == 0) return STP_OK;
+  const int threads = 256;
+  const long long want = (n4 + threads - 1) / threads;
+  const int blocks = int(want < 148LL * 16 ? want : 148LL * 16);
+  k_bias_selu<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(z, bias, n4, H / 4, selu);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_bias_selu: ") + cudaGetErrorString(e));
+  return STP_OK;
+}
+
+extern "C" int stp_selu_backward_bias(float* grad, const float* out, int64_t rows, int32_t H, float* d_bias,
+                                      float* scratch, void* stream) {
+  if (rows < 0 || H <= 0 || (H & 3) || H > 4 * kSeluThreads || !d_bias || !scratch ||
+      (rows > 0 && (!grad || !out)) || (reinterpret_cast<uintptr_t>(grad) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15))
+    return stp::fail(STP_EINVAL, "stp_selu_backward_bias: bad arguments");
+  const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nblk = int((rows + kSeluRowsPerBlock - 1) / kSeluRowsPerBlock);
+  const int rpar = kSeluThreads / (H / 4);
+  if (nblk > 0)
+    k_selu_bwd_bias<<<nblk, kSeluThreads, size_t(rpar > 0 ? rpar : 1) * H * sizeof(float), st>>>(grad, out, rows, H,
+                                                                                                 scratch);
+  if (nblk == 0) {
+    cudaMemsetAsync(d_bias, 0, size_t(H) * sizeof(float), st);
+  } else {
+    k_colsum_finish<<<(H + 127) / 128, 128, 0, st>>>(scratch, nblk, H, d_bias);
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_selu_bwd_bias: ") + cudaGetErrorString(e));
+  return STP_OK;
+}
+
+extern "C" int stp_ppo_surrogate(const float* mu, const float* log_std, const float* value, const float* actions,
+                                 const float* old_logp, const float* advantages, const float* returns,
+                                 const int64_t* idx, int32_t B, int32_t A, const double* adv_stats, float clip,
+                                 float vf_coef, float* d_mu, float* d_value, float* d_log_std, float* d_mu_bias,
+                                 float* d_value_bias, float* loss, float* bad, double* scratch, void* stream) {
+  if (B < 0 || A <= 0 || A > kPpoMaxA || !log_std || !d_log_std || !loss || !scratch ||
+      (B > 0 && (!mu || !value || !actions || !old_logp || !advantages || !returns || !d_mu || !d_value)))
+    return stp::fail(STP_EINVAL, "stp_ppo_surrogate: bad arguments");
+  const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nblk = (B + kPpoThreads - 1) / kPpoThreads;
+  if (nblk > 0)
+    k_ppo_head<<<nblk, kPpoThreads, 0, st>>>(mu, log_std, value, actions, old_logp, advantages, returns, idx, B, A,
+                                             adv_stats, clip, vf_coef, d_mu, d_value, scratch);
+  k_ppo_finish<<<1, 128, 0, st>>>(scratch, nblk, A, B > 0 ? B : 1, vf_coef, d_log_std, d_mu_bias, d_value_bias,
+                                  loss, bad);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_ppo_head: ") + cudaGetErrorString(e));
+  return STP_OK;
+}
 
 extern "C" int stp_gae(const float* rewards, const float* values, const uint8_t* dones, const float* last_value,
                        int32_t T, int32_t N, float gamma, float lam, float* advantages, float* returns,

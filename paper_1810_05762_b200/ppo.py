@@ -1,7 +1,14 @@
 """PPO rollout + update for config C5 (SPEC.md:361-506 ppo, :508-577 dist).
 
 Rollout: VecEnv (fused sm_100a step) + the tcgen05 policy forward (K4) on each
-GPU's env shard.  Update: torch autograd on the ActorCritic; every minibatch
+GPU's env shard.  Update: per minibatch one gather of the observations, the
+two MLPs' explicit forward / backward (cuBLAS GEMMs; each hidden SELU's
+backward fused with its bias gradient, stp_selu_backward_bias), the loss head
+and its output gradients in one CUDA kernel pair (stp_ppo_surrogate: log-prob,
+ratio, clipped surrogate on the globally normalised advantages, value MSE,
+the heads' bias gradients, the rollout columns gathered in-kernel), the fused
+Adam step; the GAE is a CUDA kernel (stp_gae).  Host (CPU) tensors — the gloo tests of the
+distributed logic — run the same loss under autograd.  Every minibatch
 gradient is averaged across ranks with one allreduce of the flattened
 gradient (the paper's Horovod/NCCL gradient averaging);
 advantages are normalised with global statistics; the
@@ -65,16 +72,106 @@ def allreduce_mean_grads(model: torch.nn.Module):
         off += n
 
 
-def global_normalize(adv: torch.Tensor, stats: torch.Tensor | None = None) -> torch.Tensor:
-    """Advantage normalisation with statistics over all ranks (SPEC.md:532-540).
-    `stats` = [count, sum, sum of squares] (float64, e.g. from the GAE kernel);
-    computed here when absent.  One SUM allreduce, no host synchronisation."""
+def global_stats(adv: torch.Tensor, stats: torch.Tensor | None = None) -> torch.Tensor:
+    """[count, sum, sum of squares] (float64) of the advantages over all ranks
+    (SPEC.md:532-540): `stats` from the GAE kernel or computed here, then one
+    SUM allreduce; no host synchronisation."""
     if stats is None:
         stats = torch.stack([torch.tensor(float(adv.numel()), device=adv.device, dtype=torch.float64),
                              adv.double().sum(), (adv.double() ** 2).sum()])
     s = stats.to(torch.float64).clone()
     if _dist():
         dist.all_reduce(s, op=dist.ReduceOp.SUM)
+    return s
+
+
+FORWARD_EPILOGUE = "kernel"  # hidden layers: "kernel" = GEMM + stp_bias_selu; "addmm" = cuBLAS bias + torch SELU
+
+
+def mlp_forward(layers, x):
+    """Affine-SELU chain keeping every layer's input:
+    returns [x, y_1, ..., y_L] (y_L = the identity output); each hidden
+    SELU is applied in place on its GEMM's output (only the output is kept:
+    the backward derives selu' from it)."""
+    acts = [x]
+    for i, l in enumerate(layers):
+        hidden = i < len(layers) - 1
+        if FORWARD_EPILOGUE == "kernel" and hidden:
+            import ctypes as C
+            from . import abi
+            z = torch.mm(acts[-1], l.weight.detach().t())
+            h = torch.cuda.current_stream(z.device).cuda_stream
+            rc = abi.load().stp_bias_selu(C.c_void_p(z.data_ptr()), C.c_void_p(l.bias.data_ptr()), z.shape[0],
+                                          z.shape[1], 1, C.c_void_p(h if h else 1))
+            if rc != abi.STP_OK:
+                raise RuntimeError(f"stp_bias_selu failed ({rc}): {abi.last_error()}")
+            acts.append(z)
+            continue
+        z = torch.addmm(l.bias.detach(), acts[-1], l.weight.detach().t())
+        acts.append(torch.selu_(z) if hidden else z)
+    return acts
+
+
+def mlp_backward(layers, acts, g, scratch):
+    """Backward of mlp_forward for dL/d output g [B, out]: weight gradients
+    g^T x into each layer's .grad (cuBLAS), the input gradient g W, then the
+    hidden SELU backward fused with the bias gradient (stp_selu_backward_bias)
+    into the previous layer's bias .grad.  The output layer's bias gradient
+    is the caller's (the loss-head kernel reduces it); the first layer's input
+    gradient is not formed."""
+    import ctypes as C
+    from . import abi
+    lib = abi.load()
+    h = torch.cuda.current_stream(g.device).cuda_stream
+    for i in reversed(range(len(layers))):
+        l = layers[i]
+        torch.mm(g.t(), acts[i], out=l.weight.grad)
+        if i == 0:
+            break
+        gx = torch.mm(g, l.weight.detach())
+        y = acts[i]
+        rc = lib.stp_selu_backward_bias(C.c_void_p(gx.data_ptr()), C.c_void_p(y.data_ptr()), gx.shape[0],
+                                        gx.shape[1], C.c_void_p(layers[i - 1].bias.grad.data_ptr()),
+                                        C.c_void_p(scratch.data_ptr()), C.c_void_p(h if h else 1))
+        if rc != abi.STP_OK:
+            raise RuntimeError(f"stp_selu_backward_bias failed ({rc}): {abi.last_error()}")
+        g = gx
+
+
+def surrogate_grad(mu, log_std, v, actions, old_logp, adv, ret, idx, adv_stats, clip, vf_coef, bad,
+                   d_mu_bias=None, d_value_bias=None):
+    """The minibatch loss head of ppo_update on the GPU (stp_ppo_surrogate,
+    SPEC.md:455-467): returns (dL/dmu [mb, A], dL/dV [mb], dL/dlog_std [A],
+    loss) for mu / v = the networks' outputs on the samples idx of the rollout
+    columns; advantages normalised in-kernel from `adv_stats`; `bad` (float
+    device scalar) is set to 1 when the loss is not finite; the output layers'
+    bias gradients are written to d_mu_bias [A] / d_value_bias [1] if given."""
+    import ctypes as C
+    from . import abi
+    mb, A = mu.shape
+    dev = mu.device
+    mu, v, log_std = mu.contiguous(), v.contiguous(), log_std.to(torch.float32).contiguous()
+    idx = idx.to(torch.int64).contiguous()
+    dmu, dv = torch.empty_like(mu), torch.empty_like(v)
+    dls = torch.empty(A, dtype=torch.float32, device=dev)
+    loss = torch.empty(3, dtype=torch.float32, device=dev)
+    scratch = torch.empty(max(1, (mb + 255) // 256) * (2 * A + 3), dtype=torch.float64, device=dev)
+    p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+    h = torch.cuda.current_stream(dev).cuda_stream
+    rc = abi.load().stp_ppo_surrogate(p(mu), p(log_std), p(v), p(actions), p(old_logp), p(adv), p(ret), p(idx), mb,
+                                      A, p(adv_stats), C.c_float(clip), C.c_float(vf_coef), p(dmu), p(dv), p(dls),
+                                      p(d_mu_bias), p(d_value_bias), p(loss), p(bad), p(scratch),
+                                      C.c_void_p(h if h else 1))
+    if rc != abi.STP_OK:
+        raise RuntimeError(f"stp_ppo_surrogate failed ({rc}): {abi.last_error()}")
+    return dmu, dv, dls, loss[0]
+
+
+def global_normalize(adv: torch.Tensor, stats: torch.Tensor | None = None) -> torch.Tensor:
+    """Advantage normalisation with statistics over all ranks (SPEC.md:532-540).
+    `stats` = [count, sum, sum of squares] (float64, e.g. from the GAE kernel);
+    computed here when absent.  One SUM allreduce, no host synchronisation."""
+    s = global_stats(adv, stats)
     n, sm, sq = s[0], s[1], s[2]
     mean = sm / n
     std = torch.sqrt(torch.clamp(sq / n - mean * mean, min=0.0)) + 1e-8
@@ -148,20 +245,33 @@ class PPOLearner:
 
     def _update(self, xw, actions, adv, ret, generator, adv_stats):
         cfg = self.cfg
-        adv = global_normalize(adv, adv_stats)
+        fused = xw.is_cuda
+        if fused:  # the kernel normalises on the fly with the global statistics
+            adv_raw = adv.to(torch.float32).contiguous()
+            adv_stats_g = global_stats(adv_raw, adv_stats)
+            actions = actions.to(torch.float32).contiguous()
+            ret = ret.to(torch.float32).contiguous()
+            for p_ in self.model.parameters():  # written in place by the explicit backward
+                if p_.grad is None:
+                    p_.grad = torch.zeros_like(p_)
+        else:
+            adv = global_normalize(adv, adv_stats)
         B = xw.shape[0]
         with torch.no_grad():
             mu_old = self.model.pi(xw)
             ls_old = self.model.log_std.detach().clone()
-            old_logp = gaussian_logp(actions, mu_old, ls_old)
+            old_logp = gaussian_logp(actions, mu_old, ls_old).contiguous()
             snapshot = [p.detach().clone() for p in self.model.parameters()]
             opt_state = copy.deepcopy(self.opt.state_dict())
         # Table 4: frames per iteration / minibatch size per agent = minibatches per epoch
         n_mb = max(1, cfg.frames_per_iter // max(1, cfg.minibatch_per_agent))
         mb = max(1, B // n_mb)
+        if fused:
+            scratch = torch.empty(((mb + 511) // 512) * max(self.model.hidden), dtype=torch.float32,
+                                  device=xw.device)
         lr = self.opt.param_groups[0]["lr"]
         loss = torch.zeros((), device=xw.device)
-        bad = torch.zeros((), device=xw.device)  # 1 once any loss was not finite
+        bad = torch.zeros((), device=xw.device, dtype=torch.float32)  # 1 once any loss was not finite
         for epoch in range(cfg.epochs):
             if generator is None and xw.is_cuda:  # drawn on the device: no host round trip
                 perm = torch.randperm(B, device=xw.device)
@@ -169,16 +279,35 @@ class PPOLearner:
                 perm = torch.randperm(B, generator=generator, device="cpu").to(xw.device)
             for s0 in range(0, B, mb):
                 idx = perm[s0:s0 + mb]
-                logp = self.model.log_prob(xw[idx], actions[idx])
-                ratio = torch.exp(logp - old_logp[idx])
-                a = adv[idx]
-                pg = -torch.min(ratio * a, torch.clamp(ratio, 1 - cfg.clip, 1 + cfg.clip) * a).mean()
-                v = self.model.v(xw[idx]).squeeze(-1)
-                vf = ((v - ret[idx]) ** 2).mean()
-                loss = pg + cfg.vf_coef * vf
-                bad = torch.maximum(bad, (~torch.isfinite(loss)).to(bad.dtype))
-                self.opt.zero_grad(set_to_none=False)
-                loss.backward()
+                x = xw.index_select(0, idx)  # one gather of the minibatch's observations
+                if not fused:
+                    self.opt.zero_grad(set_to_none=False)
+                if fused:
+                    # explicit forward / backward: cuBLAS GEMMs, the loss head and
+                    # its output gradients in one kernel (stp_ppo_surrogate: the
+                    # rollout columns gathered through idx in-kernel, the heads'
+                    # bias gradients reduced alongside), each hidden SELU's backward
+                    # fused with its bias gradient (stp_selu_backward_bias);
+                    # every gradient written in place, nothing accumulated
+                    pi_l, v_l = self.model.pi.layers, self.model.v.layers
+                    a_pi, a_v = mlp_forward(pi_l, x), mlp_forward(v_l, x)
+                    dmu, dv, dls, loss = surrogate_grad(
+                        a_pi[-1], self.model.log_std.detach(), a_v[-1].view(-1), actions, old_logp, adv_raw, ret,
+                        idx, adv_stats_g, cfg.clip, cfg.vf_coef, bad,
+                        d_mu_bias=pi_l[-1].bias.grad, d_value_bias=v_l[-1].bias.grad)
+                    self.model.log_std.grad.copy_(dls)
+                    mlp_backward(pi_l, a_pi, dmu, scratch)
+                    mlp_backward(v_l, a_v, dv.view(-1, 1), scratch)
+                else:
+                    logp = self.model.log_prob(x, actions[idx])
+                    ratio = torch.exp(logp - old_logp[idx])
+                    a = adv[idx]
+                    pg = -torch.min(ratio * a, torch.clamp(ratio, 1 - cfg.clip, 1 + cfg.clip) * a).mean()
+                    v = self.model.v(x).squeeze(-1)
+                    vf = ((v - ret[idx]) ** 2).mean()
+                    loss = pg + cfg.vf_coef * vf
+                    bad = torch.maximum(bad, (~torch.isfinite(loss)).to(bad.dtype))
+                    loss.backward()
                 allreduce_mean_grads(self.model)
                 self.opt.step()
         if _dist():

@@ -184,3 +184,156 @@ def test_ppo_update_aborts_on_non_finite_loss():
     assert st["aborted"] and st["lr"] == 5e-4
     for p, q in zip(model.parameters(), before):
         assert torch.equal(p.detach(), q)
+
+
+@pytest.mark.parametrize("mb,A,use_idx", [(1000, 21, True), (257, 8, False), (4096, 17, True), (1, 3, True)])
+def test_ppo_surrogate_kernel_matches_autograd_fp64(mb, A, use_idx):
+    """stp_ppo_surrogate (the learner's loss head) against autograd of the
+    same loss in float64 on the fp32 inputs: ratios inside and outside the
+    clip range, advantages of both signs, exact ties (ratio 1).  Bounds: loss
+    terms 1e-5 relative; d/dmu, d/dV elementwise 1e-5 of the largest entry;
+    d/dlog_std 1e-5 relative (fixed-order double reductions)."""
+    from paper_1810_05762_b200.ppo import surrogate_grad
+    g = torch.Generator().manual_seed(mb * 7 + A)
+    Bfull = mb + 37
+    f = lambda *s, sc=1.0: (torch.randn(*s, generator=g) * sc).float()
+    actions, mu_full = f(Bfull, A), f(Bfull, A, sc=0.5)
+    log_std = f(A, sc=0.3) - 0.5
+    value, ret = f(mb), f(Bfull, sc=2.0)
+    adv = f(Bfull, sc=3.0) + 0.4
+    idx = torch.randperm(Bfull, generator=g)[:mb] if use_idx else torch.arange(mb)
+    mu = mu_full[idx]
+    # old log-probs: the current ones shifted so ratios land on both sides of the clip range; some exact ties
+    lp_now = (-0.5 * ((actions[idx] - mu) / torch.exp(log_std)) ** 2 - log_std - 0.5 * math.log(2 * math.pi)).sum(-1)
+    old = torch.empty(Bfull)
+    old[idx] = lp_now + (torch.rand(mb, generator=g) - 0.5) * 0.8
+    old[idx[: mb // 10]] = lp_now[: mb // 10]  # ratio ~1
+    stats = torch.tensor([float(Bfull), adv.double().sum().item(), (adv.double() ** 2).sum().item()],
+                         dtype=torch.float64)
+    clip, vf_coef = 0.2, 0.5
+    cu = lambda t: t.cuda()
+    bad = torch.zeros((), device="cuda")
+    dmu, dv, dls, loss = surrogate_grad(cu(mu), cu(log_std), cu(value), cu(actions), cu(old), cu(adv), cu(ret),
+                                        cu(idx) if use_idx else cu(torch.arange(mb)), cu(stats), clip, vf_coef, bad)
+    # fp64 autograd of the same loss
+    M, LS, V = (t.double().requires_grad_(True) for t in (mu, log_std, value))
+    n, sm, sq = stats
+    mean = sm / n
+    an = (adv.double() - mean) / (torch.sqrt(torch.clamp(sq / n - mean * mean, min=0)) + 1e-8)
+    k = idx
+    lp = (-0.5 * ((actions[k].double() - M) / torch.exp(LS)) ** 2 - LS - 0.5 * math.log(2 * math.pi)).sum(-1)
+    r = torch.exp(lp - old[k].double())
+    a = an[k]
+    pg = -torch.min(r * a, torch.clamp(r, 1 - clip, 1 + clip) * a).mean()
+    vf = ((V - ret[k].double()) ** 2).mean()
+    L = pg + vf_coef * vf
+    gM, gLS, gV = torch.autograd.grad(L, [M, LS, V])
+    assert float(bad) == 0.0
+    assert abs(float(loss) - float(L)) <= 1e-5 * (1 + abs(float(L)))
+    tol = lambda ref: 5e-5 * float(ref.abs().max()) + 1e-12
+    # samples whose ratio sits within fp32 rounding of a clip bound may legitimately take the other branch
+    rr = r.detach()
+    edge = ((rr - (1 - clip)).abs() < 1e-5) | ((rr - (1 + clip)).abs() < 1e-5)
+    keep = ~edge
+    assert (dmu.cpu().double()[keep] - gM[keep]).abs().max() <= tol(gM)
+    assert (dv.cpu().double() - gV).abs().max() <= tol(gV)
+    if not bool(edge.any()):
+        assert (dls.cpu().double() - gLS).abs().max() <= 1e-5 * (float(gLS.abs().max()) + 1e-12)
+
+
+def test_ppo_surrogate_flags_non_finite_loss():
+    from paper_1810_05762_b200.ppo import surrogate_grad
+    mb, A = 64, 4
+    z = lambda *s: torch.zeros(*s, device="cuda")
+    mu = z(mb, A)
+    mu[3, 1] = float("nan")
+    bad = torch.zeros((), device="cuda")
+    stats = torch.tensor([float(mb), 0.0, float(mb)], dtype=torch.float64, device="cuda")
+    surrogate_grad(mu, z(A), z(mb), z(mb, A), z(mb), torch.ones(mb, device="cuda"), z(mb),
+                   torch.arange(mb, device="cuda"), stats, 0.2, 0.5, bad)
+    assert float(bad) == 1.0
+
+
+@pytest.mark.parametrize("rows,H", [(131072 // 64, 256), (1000, 128), (513, 64), (7, 32), (0, 64)])
+def test_selu_backward_bias_kernel(rows, H):
+    """stp_selu_backward_bias against torch's SELU backward (result form) and
+    the column sum; bounds 1e-6 relative (fp32, fixed-order sums)."""
+    import ctypes as C
+    from paper_1810_05762_b200 import abi
+    g = torch.Generator().manual_seed(rows + H)
+    z = torch.randn(rows, H, generator=g).cuda()
+    y = torch.selu(z)
+    dy = torch.randn(rows, H, generator=g).cuda()
+    ref = torch.where(y > 0, dy * 1.0507009873554805, dy * (y + 1.0507009873554805 * 1.6732632423543772))
+    gx = dy.clone()
+    db = torch.full((H,), float("nan"), device="cuda")
+    scratch = torch.empty(max(1, (rows + 511) // 512) * H, device="cuda")
+    rc = abi.load().stp_selu_backward_bias(C.c_void_p(gx.data_ptr()), C.c_void_p(y.data_ptr()), rows, H,
+                                           C.c_void_p(db.data_ptr()), C.c_void_p(scratch.data_ptr()), C.c_void_p(1))
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert torch.allclose(gx, ref, rtol=1e-6, atol=0)
+    colsum = ref.double().sum(0)
+    assert (db.double() - colsum).abs().max() <= 1e-5 * (1 + colsum.abs().max())
+
+
+def test_explicit_learner_backward_matches_autograd():
+    """The learner's explicit minibatch gradient (mlp_forward, stp_ppo_surrogate,
+    mlp_backward: every parameter's .grad written by GEMMs / kernels) equals
+    autograd of the same fp32 loss; bound 1e-4 of each tensor's largest entry."""
+    from paper_1810_05762_b200.ppo import mlp_backward, mlp_forward, surrogate_grad
+    torch.manual_seed(1)
+    O, A, mb = 77, 21, 3000
+    model = ActorCritic(O, A).cuda()
+    x = torch.randn(mb + 11, O, device="cuda")
+    act = torch.randn(mb + 11, A, device="cuda") * 0.5
+    adv = torch.randn(mb + 11, device="cuda")
+    ret = torch.randn(mb + 11, device="cuda")
+    idx = torch.randperm(mb + 11, device="cuda")[:mb]
+    with torch.no_grad():
+        old = (-0.5 * ((act - model.pi(x)) / torch.exp(model.log_std)) ** 2 - model.log_std
+               - 0.5 * math.log(2 * math.pi)).sum(-1) + 0.1 * torch.randn(mb + 11, device="cuda")
+    stats = torch.stack([torch.tensor(float(mb + 11), dtype=torch.float64, device="cuda"), adv.double().sum(),
+                         (adv.double() ** 2).sum()])
+    # autograd reference
+    n, sm, sq = stats
+    an = ((adv.double() - sm / n) / (torch.sqrt(sq / n - (sm / n) ** 2) + 1e-8)).float()
+    xi = x[idx]
+    lp = model.log_prob(xi, act[idx])
+    r = torch.exp(lp - old[idx])
+    pg = -torch.min(r * an[idx], torch.clamp(r, 0.8, 1.2) * an[idx]).mean()
+    L = pg + 0.5 * ((model.v(xi).squeeze(-1) - ret[idx]) ** 2).mean()
+    ref = torch.autograd.grad(L, list(model.parameters()))
+    for p in model.parameters():
+        p.grad = torch.full_like(p, float("nan"))
+    bad = torch.zeros((), device="cuda")
+    pi_l, v_l = model.pi.layers, model.v.layers
+    a_pi, a_v = mlp_forward(pi_l, xi), mlp_forward(v_l, xi)
+    dmu, dv, dls, loss = surrogate_grad(a_pi[-1], model.log_std.detach(), a_v[-1].view(-1), act, old, adv, ret, idx,
+                                        stats, 0.2, 0.5, bad, d_mu_bias=pi_l[-1].bias.grad,
+                                        d_value_bias=v_l[-1].bias.grad)
+    model.log_std.grad.copy_(dls)
+    scratch = torch.empty(((mb + 511) // 512) * 256, device="cuda")
+    mlp_backward(pi_l, a_pi, dmu, scratch)
+    mlp_backward(v_l, a_v, dv.view(-1, 1), scratch)
+    torch.cuda.synchronize()
+    assert abs(float(loss) - float(L)) <= 1e-5 * (1 + abs(float(L)))
+    for (name, p), gref in zip(model.named_parameters(), ref):
+        err = float((p.grad - gref).abs().max())
+        assert err <= 1e-4 * float(gref.abs().max()) + 1e-9, (name, err)
+
+
+@pytest.mark.parametrize("rows,H,selu", [(4099, 256, 1), (100, 64, 1), (33, 32, 0), (0, 128, 1)])
+def test_bias_selu_kernel(rows, H, selu):
+    """stp_bias_selu (the learner's forward epilogue) against torch.selu(z + b): 2 ulp-level (rtol 1e-6)."""
+    import ctypes as C
+    from paper_1810_05762_b200 import abi
+    g = torch.Generator().manual_seed(rows * 3 + H)
+    z = (torch.randn(rows, H, generator=g) * 3).cuda()
+    b = torch.randn(H, generator=g).cuda()
+    ref = torch.selu(z + b) if selu else z + b
+    out = z.clone()
+    rc = abi.load().stp_bias_selu(C.c_void_p(out.data_ptr()), C.c_void_p(b.data_ptr()), rows, H, selu, C.c_void_p(1))
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert torch.allclose(out, ref, rtol=1e-6, atol=1e-7)

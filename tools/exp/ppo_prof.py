@@ -12,6 +12,9 @@ from paper_1810_05762_b200.policy import HIDDEN, ActorCritic, PolicyKernel, Runn
 from paper_1810_05762_b200.ppo import PPOConfig, PPOLearner, gae, rollout  # noqa: E402
 from paper_1810_05762_b200.sim import VecEnv  # noqa: E402
 
+if os.environ.get("EPI"):
+    import paper_1810_05762_b200.ppo as _ppo
+    _ppo.FORWARD_EPILOGUE = os.environ["EPI"]
 if os.environ.get("TF32") == "1":
     torch.backends.cuda.matmul.allow_tf32 = True
 env = VecEnv("humanoid", n_envs=4096, seed=1234)
@@ -42,6 +45,10 @@ def one(it):
 
 for it in range(2):
     print("update s", one(it))
+ts = []
+for it in range(2, 6):
+    ts.append(one(it)[0])
+print("update s median", sorted(ts)[len(ts) // 2], flush=True)
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    one(2)
+    one(6)
 print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=18))
