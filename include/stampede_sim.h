@@ -327,9 +327,9 @@ int stp_gae(const float* rewards, const float* values, const uint8_t* dones, con
  * layers' bias gradients d_mu_bias [A] = sum_i d_mu[i] and d_value_bias [1]
  * (either may be NULL), loss[3] = (total, surrogate, value error) and sets
  * *bad = 1 when the total is not finite (bad may be NULL).
- * scratch: double[ceil(B / 256) * (2A + 3)].
+ * scratch: double[ceil(B / 128) * (2A + 3)].
  * Deterministic (fixed-order reductions); asynchronous on `stream`.
- * 1 <= A <= 64. */
+ * 1 <= A <= 32. */
 int stp_ppo_surrogate(const float* mu, const float* log_std, const float* value, const float* actions,
                       const float* old_logp, const float* advantages, const float* returns, const int64_t* idx,
                       int32_t B, int32_t A, const double* adv_stats, float clip, float vf_coef, float* d_mu,
@@ -341,7 +341,7 @@ int stp_ppo_surrogate(const float* mu, const float* log_std, const float* value,
  * the output `out` [rows][H]: selu'(z) = lambda for out > 0, else
  * out + lambda alpha) and d_bias [H] = the column sums of the result (the
  * layer's bias gradient), reduced in a fixed order (deterministic).
- * H % 4 == 0, H <= 1024, 16-byte aligned rows; scratch: float[ceil(rows / 512) * H].
+ * H % 4 == 0, H <= 1024, 16-byte aligned rows; scratch: float[592 * H].
  * Asynchronous on `stream`. */
 int stp_selu_backward_bias(float* grad, const float* out, int64_t rows, int32_t H, float* d_bias, float* scratch,
                            void* stream);

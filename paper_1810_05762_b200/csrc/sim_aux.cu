@@ -103,8 +103,12 @@ __global__ void k_gae(const float* __restrict__ rew, const float* __restrict__ v
 // Block partials [2A + 3] (dL/dls, the column sums of dL/dmu and dL/dV —
 // the heads' bias gradients — the surrogate sum, the value-error sum) go to
 // scratch and are summed in a fixed order by k_ppo_finish: deterministic.
-constexpr int kPpoThreads = 256;
-constexpr int kPpoMaxA = 64;
+// The tile's mu rows (contiguous), gathered action rows and the d_mu
+// result move through shared memory with coalesced loads / stores (row
+// stride A | 1 words: conflict-free column reads); the per-sample math reads
+// the tiles.
+constexpr int kPpoThreads = 128;
+constexpr int kPpoMaxA = 32;
 
 __global__ void __launch_bounds__(kPpoThreads) k_ppo_head(
     const float* __restrict__ mu, const float* __restrict__ log_std, const float* __restrict__ value,
@@ -112,10 +116,22 @@ __global__ void __launch_bounds__(kPpoThreads) k_ppo_head(
     const float* __restrict__ ret, const int64_t* __restrict__ idx, int B, int A, const double* __restrict__ adv_stats,
     float clip, float vf_coef, float* __restrict__ d_mu, float* __restrict__ d_value, double* __restrict__ partials) {
   __shared__ float s_ls[kPpoMaxA], s_isig[kPpoMaxA];
-  __shared__ double s_red[kPpoThreads / 32][2 * kPpoMaxA + 3];
+  __shared__ float s_mu[kPpoThreads * (kPpoMaxA + 1)], s_a[kPpoThreads * (kPpoMaxA + 1)];
+  __shared__ long long s_row[kPpoThreads];
+  __shared__ double s_red[kPpoThreads / 32][3];
+  const int SA = A | 1;
+  const int i0 = blockIdx.x * kPpoThreads;
+  const int nrow = min(kPpoThreads, B - i0);
   for (int j = threadIdx.x; j < A; j += blockDim.x) {
     s_ls[j] = log_std[j];
     s_isig[j] = expf(-log_std[j]);
+  }
+  if (threadIdx.x < nrow) s_row[threadIdx.x] = idx ? (long long)idx[i0 + threadIdx.x] : (long long)(i0 + threadIdx.x);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nrow * A; e += kPpoThreads) {  // coalesced tile loads
+    const int r = e / A, c = e - r * A;
+    s_mu[r * SA + c] = mu[(long long)i0 * A + e];
+    s_a[r * SA + c] = actions[s_row[r] * A + c];
   }
   __syncthreads();
   double an_mean = 0.0, an_inv = 1.0;
@@ -126,16 +142,14 @@ __global__ void __launch_bounds__(kPpoThreads) k_ppo_head(
   }
   const float inv_b = 1.0f / float(B);
   const float kHalfLog2Pi = 0.91893853320467274f;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = threadIdx.x, i = i0 + t;
+  const int lane = t & 31, warp = t >> 5;
   double acc_pg = 0.0, acc_vf = 0.0, acc_dv = 0.0;
   float g = 0.f;
-  const float* a_row = nullptr;
-  const float* mu_row = nullptr;
-  if (i < B) {
-    const long long k = idx ? (long long)idx[i] : (long long)i;
-    a_row = actions + k * A;
-    mu_row = mu + (long long)i * A;
+  float* a_row = s_a + t * SA;
+  float* mu_row = s_mu + t * SA;
+  if (t < nrow) {
+    const long long k = s_row[t];
     float logp = 0.f;
     for (int j = 0; j < A; ++j) {
       const float z = (a_row[j] - mu_row[j]) * s_isig[j];
@@ -153,26 +167,17 @@ __global__ void __launch_bounds__(kPpoThreads) k_ppo_head(
     acc_pg = (s1 != s1 || s2 != s2) ? double(s1 + s2) : double(fminf(s1, s2));
     const float dv = value[i] - ret[k];
     acc_vf = double(dv) * double(dv);
-    d_value[i] = 2.f * vf_coef * dv * inv_b;
-    acc_dv = double(d_value[i]);
+    const float dvo = 2.f * vf_coef * dv * inv_b;
+    d_value[i] = dvo;
+    acc_dv = double(dvo);
   }
-  // per output column: d_mu, and the column's dL/dls contribution reduced over the block
-  for (int j = 0; j < A; ++j) {
-    double t = 0.0, u = 0.0;
-    if (i < B) {
+  // per output column: d_mu into the mu tile and g (z^2 - 1) into the action
+  // tile, in place (each entry is read before it is overwritten)
+  if (t < nrow) {
+    for (int j = 0; j < A; ++j) {
       const float z = (a_row[j] - mu_row[j]) * s_isig[j];
-      const float dm = g * z * s_isig[j];
-      d_mu[(long long)i * A + j] = dm;
-      t = double(g) * double(z * z - 1.f);
-      u = double(dm);
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-      t += __shfl_xor_sync(0xffffffffu, t, off);
-      u += __shfl_xor_sync(0xffffffffu, u, off);
-    }
-    if (lane == 0) {
-      s_red[warp][j] = t;
-      s_red[warp][A + j] = u;
+      mu_row[j] = g * z * s_isig[j];
+      a_row[j] = g * (z * z - 1.f);
     }
   }
   for (int off = 16; off > 0; off >>= 1) {
@@ -181,41 +186,72 @@ __global__ void __launch_bounds__(kPpoThreads) k_ppo_head(
     acc_dv += __shfl_xor_sync(0xffffffffu, acc_dv, off);
   }
   if (lane == 0) {
-    s_red[warp][2 * A] = acc_dv;
-    s_red[warp][2 * A + 1] = acc_pg;
-    s_red[warp][2 * A + 2] = acc_vf;
+    s_red[warp][0] = acc_dv;
+    s_red[warp][1] = acc_pg;
+    s_red[warp][2] = acc_vf;
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < 2 * A + 3; j += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < kPpoThreads / 32; ++w) s += s_red[w][j];
-    partials[(long long)blockIdx.x * (2 * A + 3) + j] = s;
+  for (int e = threadIdx.x; e < nrow * A; e += kPpoThreads) {  // coalesced d_mu store
+    const int r = e / A, c = e - r * A;
+    d_mu[(long long)i0 * A + e] = s_mu[r * SA + c];
+  }
+  // column sums of the two tiles (dL/dls, then dL/dmu): warp w takes columns
+  // w, w + 4, ...; lane l adds rows l, l + 32, ... in double, then a fixed tree
+  double* out = partials + (long long)blockIdx.x * (2 * A + 3);
+  for (int col = warp; col < 2 * A; col += kPpoThreads / 32) {
+    const float* tile = col < A ? s_a + col : s_mu + (col - A);
+    double sm = 0.0;
+    for (int r = lane; r < nrow; r += 32) sm += double(tile[r * SA]);
+    for (int off = 16; off > 0; off >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, off);
+    if (lane == 0) out[col] = sm;
+  }
+  if (threadIdx.x < 3) {
+    double sm = 0.0;
+    for (int w = 0; w < kPpoThreads / 32; ++w) sm += s_red[w][threadIdx.x];
+    out[2 * A + threadIdx.x] = sm;
   }
 }
 
-// Sums the block partials in block order: d_log_std[A], the heads' bias
-// gradients, loss[3] = (total, surrogate, value error) and bad = max(bad,
-// loss not finite) (ppo.py's abort flag, read once after the epochs).
-__global__ void k_ppo_finish(const double* __restrict__ partials, int nblk, int A, int B, float vf_coef,
-                             float* __restrict__ d_log_std, float* __restrict__ d_mu_bias,
-                             float* __restrict__ d_value_bias, float* __restrict__ loss, float* __restrict__ bad) {
-  for (int j = threadIdx.x; j < 2 * A + 3; j += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += partials[(long long)b * (2 * A + 3) + j];
-    if (j < A) {
-      d_log_std[j] = float(s);
-    } else if (j < 2 * A) {
-      if (d_mu_bias) d_mu_bias[j - A] = float(s);
-    } else if (j == 2 * A) {
-      if (d_value_bias) *d_value_bias = float(s);
-    } else if (j == 2 * A + 1) {
-      loss[1] = float(-s / B);
-    } else {
-      loss[2] = float(s / B);
-    }
-  }
+// Sums the block partials: d_log_std[A], the heads' bias gradients, loss[3]
+// = (total, surrogate, value error) and bad = max(bad, loss not finite)
+// (ppo.py's abort flag, read once after the epochs).  Block c < 2A + 1 owns
+// column c, the last block the two loss columns; each column is summed by
+// 256 threads in a fixed order (strided partial sums, then a fixed tree):
+// deterministic.
+__device__ double colsum_fixed(const double* __restrict__ partials, int nblk, int ncol, int c, double* s_tree) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += partials[(long long)b * ncol + c];
+  s_tree[threadIdx.x] = s;
   __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) s_tree[threadIdx.x] += s_tree[threadIdx.x + h];
+    __syncthreads();
+  }
+  const double r = s_tree[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) k_ppo_finish(const double* __restrict__ partials, int nblk, int A, int B,
+                                                    float vf_coef, float* __restrict__ d_log_std,
+                                                    float* __restrict__ d_mu_bias, float* __restrict__ d_value_bias,
+                                                    float* __restrict__ loss, float* __restrict__ bad) {
+  __shared__ double s_tree[256];
+  const int ncol = 2 * A + 3, c = blockIdx.x;
+  if (c < 2 * A + 1) {
+    const double s = colsum_fixed(partials, nblk, ncol, c, s_tree);
+    if (threadIdx.x == 0) {
+      if (c < A) d_log_std[c] = float(s);
+      else if (c < 2 * A) { if (d_mu_bias) d_mu_bias[c - A] = float(s); }
+      else if (d_value_bias) *d_value_bias = float(s);
+    }
+    return;
+  }
+  const double pg = colsum_fixed(partials, nblk, ncol, 2 * A + 1, s_tree);
+  const double vf = colsum_fixed(partials, nblk, ncol, 2 * A + 2, s_tree);
   if (threadIdx.x == 0) {
+    loss[1] = float(-pg / B);
+    loss[2] = float(vf / B);
     const float total = loss[1] + vf_coef * loss[2];
     loss[0] = total;
     if (bad && !isfinite(total)) *bad = 1.f;
@@ -230,21 +266,23 @@ __global__ void k_ppo_finish(const double* __restrict__ partials, int nblk, int 
 // per column in registers + shared memory and writes one partial row, which
 // k_colsum_finish adds in block order (deterministic).
 constexpr int kSeluThreads = 256;
-constexpr int kSeluRowsPerBlock = 512;
+constexpr int kSeluBlocks = 148 * 4;  // 4 blocks per SM; the row split depends only on rows and H
 
 __global__ void __launch_bounds__(kSeluThreads) k_selu_bwd_bias(float* __restrict__ g, const float* __restrict__ y,
-                                                               long long rows, int H, float* __restrict__ partials) {
+                                                               long long rows, int H, long long rows_per_block,
+                                                               float* __restrict__ partials) {
   extern __shared__ float s_part[];  // [kSeluThreads / (H/4)][H]
   const float kL = 1.0507009873554805f, kLA = 1.0507009873554805f * 1.6732632423543772f;
   const int q = H >> 2;                       // float4 per row
   const int c4 = threadIdx.x % q, rlane = threadIdx.x / q, rpar = kSeluThreads / q;
-  const long long r0 = (long long)blockIdx.x * kSeluRowsPerBlock;
-  const long long r1 = min(rows, r0 + kSeluRowsPerBlock);
+  const long long r0 = (long long)blockIdx.x * rows_per_block;
+  const long long r1 = min(rows, r0 + rows_per_block);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (rlane < rpar) {
+#pragma unroll 4
     for (long long r = r0 + rlane; r < r1; r += rpar) {
       float4* gp = reinterpret_cast<float4*>(g + r * H) + c4;
-      const float4 yv = reinterpret_cast<const float4*>(y + r * H)[c4];
+      const float4 yv = __ldcs(reinterpret_cast<const float4*>(y + r * H) + c4);
       float4 d = *gp;
       d.x *= yv.x > 0.f ? kL : yv.x + kLA;
       d.y *= yv.y > 0.f ? kL : yv.y + kLA;
@@ -256,8 +294,8 @@ __global__ void __launch_bounds__(kSeluThreads) k_selu_bwd_bias(float* __restric
       acc.z += d.z;
       acc.w += d.w;
     }
+    reinterpret_cast<float4*>(s_part + rlane * H)[c4] = acc;
   }
-  if (rlane < rpar) reinterpret_cast<float4*>(s_part + rlane * H)[c4] = acc;
   __syncthreads();
   for (int c = threadIdx.x; c < H; c += kSeluThreads) {
     float s = 0.f;
@@ -266,12 +304,24 @@ __global__ void __launch_bounds__(kSeluThreads) k_selu_bwd_bias(float* __restric
   }
 }
 
-__global__ void k_colsum_finish(const float* __restrict__ partials, int nblk, int H, float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= H) return;
+// Column sums of partials [nblk][H]: a block per 32 columns, warp w adds
+// the rows b = w, w + 8, ... in order, then the 8 warp sums in order
+// (coalesced, deterministic).
+__global__ void __launch_bounds__(256) k_colsum_finish(const float* __restrict__ partials, int nblk, int H,
+                                                       float* __restrict__ out) {
+  __shared__ float s_w[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int b = 0; b < nblk; ++b) s += partials[(long long)b * H + c];
-  out[c] = s;
+  if (c < H)
+    for (int b = w; b < nblk; b += 8) s += partials[(long long)b * H + c];
+  s_w[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < H) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += s_w[k][lane];
+    out[c] = t;
+  }
 }
 
 // Forward epilogue of a learner layer: z += bias (+ SELU) in place over the
@@ -320,15 +370,16 @@ extern "C" int stp_selu_backward_bias(float* grad, const float* out, int64_t row
       (reinterpret_cast<uintptr_t>(out) & 15))
     return stp::fail(STP_EINVAL, "stp_selu_backward_bias: bad arguments");
   const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int nblk = int((rows + kSeluRowsPerBlock - 1) / kSeluRowsPerBlock);
-  const int rpar = kSeluThreads / (H / 4);
-  if (nblk > 0)
-    k_selu_bwd_bias<<<nblk, kSeluThreads, size_t(rpar > 0 ? rpar : 1) * H * sizeof(float), st>>>(grad, out, rows, H,
-                                                                                                 scratch);
-  if (nblk == 0) {
-    cudaMemsetAsync(d_bias, 0, size_t(H) * sizeof(float), st);
+  const int rpar = kSeluThreads / (H / 4) > 0 ? kSeluThreads / (H / 4) : 1;
+  // rows per block: a multiple of the rows in flight, at most kSeluBlocks blocks
+  long long rpb = (rows + kSeluBlocks - 1) / kSeluBlocks;
+  rpb = (rpb + rpar - 1) / rpar * rpar;
+  const int nblk = rows > 0 ? int((rows + rpb - 1) / rpb) : 0;
+  if (nblk > 0) {
+    k_selu_bwd_bias<<<nblk, kSeluThreads, size_t(rpar) * H * sizeof(float), st>>>(grad, out, rows, H, rpb, scratch);
+    k_colsum_finish<<<(H + 31) / 32, 256, 0, st>>>(scratch, nblk, H, d_bias);
   } else {
-    k_colsum_finish<<<(H + 127) / 128, 128, 0, st>>>(scratch, nblk, H, d_bias);
+    cudaMemsetAsync(d_bias, 0, size_t(H) * sizeof(float), st);
   }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_selu_bwd_bias: ") + cudaGetErrorString(e));
@@ -348,8 +399,8 @@ extern "C" int stp_ppo_surrogate(const float* mu, const float* log_std, const fl
   if (nblk > 0)
     k_ppo_head<<<nblk, kPpoThreads, 0, st>>>(mu, log_std, value, actions, old_logp, advantages, returns, idx, B, A,
                                              adv_stats, clip, vf_coef, d_mu, d_value, scratch);
-  k_ppo_finish<<<1, 128, 0, st>>>(scratch, nblk, A, B > 0 ? B : 1, vf_coef, d_log_std, d_mu_bias, d_value_bias,
-                                  loss, bad);
+  k_ppo_finish<<<2 * A + 2, 256, 0, st>>>(scratch, nblk, A, B > 0 ? B : 1, vf_coef, d_log_std, d_mu_bias,
+                                          d_value_bias, loss, bad);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_ppo_head: ") + cudaGetErrorString(e));
   return STP_OK;

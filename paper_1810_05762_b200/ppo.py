@@ -155,7 +155,7 @@ def surrogate_grad(mu, log_std, v, actions, old_logp, adv, ret, idx, adv_stats, 
     dmu, dv = torch.empty_like(mu), torch.empty_like(v)
     dls = torch.empty(A, dtype=torch.float32, device=dev)
     loss = torch.empty(3, dtype=torch.float32, device=dev)
-    scratch = torch.empty(max(1, (mb + 255) // 256) * (2 * A + 3), dtype=torch.float64, device=dev)
+    scratch = torch.empty(max(1, (mb + 127) // 128) * (2 * A + 3), dtype=torch.float64, device=dev)
     p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
     h = torch.cuda.current_stream(dev).cuda_stream
     rc = abi.load().stp_ppo_surrogate(p(mu), p(log_std), p(v), p(actions), p(old_logp), p(adv), p(ret), p(idx), mb,
@@ -267,7 +267,7 @@ class PPOLearner:
         n_mb = max(1, cfg.frames_per_iter // max(1, cfg.minibatch_per_agent))
         mb = max(1, B // n_mb)
         if fused:
-            scratch = torch.empty(((mb + 511) // 512) * max(self.model.hidden), dtype=torch.float32,
+            scratch = torch.empty(592 * max(self.model.hidden), dtype=torch.float32,
                                   device=xw.device)
         lr = self.opt.param_groups[0]["lr"]
         loss = torch.zeros((), device=xw.device)

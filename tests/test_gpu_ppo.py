@@ -267,7 +267,7 @@ def test_selu_backward_bias_kernel(rows, H):
     ref = torch.where(y > 0, dy * 1.0507009873554805, dy * (y + 1.0507009873554805 * 1.6732632423543772))
     gx = dy.clone()
     db = torch.full((H,), float("nan"), device="cuda")
-    scratch = torch.empty(max(1, (rows + 511) // 512) * H, device="cuda")
+    scratch = torch.empty(592 * H, device="cuda")
     rc = abi.load().stp_selu_backward_bias(C.c_void_p(gx.data_ptr()), C.c_void_p(y.data_ptr()), rows, H,
                                            C.c_void_p(db.data_ptr()), C.c_void_p(scratch.data_ptr()), C.c_void_p(1))
     assert rc == 0
@@ -313,7 +313,7 @@ def test_explicit_learner_backward_matches_autograd():
                                         stats, 0.2, 0.5, bad, d_mu_bias=pi_l[-1].bias.grad,
                                         d_value_bias=v_l[-1].bias.grad)
     model.log_std.grad.copy_(dls)
-    scratch = torch.empty(((mb + 511) // 512) * 256, device="cuda")
+    scratch = torch.empty(592 * 256, device="cuda")
     mlp_backward(pi_l, a_pi, dmu, scratch)
     mlp_backward(v_l, a_v, dv.view(-1, 1), scratch)
     torch.cuda.synchronize()
