@@ -21,6 +21,7 @@ from __future__ import annotations
 import copy
 import dataclasses
 import math
+import os
 
 import torch
 import torch.distributed as dist
@@ -213,6 +214,80 @@ def gae(rewards, values, dones, last_value, gamma, lam, stats: torch.Tensor | No
     return adv, adv + values
 
 
+class _MinibatchStep:
+    """The GPU minibatch gradient of ppo_update: gather the minibatch's
+    observations, both MLPs' explicit forward, the loss head with its output
+    gradients (stp_ppo_surrogate, the rollout columns read through idx), both
+    explicit backwards — every parameter's .grad written in place.  It reads
+    only static buffers (the update's rollout columns are copied in once per
+    update), so it is captured as one CUDA graph per shape and replayed per
+    minibatch (~40 launches -> one graph launch; STP_LEARNER_GRAPH=0 runs it
+    eagerly)."""
+
+    def __init__(self, model: ActorCritic, cfg: PPOConfig, B: int, mb: int, O: int, A: int, dev):
+        self.model, self.cfg, self.mb = model, cfg, mb
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.xw = torch.empty(B, O, **f32)
+        self.act = torch.empty(B, A, **f32)
+        self.old = torch.empty(B, **f32)
+        self.adv = torch.empty(B, **f32)
+        self.ret = torch.empty(B, **f32)
+        self.stats = torch.empty(3, dtype=torch.float64, device=dev)
+        self.idx = torch.empty(mb, dtype=torch.int64, device=dev)
+        self.bad = torch.zeros((), **f32)
+        self.scratch = torch.empty(592 * max(model.hidden), **f32)
+        self.graph, self.loss = None, None
+        self.use_graph = os.environ.get("STP_LEARNER_GRAPH", "1") != "0"
+        self.key = self._key()
+
+    def _key(self):
+        return (tuple(p.data_ptr() for p in self.model.parameters()),
+                tuple(p.grad.data_ptr() for p in self.model.parameters()), self.cfg.matmul, self.cfg.clip,
+                self.cfg.vf_coef)
+
+    def load(self, xw, act, old, adv, ret, stats):
+        self.xw.copy_(xw)
+        self.act.copy_(act)
+        self.old.copy_(old)
+        self.adv.copy_(adv)
+        self.ret.copy_(ret)
+        self.stats.copy_(stats)
+        self.bad.zero_()
+
+    def _body(self):
+        m, cfg = self.model, self.cfg
+        x = self.xw.index_select(0, self.idx)  # one gather of the minibatch's observations
+        pi_l, v_l = m.pi.layers, m.v.layers
+        a_pi, a_v = mlp_forward(pi_l, x), mlp_forward(v_l, x)
+        dmu, dv, dls, loss = surrogate_grad(a_pi[-1], m.log_std.detach(), a_v[-1].view(-1), self.act, self.old,
+                                            self.adv, self.ret, self.idx, self.stats, cfg.clip, cfg.vf_coef,
+                                            self.bad, d_mu_bias=pi_l[-1].bias.grad, d_value_bias=v_l[-1].bias.grad)
+        m.log_std.grad.copy_(dls)
+        mlp_backward(pi_l, a_pi, dmu, self.scratch)
+        mlp_backward(v_l, a_v, dv.view(-1, 1), self.scratch)
+        return loss
+
+    def run(self, idx):
+        self.idx.copy_(idx)
+        if not self.use_graph:
+            return self._body()
+        if self.graph is None:
+            # warm-up on a side stream (cuBLAS handles / workspaces), then capture;
+            # the warm-up computes this same minibatch, so its flag contribution
+            # is the replay's
+            side = torch.cuda.Stream(device=self.idx.device)
+            side.wait_stream(torch.cuda.current_stream(self.idx.device))
+            with torch.cuda.stream(side):
+                self._body()
+            torch.cuda.current_stream(self.idx.device).wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.loss = self._body()
+            self.graph = g
+        self.graph.replay()
+        return self.loss
+
+
 class PPOLearner:
     def __init__(self, model: ActorCritic, cfg: PPOConfig):
         self.model, self.cfg = model, cfg
@@ -220,7 +295,19 @@ class PPOLearner:
         # beta 0.9 / 0.999, eps 1e-8, bias correction)
         cuda = next(model.parameters()).is_cuda
         self.opt = torch.optim.Adam(model.parameters(), lr=cfg.lr, fused=cuda)
+        self._mbs = {}
         broadcast_params(model)
+
+    def _minibatch_step(self, B, mb, xw, actions, old_logp, adv, ret, stats):
+        """The (cached) captured minibatch step for this shape, loaded with this
+        update's rollout columns."""
+        key = (B, mb, xw.shape[1], actions.shape[1], xw.device)
+        st = self._mbs.get(key)
+        if st is None or st.key != st._key():
+            st = _MinibatchStep(self.model, self.cfg, B, mb, xw.shape[1], actions.shape[1], xw.device)
+            self._mbs = {key: st}  # one shape at a time: drop graphs of older shapes
+        st.load(xw, actions, old_logp, adv, ret, stats)
+        return st
 
     def update(self, xw, actions, old_logp=None, adv=None, ret=None, generator: torch.Generator | None = None,
                adv_stats: torch.Tensor | None = None):
@@ -266,12 +353,12 @@ class PPOLearner:
         # Table 4: frames per iteration / minibatch size per agent = minibatches per epoch
         n_mb = max(1, cfg.frames_per_iter // max(1, cfg.minibatch_per_agent))
         mb = max(1, B // n_mb)
-        if fused:
-            scratch = torch.empty(592 * max(self.model.hidden), dtype=torch.float32,
-                                  device=xw.device)
         lr = self.opt.param_groups[0]["lr"]
         loss = torch.zeros((), device=xw.device)
         bad = torch.zeros((), device=xw.device, dtype=torch.float32)  # 1 once any loss was not finite
+        if fused:
+            mbg = self._minibatch_step(B, mb, xw, actions, old_logp, adv_raw, ret, adv_stats_g)
+            bad = mbg.bad
         for epoch in range(cfg.epochs):
             if generator is None and xw.is_cuda:  # drawn on the device: no host round trip
                 perm = torch.randperm(B, device=xw.device)
@@ -279,25 +366,11 @@ class PPOLearner:
                 perm = torch.randperm(B, generator=generator, device="cpu").to(xw.device)
             for s0 in range(0, B, mb):
                 idx = perm[s0:s0 + mb]
-                x = xw.index_select(0, idx)  # one gather of the minibatch's observations
                 if not fused:
+                    x = xw.index_select(0, idx)
                     self.opt.zero_grad(set_to_none=False)
                 if fused:
-                    # explicit forward / backward: cuBLAS GEMMs, the loss head and
-                    # its output gradients in one kernel (stp_ppo_surrogate: the
-                    # rollout columns gathered through idx in-kernel, the heads'
-                    # bias gradients reduced alongside), each hidden SELU's backward
-                    # fused with its bias gradient (stp_selu_backward_bias);
-                    # every gradient written in place, nothing accumulated
-                    pi_l, v_l = self.model.pi.layers, self.model.v.layers
-                    a_pi, a_v = mlp_forward(pi_l, x), mlp_forward(v_l, x)
-                    dmu, dv, dls, loss = surrogate_grad(
-                        a_pi[-1], self.model.log_std.detach(), a_v[-1].view(-1), actions, old_logp, adv_raw, ret,
-                        idx, adv_stats_g, cfg.clip, cfg.vf_coef, bad,
-                        d_mu_bias=pi_l[-1].bias.grad, d_value_bias=v_l[-1].bias.grad)
-                    self.model.log_std.grad.copy_(dls)
-                    mlp_backward(pi_l, a_pi, dmu, scratch)
-                    mlp_backward(v_l, a_v, dv.view(-1, 1), scratch)
+                    loss = mbg.run(idx)
                 else:
                     logp = self.model.log_prob(x, actions[idx])
                     ratio = torch.exp(logp - old_logp[idx])

@@ -337,3 +337,35 @@ def test_bias_selu_kernel(rows, H, selu):
     assert rc == 0
     torch.cuda.synchronize()
     assert torch.allclose(out, ref, rtol=1e-6, atol=1e-7)
+
+
+def test_captured_minibatch_step_equals_eager(monkeypatch):
+    """The learner's minibatch step replayed from its CUDA graph gives the same
+    update as the eager launches (same kernels, same GEMM calls): parameters
+    after a 4-epoch, 2-minibatch update agree to 1e-6 of each tensor's scale,
+    and a second update (graph reused with new rollout columns) too."""
+    import copy as _copy
+    torch.manual_seed(3)
+    O, A, B = 77, 21, 4096
+    base = ActorCritic(O, A).cuda()
+    cfg = PPOConfig(frames_per_iter=8, epochs=4, minibatch_per_agent=4)
+    results = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("STP_LEARNER_GRAPH", flag)
+        model = _copy.deepcopy(base)
+        learner = PPOLearner(model, cfg)
+        stats = []
+        for it in range(2):
+            g = torch.Generator().manual_seed(10 + it)
+            xw = torch.randn(B, O, generator=g).cuda()
+            act = torch.randn(B, A, generator=g).cuda()
+            adv = torch.randn(B, generator=g).cuda()
+            ret = torch.randn(B, generator=g).cuda()
+            stats.append(learner.update(xw, act, None, adv, ret, generator=torch.Generator().manual_seed(it)))
+        assert isinstance(learner._mbs[next(iter(learner._mbs))].graph, torch.cuda.CUDAGraph) == (flag == "1")
+        results.append(([p.detach().clone() for p in model.parameters()], stats))
+    (pe, se), (pg, sg) = results
+    for a, b in zip(pe, pg):
+        assert (a - b).abs().max() <= 1e-6 * (a.abs().max() + 1e-12)
+    for a, b in zip(se, sg):
+        assert abs(a["kl"] - b["kl"]) <= 1e-5 * (abs(a["kl"]) + 1e-12) and a["lr"] == b["lr"]

@@ -21,7 +21,7 @@ env = VecEnv("humanoid", n_envs=4096, seed=1234)
 dev = torch.device("cuda:0")
 torch.manual_seed(0)
 model = ActorCritic(env.obs_dim, env.action_dim, HIDDEN["humanoid"]).to(dev)
-cfg = PPOConfig()
+cfg = PPOConfig(frames_per_iter=int(os.environ.get("FRAMES", "32")))
 learner = PPOLearner(model, cfg)
 kern = PolicyKernel(model, dev)
 st = RunningStat(env.obs_dim, device=dev)
