@@ -6,9 +6,10 @@ two MLPs' explicit forward / backward (cuBLAS GEMMs; each hidden SELU's
 backward fused with its bias gradient, stp_selu_backward_bias), the loss head
 and its output gradients in one CUDA kernel pair (stp_ppo_surrogate: log-prob,
 ratio, clipped surrogate on the globally normalised advantages, value MSE,
-the heads' bias gradients, the rollout columns gathered in-kernel), the fused
-Adam step; the GAE is a CUDA kernel (stp_gae).  Host (CPU) tensors — the gloo tests of the
-distributed logic — run the same loss under autograd.  Every minibatch
+the heads' bias gradients, the rollout columns gathered in-kernel) — all of
+it one CUDA graph replay — then the fused Adam step; the GAE is a CUDA kernel
+(stp_gae).  Host (CPU) tensors (the gloo tests of the distributed logic) run
+the same loss under autograd.  Every minibatch
 gradient is averaged across ranks with one allreduce of the flattened
 gradient (the paper's Horovod/NCCL gradient averaging, PAPER.md:240-241);
 advantages are normalised with global statistics; the
@@ -151,6 +152,9 @@ def surrogate_grad(mu, log_std, v, actions, old_logp, adv, ret, idx, adv_stats, 
     from . import abi
     mb, A = mu.shape
     dev = mu.device
+    for name, t in (("actions", actions), ("old_logp", old_logp), ("adv", adv), ("ret", ret)):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValueError(f"surrogate_grad: {name} must be a contiguous float32 CUDA tensor")
     mu, v, log_std = mu.contiguous(), v.contiguous(), log_std.to(torch.float32).contiguous()
     idx = idx.to(torch.int64).contiguous()
     dmu, dv = torch.empty_like(mu), torch.empty_like(v)
