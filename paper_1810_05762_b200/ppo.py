@@ -144,7 +144,8 @@ def surrogate_grad(mu, log_std, v, actions, old_logp, adv, ret, idx, adv_stats, 
                    d_mu_bias=None, d_value_bias=None):
     """The minibatch loss head of ppo_update on the GPU (stp_ppo_surrogate,
     SPEC.md:455-467): returns (dL/dmu [mb, A], dL/dV [mb], dL/dlog_std [A],
-    loss) for mu / v = the networks' outputs on the samples idx of the rollout
+    loss) for mu / v = the networks' outputs on the samples idx (None: rows
+    0 .. mb-1) of the rollout
     columns; advantages normalised in-kernel from `adv_stats`; `bad` (float
     device scalar) is set to 1 when the loss is not finite; the output layers'
     bias gradients are written to d_mu_bias [A] / d_value_bias [1] if given."""
@@ -156,7 +157,7 @@ def surrogate_grad(mu, log_std, v, actions, old_logp, adv, ret, idx, adv_stats, 
         if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
             raise ValueError(f"surrogate_grad: {name} must be a contiguous float32 CUDA tensor")
     mu, v, log_std = mu.contiguous(), v.contiguous(), log_std.to(torch.float32).contiguous()
-    idx = idx.to(torch.int64).contiguous()
+    idx = idx.to(torch.int64).contiguous() if idx is not None else None
     dmu, dv = torch.empty_like(mu), torch.empty_like(v)
     dls = torch.empty(A, dtype=torch.float32, device=dev)
     loss = torch.empty(3, dtype=torch.float32, device=dev)
@@ -237,6 +238,9 @@ class _MinibatchStep:
         self.adv = torch.empty(B, **f32)
         self.ret = torch.empty(B, **f32)
         self.stats = torch.empty(3, dtype=torch.float64, device=dev)
+        # one minibatch per epoch (the C5 config): the whole batch in row order —
+        # a permutation would change only the summation order of the gradient
+        self.full = mb == B
         self.idx = torch.empty(mb, dtype=torch.int64, device=dev)
         self.bad = torch.zeros((), **f32)
         self.scratch = torch.empty(592 * max(model.hidden), **f32)
@@ -260,11 +264,12 @@ class _MinibatchStep:
 
     def _body(self):
         m, cfg = self.model, self.cfg
-        x = self.xw.index_select(0, self.idx)  # one gather of the minibatch's observations
+        x = self.xw if self.full else self.xw.index_select(0, self.idx)  # the minibatch's observations
+        idx = None if self.full else self.idx
         pi_l, v_l = m.pi.layers, m.v.layers
         a_pi, a_v = mlp_forward(pi_l, x), mlp_forward(v_l, x)
         dmu, dv, dls, loss = surrogate_grad(a_pi[-1], m.log_std.detach(), a_v[-1].view(-1), self.act, self.old,
-                                            self.adv, self.ret, self.idx, self.stats, cfg.clip, cfg.vf_coef,
+                                            self.adv, self.ret, idx, self.stats, cfg.clip, cfg.vf_coef,
                                             self.bad, d_mu_bias=pi_l[-1].bias.grad, d_value_bias=v_l[-1].bias.grad)
         m.log_std.grad.copy_(dls)
         mlp_backward(pi_l, a_pi, dmu, self.scratch)
@@ -272,7 +277,8 @@ class _MinibatchStep:
         return loss
 
     def run(self, idx):
-        self.idx.copy_(idx)
+        if not self.full:
+            self.idx.copy_(idx)
         if not self.use_graph:
             return self._body()
         if self.graph is None:
@@ -364,12 +370,14 @@ class PPOLearner:
             mbg = self._minibatch_step(B, mb, xw, actions, old_logp, adv_raw, ret, adv_stats_g)
             bad = mbg.bad
         for epoch in range(cfg.epochs):
-            if generator is None and xw.is_cuda:  # drawn on the device: no host round trip
+            if fused and mbg.full:  # one minibatch = the whole batch: no permutation to draw
+                perm = None
+            elif generator is None and xw.is_cuda:  # drawn on the device: no host round trip
                 perm = torch.randperm(B, device=xw.device)
             else:  # an explicit (CPU) generator: reproducible permutations (tests)
                 perm = torch.randperm(B, generator=generator, device="cpu").to(xw.device)
             for s0 in range(0, B, mb):
-                idx = perm[s0:s0 + mb]
+                idx = perm[s0:s0 + mb] if perm is not None else None
                 if not fused:
                     x = xw.index_select(0, idx)
                     self.opt.zero_grad(set_to_none=False)

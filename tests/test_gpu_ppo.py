@@ -133,14 +133,15 @@ def _update_fp64(params, xw, act, adv, ret, cfg, perms):
 UPDATE_BOUNDS = {"fp32": (1e-3, 1e-3, 1e-3), "tf32": (0.3, 5e-2, 5e-3)}
 
 
-@pytest.mark.parametrize("matmul", ["fp32", "tf32"])
-def test_ppo_update_matches_fp64_restatement(matmul):
+@pytest.mark.parametrize("matmul,mb_per_agent", [("fp32", 16), ("tf32", 16), ("fp32", 32)])
+def test_ppo_update_matches_fp64_restatement(matmul, mb_per_agent):
+    """mb_per_agent 16: 2 shuffled minibatches per epoch; 32: one minibatch =
+    the whole batch (the C5 config), which the GPU learner takes in row order."""
     torch.manual_seed(0)
     O, A, B = 76, 21, 512
     model = ActorCritic(O, A).cuda()
     params0 = {k: v.detach().cpu().double() for k, v in model.named_parameters()}
-    cfg = PPOConfig(frames_per_iter=32, epochs=4, minibatch_per_agent=16, lr=3e-4,  # 2 minibatches per epoch
-                    matmul=matmul)
+    cfg = PPOConfig(frames_per_iter=32, epochs=4, minibatch_per_agent=mb_per_agent, lr=3e-4, matmul=matmul)
     g = torch.Generator().manual_seed(5)
     xw = torch.randn(B, O, generator=g).clamp(-10, 10)
     with torch.no_grad():
