@@ -336,6 +336,14 @@ int stp_ppo_surrogate(const float* mu, const float* log_std, const float* value,
                       float* d_value, float* d_log_std, float* d_mu_bias, float* d_value_bias, float* loss,
                       float* bad, double* scratch, void* stream);
 
+/* KL(old || new) of the diagonal Gaussian policies (kl_diag_gaussian,
+ * SPEC.md:428-436) averaged over B states: mu_old / mu_new [B][A], log-stds
+ * [A]; *kl_mean (device float) = mean_i sum_j (ls1 - ls0 + (s0^2 + (mu0 -
+ * mu1)^2) / (2 s1^2) - 1/2), the input of the learning-rate rule (:468-475).
+ * scratch: double[ceil(B / 256)].  Deterministic; asynchronous on `stream`. */
+int stp_ppo_kl(const float* mu_old, const float* log_std_old, const float* mu_new, const float* log_std_new,
+               int32_t B, int32_t A, float* kl_mean, double* scratch, void* stream);
+
 /* Backward of a hidden layer's SELU in the PPO learner: grad [rows][H]
  * (dL/d the layer's output, overwritten with dL/d its pre-activation, using
  * the output `out` [rows][H]: selu'(z) = lambda for out > 0, else

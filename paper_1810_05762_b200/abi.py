@@ -179,6 +179,7 @@ SIGNATURES = [
                                _P, _P, _P, _P, _P, _P]),
     ("stp_selu_backward_bias", _I, [_P, _P, C.c_int64, _I32, _P, _P, _P]),
     ("stp_bias_selu", _I, [_P, _P, C.c_int64, _I32, _I32, _P]),
+    ("stp_ppo_kl", _I, [_P, _P, _P, _P, _I32, _I32, _P, _P, _P]),
     ("stp_debug_first_system", _I, [_P, _I32, _P, _P, _P, _P, _P]),
     ("stp_debug_math", _I, [_I32, _P, _P, _P, _P, C.c_int64, _P]),
 ]

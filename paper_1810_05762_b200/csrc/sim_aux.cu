@@ -258,6 +258,44 @@ __global__ void __launch_bounds__(256) k_ppo_finish(const double* __restrict__ p
   }
 }
 
+// KL(old || new) of the diagonal Gaussian policies averaged over the batch
+// (kl_diag_gaussian; the learning-rate rule's input,
+// :468-475): one thread per state, per-block double sums, then a fixed-order
+// sum in k_kl_finish (deterministic).
+constexpr int kKlThreads = 256;
+
+__global__ void __launch_bounds__(kKlThreads) k_kl(const float* __restrict__ mu0, const float* __restrict__ ls0,
+                                                   const float* __restrict__ mu1, const float* __restrict__ ls1,
+                                                   int B, int A, double* __restrict__ partials) {
+  __shared__ double s_w[kKlThreads / 32];
+  const int i = blockIdx.x * kKlThreads + threadIdx.x;
+  double kl = 0.0;
+  if (i < B) {
+    float acc = 0.f;
+    for (int j = 0; j < A; ++j) {
+      const float v0 = expf(2.f * ls0[j]), v1 = expf(2.f * ls1[j]);
+      const float d = mu0[(long long)i * A + j] - mu1[(long long)i * A + j];
+      acc += ls1[j] - ls0[j] + (v0 + d * d) / (2.f * v1) - 0.5f;
+    }
+    kl = double(acc);
+  }
+  for (int off = 16; off > 0; off >>= 1) kl += __shfl_xor_sync(0xffffffffu, kl, off);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = kl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kKlThreads / 32; ++w) t += s_w[w];
+    partials[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_kl_finish(const double* __restrict__ partials, int nblk, int B,
+                                                   float* __restrict__ out) {
+  __shared__ double s_tree[256];
+  const double s = colsum_fixed(partials, nblk, 1, 0, s_tree);
+  if (threadIdx.x == 0) *out = float(s / B);
+}
+
 // Backward of one hidden layer's SELU for the learner (§4.4 SELU
 // networks): g = dy * selu'(z) from the layer's OUTPUT y (y > 0: lambda;
 // else y + lambda alpha = lambda alpha e^z, autograd's result form), written
@@ -360,6 +398,20 @@ extern "C" int stp_bias_selu(float* z, const float* bias, int64_t rows, int32_t 
   k_bias_selu<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(z, bias, n4, H / 4, selu);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_bias_selu: ") + cudaGetErrorString(e));
+  return STP_OK;
+}
+
+extern "C" int stp_ppo_kl(const float* mu_old, const float* log_std_old, const float* mu_new,
+                          const float* log_std_new, int32_t B, int32_t A, float* kl_mean, double* scratch,
+                          void* stream) {
+  if (B <= 0 || A <= 0 || !mu_old || !log_std_old || !mu_new || !log_std_new || !kl_mean || !scratch)
+    return stp::fail(STP_EINVAL, "stp_ppo_kl: bad arguments");
+  const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nblk = (B + kKlThreads - 1) / kKlThreads;
+  k_kl<<<nblk, kKlThreads, 0, st>>>(mu_old, log_std_old, mu_new, log_std_new, B, A, scratch);
+  k_kl_finish<<<1, 256, 0, st>>>(scratch, nblk, B, kl_mean);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return stp::fail(STP_ECUDA, std::string("k_kl: ") + cudaGetErrorString(e));
   return STP_OK;
 }
 

@@ -407,7 +407,10 @@ class PPOLearner:
                 g["lr"] = lr
             return {"kl": 0.0, "lr": lr, "loss": float("nan"), "aborted": True}
         with torch.no_grad():
-            kl = gaussian_kl(mu_old, ls_old, self.model.pi(xw), self.model.log_std).mean()
+            if fused:
+                kl = policy_kl(mu_old, ls_old, self.model.pi(xw), self.model.log_std.detach())
+            else:
+                kl = gaussian_kl(mu_old, ls_old, self.model.pi(xw), self.model.log_std).mean()
             if _dist():
                 dist.all_reduce(kl, op=dist.ReduceOp.SUM)
                 kl /= dist.get_world_size()
@@ -430,6 +433,24 @@ def adapt_learning_rate(lr: float, measured_kl: float, desired_kl: float) -> flo
 def gaussian_logp(actions, mu, log_std):
     """log N(actions; mu, exp(log_std)^2) summed over action dims."""
     return (-0.5 * ((actions - mu) / torch.exp(log_std)) ** 2 - log_std - 0.5 * math.log(2 * math.pi)).sum(-1)
+
+
+def policy_kl(mu0, ls0, mu1, ls1) -> torch.Tensor:
+    """Mean KL(old || new) over the batch on the GPU (stp_ppo_kl; a device
+    scalar, deterministic)."""
+    import ctypes as C
+    from . import abi
+    B, A = mu0.shape
+    dev = mu0.device
+    t = [x.to(torch.float32).contiguous() for x in (mu0, ls0, mu1, ls1)]
+    out = torch.empty((), dtype=torch.float32, device=dev)
+    scratch = torch.empty(max(1, (B + 255) // 256), dtype=torch.float64, device=dev)
+    h = torch.cuda.current_stream(dev).cuda_stream
+    rc = abi.load().stp_ppo_kl(*[C.c_void_p(x.data_ptr()) for x in t], B, A, C.c_void_p(out.data_ptr()),
+                               C.c_void_p(scratch.data_ptr()), C.c_void_p(h if h else 1))
+    if rc != abi.STP_OK:
+        raise RuntimeError(f"stp_ppo_kl failed ({rc}): {abi.last_error()}")
+    return out
 
 
 def gaussian_kl(mu0, ls0, mu1, ls1):

@@ -370,3 +370,16 @@ def test_captured_minibatch_step_equals_eager(monkeypatch):
         assert (a - b).abs().max() <= 1e-6 * (a.abs().max() + 1e-12)
     for a, b in zip(se, sg):
         assert abs(a["kl"] - b["kl"]) <= 1e-5 * (abs(a["kl"]) + 1e-12) and a["lr"] == b["lr"]
+
+
+@pytest.mark.parametrize("B,A", [(4096, 21), (300, 8), (1, 3)])
+def test_ppo_kl_kernel(B, A):
+    """stp_ppo_kl against the fp64 KL of diagonal Gaussians: 1e-5 relative."""
+    from paper_1810_05762_b200.ppo import gaussian_kl, policy_kl
+    g = torch.Generator().manual_seed(B + A)
+    mu0, mu1 = torch.randn(B, A, generator=g), torch.randn(B, A, generator=g) * 0.1
+    mu1 = mu0 + mu1
+    ls0, ls1 = torch.randn(A, generator=g) * 0.2 - 0.5, torch.randn(A, generator=g) * 0.2 - 0.5
+    ref = float(gaussian_kl(mu0.double(), ls0.double(), mu1.double(), ls1.double()).mean())
+    got = float(policy_kl(mu0.cuda(), ls0.cuda(), mu1.cuda(), ls1.cuda()))
+    assert abs(got - ref) <= 1e-5 * abs(ref) + 1e-7
