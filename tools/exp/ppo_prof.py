@@ -49,6 +49,7 @@ ts = []
 for it in range(2, 6):
     ts.append(one(it)[0])
 print("update s median", sorted(ts)[len(ts) // 2], flush=True)
+print("graphs", {str(k): v.captures for k, v in learner._mbs.items()}, flush=True)
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     one(6)
 print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=18))
